@@ -1,0 +1,24 @@
+# Build the in-tree C-ABI extension for sm_100a (B200).  `make` is what
+# __graft_entry__.build() runs; the .so lands next to the Python package.
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Ipaper_2412_06198_b200/csrc \
+           --expt-relaxed-constexpr -Xptxas -v
+SRC := $(wildcard paper_2412_06198_b200/csrc/*.cu)
+HDR := $(wildcard paper_2412_06198_b200/csrc/*.cuh paper_2412_06198_b200/csrc/*.h include/*.h)
+OBJ := $(patsubst paper_2412_06198_b200/csrc/%.cu,build/%.o,$(SRC))
+LIB := paper_2412_06198_b200/_sa_b200.so
+
+all: $(LIB)
+
+build/%.o: paper_2412_06198_b200/csrc/%.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; false)
+
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart_static
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all clean

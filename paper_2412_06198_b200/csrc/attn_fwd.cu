@@ -1,0 +1,376 @@
+// attn_fwd.cu — tile-sparse causal FlashAttention forward for sm_100a.
+//
+// One kernel serves the three pattern families of the reference
+// (patterns.py:353-435 vertical_slash_attention, which also runs the
+// Triangular index per patterns.py:262-276/495-497, and patterns.py:438-484
+// block_sparse_attention) plus the dense reference (core.py:138-154):
+// the index is turned into a per-(head, query-tile) list of 128-key tiles,
+// each tagged with a mask kind (sa_types.h), and the kernel evaluates logits
+// only on listed tiles.  Inside a tile, positions outside the index get -inf
+// before the row softmax, which reproduces "weights off the index are
+// exactly 0" (patterns.py:353-435 docstring) and the column-wins dedupe
+// (a position is one element of the union, evaluated once).
+//
+// Per CTA: one (head, 128-row query tile).  192 threads:
+//   warps 0-3  softmax: thread r owns query row r (TMEM lane r)
+//   warp  4    TMA producer: Q once, then K_j / V_j into two 32 KB slots
+//   warp  5    TMEM allocator + single-thread tcgen05.mma issuer
+// TMEM (256 columns): S = Q K^T fp32 at col 0 (P = bf16(softmax) aliased
+// over cols 0..63), O accumulator at col 128.  Two CTAs co-reside per SM
+// (96 KB smem, 256 TMEM columns each), so one CTA's softmax overlaps the
+// other CTA's MMAs.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "sa_types.h"
+#include "sm100_common.cuh"
+
+namespace sa {
+
+struct AttnArgs {
+  CUtensorMap tmap_q;  // [HH, n, 128] bf16, box {64, 128, 1}, SW128
+  CUtensorMap tmap_k;  // [HK, n, 128]
+  CUtensorMap tmap_v;  // [HK, n, 128]
+  __nv_bfloat16* out;
+  long long out_batch_stride;  // elements between batches
+  long long out_row_stride;    // elements between rows (H * 128 for (B, L, H*d))
+  int n;
+  int heads;     // query heads per batch
+  int kv_heads;  // key/value heads per batch
+  int nqt;       // query tiles = ceil(n / 128)
+  int hh_total;  // batch * heads
+  float scale_log2;
+  const int32_t* tile_off;  // [hh_total * nqt]
+  const int32_t* tile_cnt;  // [hh_total * nqt]
+  const uint32_t* tiles;
+  const int32_t* work;  // optional CTA -> (hh * nqt + qt) order; null = heavy-first default
+  HeadIndexView idx;
+  float* lse;  // optional [hh_total, n] natural-log row log-sum-exp
+};
+
+constexpr int kThreads = 192;
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kColS = 0;
+constexpr uint32_t kColP = 0;
+constexpr uint32_t kColO = 128;
+constexpr int kSmemQ = 0;
+constexpr int kSmemK = 32768;
+constexpr int kSmemV = 65536;
+constexpr int kSmemBar = 98304;
+constexpr int kSmemBytes = kSmemBar + 128 + 1024;  // + barriers + alignment slack
+
+enum Bar { B_Q = 0, B_KF, B_KE, B_VF, B_VE, B_SF, B_PF, B_OF, B_NUM };
+
+__device__ __forceinline__ void build_row_mask(const AttnArgs& a, uint32_t kind, int hh, int i,
+                                               int j0, int qt, int kt, uint32_t (&m)[4]) {
+  m[0] = m[1] = m[2] = m[3] = 0u;
+  const int diag_c = i - j0;  // column (within tile) of the main diagonal
+  if (kind == TK_CAUSAL) {
+    mask_set_range(m, 0, diag_c + 1);
+    return;
+  }
+  if (kind == TK_BAND) {
+    const int w = a.idx.tri_window[hh];
+    const int s = a.idx.tri_sinks[hh];
+    mask_set_range(m, diag_c - w + 1, diag_c + 1);
+    mask_set_range(m, 0, min(s - j0, diag_c + 1));
+    return;
+  }
+  if (kind == TK_VS) {
+    const uint32_t* cb = a.idx.colbits + (size_t)hh * a.idx.vs_words + (j0 >> 5);
+    const uint32_t* dr = a.idx.diagrev + (size_t)hh * a.idx.vs_words;
+    // window bit c <=> diag[i - j0 - c] <=> diagrev bit (n + 127 - i + j0 + c)
+    const int p = a.n + 127 - i + j0;
+    const int w0 = p >> 5, sh = p & 31;
+    uint32_t d[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) d[k] = __ldg(dr + w0 + k);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m[k] = __ldg(cb + k) | __funnelshift_r(d[k], d[k + 1], sh);
+    if (diag_c >= 0 && diag_c < 128) m[diag_c >> 5] |= 1u << (diag_c & 31);  // forced diagonal
+    if (kt == qt) {  // causal cut on the diagonal tile
+      uint32_t c4[4] = {0u, 0u, 0u, 0u};
+      mask_set_range(c4, 0, diag_c + 1);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) m[k] &= c4[k];
+    }
+    return;
+  }
+  if (kind == TK_BLOCK) {
+    const int b = a.idx.blk_b[hh];
+    const int gq = i / b;
+    const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
+    int lo = ro[gq], hi = ro[gq + 1];
+    // first listed key block whose end lies past j0
+    int L = lo, R = hi;
+    while (L < R) {
+      int mid = (L + R) >> 1;
+      if ((a.idx.blk_idx[mid] + 1) * b > j0) R = mid; else L = mid + 1;
+    }
+    for (int k = L; k < hi; ++k) {
+      const int gk = a.idx.blk_idx[k];
+      if (gk * b >= j0 + 128) break;
+      mask_set_range(m, gk * b - j0, (gk + 1) * b - j0);
+    }
+    uint32_t c4[4] = {0u, 0u, 0u, 0u};
+    mask_set_range(c4, 0, diag_c + 1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m[k] &= c4[k];
+    return;
+  }
+  // TK_FULL never reaches here
+  m[0] = m[1] = m[2] = m[3] = 0xffffffffu;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem + kSmemQ;
+  uint8_t* sK = smem + kSmemK;
+  uint8_t* sV = smem + kSmemV;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + B_NUM);
+
+  const int warp = warp_id();
+  int item;
+  if (a.work != nullptr) {
+    item = a.work[blockIdx.x];
+  } else {  // heaviest query tiles (most causal key tiles) first
+    const int qt = a.nqt - 1 - blockIdx.x / a.hh_total;
+    item = (blockIdx.x % a.hh_total) * a.nqt + qt;
+  }
+  const int hh = item / a.nqt;
+  const int qt = item % a.nqt;
+  const int bidx = hh / a.heads;
+  const int h = hh % a.heads;
+  const int hkv = bidx * a.kv_heads + h / (a.heads / a.kv_heads);
+  const int cnt = a.tile_cnt[item];
+  const uint32_t* tl = a.tiles + a.tile_off[item];
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[B_Q], 1);
+    mbar_init(&bars[B_KF], 1);
+    mbar_init(&bars[B_KE], 1);
+    mbar_init(&bars[B_VF], 1);
+    mbar_init(&bars[B_VE], 1);
+    mbar_init(&bars[B_SF], 1);
+    mbar_init(&bars[B_PF], 128);
+    mbar_init(&bars[B_OF], 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_holder, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch(&a.tmap_q);
+      tma_prefetch(&a.tmap_k);
+      tma_prefetch(&a.tmap_v);
+      mbar_arrive_expect_tx(&bars[B_Q], 32768);
+      tma_load_3d(sQ, &a.tmap_q, &bars[B_Q], 0, qt * kTile, hh);
+      tma_load_3d(sQ + 16384, &a.tmap_q, &bars[B_Q], 64, qt * kTile, hh);
+      for (int j = 0; j < cnt; ++j) {
+        const int row = (int)tile_ktile(tl[j]) * kTile;
+        if (j > 0) mbar_wait(&bars[B_KE], (j - 1) & 1);
+        mbar_arrive_expect_tx(&bars[B_KF], 32768);
+        tma_load_3d(sK, &a.tmap_k, &bars[B_KF], 0, row, hkv);
+        tma_load_3d(sK + 16384, &a.tmap_k, &bars[B_KF], 64, row, hkv);
+        if (j > 0) mbar_wait(&bars[B_VE], (j - 1) & 1);
+        mbar_arrive_expect_tx(&bars[B_VF], 32768);
+        tma_load_3d(sV, &a.tmap_v, &bars[B_VF], 0, row, hkv);
+        tma_load_3d(sV + 16384, &a.tmap_v, &bars[B_VF], 64, row, hkv);
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
+      const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+      mbar_wait(&bars[B_Q], 0);
+      tc_fence_after();
+      for (int j = 0; j < cnt; ++j) {
+        mbar_wait(&bars[B_KF], j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tbase + kColS, sdesc_sw128(q_addr + off, 16, 1024),
+                 sdesc_sw128(k_addr + off, 16, 1024), idesc_qk, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&bars[B_KE]);
+        mma_commit(&bars[B_SF]);
+        mbar_wait(&bars[B_PF], j & 1);
+        tc_fence_after();
+        mbar_wait(&bars[B_VF], j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          mma_ts(tbase + kColO, tbase + kColP + kk * 8, sdesc_sw128(v_addr + kk * 2048, 16384, 1024),
+                 idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&bars[B_VE]);
+      }
+      mma_commit(&bars[B_OF]);
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps
+    const int r = threadIdx.x;  // 0..127
+    const int i = qt * kTile + r;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const float sl2 = a.scale_log2;
+    float m_used = -INFINITY;
+    float l = 0.f;
+    for (int j = 0; j < cnt; ++j) {
+      const uint32_t e = tl[j];
+      const uint32_t kind = tile_kind(e);
+      const int kt = (int)tile_ktile(e);
+      const int j0 = kt * kTile;
+      uint32_t msk[4];
+      if (kind != TK_FULL) build_row_mask(a, kind, hh, i, j0, qt, kt, msk);
+
+      mbar_wait(&bars[B_SF], j & 1);
+      tc_fence_after();
+      uint32_t s[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tbase + lane_off + kColS + 32 * c, s[c]);
+      tmem_ld_wait();
+      float mx = -INFINITY;
+      if (kind != TK_FULL) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (!((msk[c] >> t) & 1u)) s[c][t] = __float_as_uint(-INFINITY);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int t = 0; t < 32; ++t) mx = fmaxf(mx, __uint_as_float(s[c][t]));
+      const float mt = mx * sl2;
+      if (mt > m_used + 8.0f) {
+        const float alpha = fast_exp2(m_used - mt);  // 0 when m_used == -inf
+        l *= alpha;
+        if (j > 0) {
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tbase + lane_off + kColO + 32 * c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+            tmem_st32(tbase + lane_off + kColO + 32 * c, o);
+          }
+          tmem_st_wait();
+        }
+        m_used = mt;
+      }
+      const float moff = (m_used == -INFINITY) ? 0.f : m_used;
+      float rs0 = 0.f, rs1 = 0.f;
+      uint32_t p[2][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+          const float p0 = fast_exp2(fmaf(__uint_as_float(s[c][t]), sl2, -moff));
+          const float p1 = fast_exp2(fmaf(__uint_as_float(s[c][t + 1]), sl2, -moff));
+          rs0 += p0;
+          rs1 += p1;
+          p[c >> 1][(c & 1) * 16 + (t >> 1)] = pack_bf16(p0, p1);
+        }
+      l += rs0 + rs1;
+      tmem_st32(tbase + lane_off + kColP, p[0]);
+      tmem_st32(tbase + lane_off + kColP + 32, p[1]);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars[B_PF]);
+    }
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(&bars[B_OF], 0);
+    tc_fence_after();
+    const float inv = 1.0f / l;
+    const bool valid = i < a.n;
+    __nv_bfloat16* orow = a.out + (long long)bidx * a.out_batch_stride +
+                          (long long)i * a.out_row_stride + (long long)h * kHeadDim;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      tmem_ld32(tbase + lane_off + kColO + 32 * c, o);
+      tmem_ld_wait();
+      uint32_t pk[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        pk[t] = pack_bf16(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
+      if (valid) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+      }
+    }
+    if (valid && a.lse != nullptr) {
+      a.lse[(size_t)hh * a.n + i] = (m_used + log2f(l)) * 0.69314718055994531f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc(tbase, kTmemCols);
+}
+
+}  // namespace sa
+
+// ------------------------------------------------------------------ C ABI
+#include "api_common.h"
+
+extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float scale,
+                              const void* q, const void* k, const void* v, void* out,
+                              const sa_head_index* index, const int32_t* tile_off,
+                              const int32_t* tile_cnt, const uint32_t* tiles, float* lse,
+                              void* stream) {
+  using namespace sa;
+  if (batch < 1 || heads < 1 || kv_heads < 1 || n < 1)
+    return fail(SA_ERR_DIMENSION, "need batch, heads, kv_heads, n >= 1");
+  if (heads % kv_heads != 0)
+    return fail(SA_ERR_DIMENSION, "heads=%d not a multiple of kv_heads=%d", heads, kv_heads);
+  if (!(scale > 0.f) || !std::isfinite(scale))
+    return fail(SA_ERR_DIMENSION, "scale must be positive and finite");
+  if (!q || !k || !v || !out || !index || !tile_off || !tile_cnt || !tiles)
+    return fail(SA_ERR_DIMENSION, "null pointer argument");
+  AttnArgs a;
+  memset(&a, 0, sizeof(a));
+  int st;
+  if ((st = make_tmap_3d_bf16(&a.tmap_q, q, kHeadDim, n, batch * heads, kTile))) return st;
+  if ((st = make_tmap_3d_bf16(&a.tmap_k, k, kHeadDim, n, batch * kv_heads, kTile))) return st;
+  if ((st = make_tmap_3d_bf16(&a.tmap_v, v, kHeadDim, n, batch * kv_heads, kTile))) return st;
+  a.out = reinterpret_cast<__nv_bfloat16*>(out);
+  a.out_row_stride = (long long)heads * kHeadDim;
+  a.out_batch_stride = (long long)n * heads * kHeadDim;
+  a.n = n;
+  a.heads = heads;
+  a.kv_heads = kv_heads;
+  a.nqt = (n + kTile - 1) / kTile;
+  a.hh_total = batch * heads;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  a.tile_off = tile_off;
+  a.tile_cnt = tile_cnt;
+  a.tiles = tiles;
+  a.work = nullptr;
+  a.idx = *index;
+  a.lse = lse;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr_set = true;
+  }
+  const int grid = a.hh_total * a.nqt;
+  attn_fwd_kernel<<<grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  return check_launch("attn_fwd_kernel");
+}

@@ -1,0 +1,36 @@
+// sa_types.h — device-side data layout shared by the kernels of the prefill
+// sparse-attention path.
+#pragma once
+#include <cstdint>
+
+#include "sparseattn_b200.h"
+
+namespace sa {
+
+// Pattern families, in the reference's DEFAULT_FAMILIES order
+// (search.py:322): the selector's argmin index is the family id.
+enum Family : int32_t { FAM_TRI = 0, FAM_VS = 1, FAM_BLOCK = 2, FAM_DENSE = 3 };
+
+// Per-tile mask kinds (bits 28..31 of a tile-list entry).
+enum TileKind : uint32_t {
+  TK_FULL = 0,    // every (i, j) of the 128x128 tile is included
+  TK_CAUSAL = 1,  // j <= i
+  TK_BAND = 2,    // Triangular: (i - j < window || j < sinks) && j <= i
+  TK_VS = 3,      // column bitmap | diagonal bitmap | i == j, && j <= i
+  TK_BLOCK = 4,   // (i/b, j/b) in the block list of the row's query block, && j <= i
+};
+
+constexpr int kTile = 128;   // query rows and key rows per tile
+constexpr int kHeadDim = 128;
+
+__host__ __device__ inline uint32_t tile_entry(uint32_t ktile, uint32_t kind) {
+  return ktile | (kind << 28);
+}
+__host__ __device__ inline uint32_t tile_ktile(uint32_t e) { return e & 0x0FFFFFFFu; }
+__host__ __device__ inline uint32_t tile_kind(uint32_t e) { return e >> 28; }
+
+// The device-resident realised index (C ABI struct, include/sparseattn_b200.h).
+using HeadIndexView = sa_head_index;
+
+
+}  // namespace sa

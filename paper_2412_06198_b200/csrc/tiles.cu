@@ -1,0 +1,151 @@
+// tiles.cu — turn each head's realised index into the per-(head, query-tile)
+// list of 128-key tiles the attention kernel executes.
+//
+// A tile (qt, kt) is listed iff the index covers at least one causal position
+// inside it (so the executed work is exactly the tiles the index touches);
+// its kind says which mask the softmax applies (sa_types.h).  Semantics
+// follow the reference's SparseIndex field definitions (patterns.py:113-133):
+// columns (i >= j), diagonals (i - j = o), blocks (token causality inside),
+// always_diagonal (forced (i, i)).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sa_types.h"
+
+namespace sa {
+
+struct TileBuildArgs {
+  int n, nqt, hh_total;
+  HeadIndexView idx;
+  int32_t* tile_off;  // [hh_total * nqt]
+  int32_t* tile_cnt;  // [hh_total * nqt]
+  uint32_t* tiles;    // capacity hh_total * nqt * (nqt + 1) / 2
+  long long* work_cost;  // optional per (hh, qt): tile count (for scheduling / accounting)
+};
+
+__device__ __forceinline__ int popc_range(const uint32_t* bits, int lo, int hi) {
+  // number of set bits in [lo, hi), bits stored LSB-first in 32-bit words
+  if (hi <= lo) return 0;
+  int total = 0;
+  int w0 = lo >> 5, w1 = (hi - 1) >> 5;
+  for (int w = w0; w <= w1; ++w) {
+    uint32_t v = bits[w];
+    if (w == w0) v &= 0xffffffffu << (lo & 31);
+    if (w == w1) {
+      int top = (hi - 1) & 31;
+      v &= (top == 31) ? 0xffffffffu : ((2u << top) - 1u);
+    }
+    total += __popc(v);
+  }
+  return total;
+}
+
+// One warp per (hh, qt).  Lanes evaluate 32 candidate key tiles at a time and
+// compact the included ones in key order with a ballot prefix.
+__global__ void build_tiles_kernel(TileBuildArgs a) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= a.hh_total * a.nqt) return;
+  const int hh = gw / a.nqt;
+  const int qt = gw % a.nqt;
+  const int fam = a.idx.family[hh];
+  const long long base = (long long)hh * a.nqt * (a.nqt + 1) / 2 + (long long)qt * (qt + 1) / 2;
+  uint32_t* out = a.tiles + base;
+  const int i0 = qt * kTile;
+  const int i1 = i0 + kTile - 1;       // last row of the tile (may be padding)
+  const int i1v = min(i1, a.n - 1);    // last real row
+  int count = 0;
+
+  // Block family: mark touched key tiles in a per-warp bitmap first.
+  __shared__ uint32_t blk_mark_all[8][64];  // up to 2048 key tiles per warp (n <= 262144)
+  uint32_t* blk_mark = blk_mark_all[(threadIdx.x >> 5) & 7];
+  int b = 0;
+  if (fam == FAM_BLOCK) {
+    b = a.idx.blk_b[hh];
+    const int words = (a.nqt + 31) >> 5;
+    for (int w = lane; w < words; w += 32) blk_mark[w] = 0u;
+    __syncwarp();
+    const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
+    const int g0 = i0 / b, g1 = i1v / b;
+    for (int gq = g0; gq <= g1; ++gq) {
+      for (int k = ro[gq] + lane; k < ro[gq + 1]; k += 32) {
+        const int gk = a.idx.blk_idx[k];
+        const int t0 = (gk * b) / kTile;
+        const int t1 = min((gk + 1) * b - 1, a.n - 1) / kTile;
+        for (int t = t0; t <= t1 && t <= qt; ++t) atomicOr(&blk_mark[t >> 5], 1u << (t & 31));
+      }
+    }
+    __syncwarp();
+  }
+
+  for (int kt0 = 0; kt0 <= qt; kt0 += 32) {
+    const int kt = kt0 + lane;
+    bool inc = false;
+    uint32_t kind = TK_FULL;
+    if (kt <= qt) {
+      const int j0 = kt * kTile, j1 = j0 + kTile - 1;
+      if (fam == FAM_DENSE) {
+        inc = true;
+        kind = (kt < qt) ? TK_FULL : TK_CAUSAL;
+      } else if (fam == FAM_TRI) {
+        const int w = a.idx.tri_window[hh], s = a.idx.tri_sinks[hh];
+        const bool band = (j1 >= i0 - w + 1);  // j0 <= i1 holds for kt <= qt
+        const bool sink = (j0 < s);
+        inc = band || sink || kt == qt;
+        const bool full = (kt < qt) && ((i1 - j0 < w) || (j1 < s));
+        kind = full ? TK_FULL : TK_BAND;
+      } else if (fam == FAM_VS) {
+        const uint32_t* cb = a.idx.colbits + (size_t)hh * a.idx.vs_words;
+        const uint32_t* dr = a.idx.diagrev + (size_t)hh * a.idx.vs_words;
+        inc = (kt == qt) || popc_range(cb, j0, min(j1, a.n - 1) + 1) > 0;
+        if (!inc) {
+          // diagonal offsets touching the tile: [i0 - j1, i1v - j0] (clipped at 0)
+          const int olo = max(0, i0 - j1), ohi = i1v - j0;
+          // diagrev bit (n + 127 - o): offsets [olo, ohi] <-> bits [n+127-ohi, n+127-olo]
+          inc = popc_range(dr, a.n + 127 - ohi, a.n + 127 - olo + 1) > 0;
+        }
+        kind = TK_VS;
+      } else {  // FAM_BLOCK
+        inc = (kt == qt) || ((blk_mark[kt >> 5] >> (kt & 31)) & 1u);
+        if (b % kTile == 0) kind = (kt < qt) ? TK_FULL : TK_CAUSAL;
+        else kind = TK_BLOCK;
+      }
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, inc);
+    if (inc) out[count + __popc(bal & ((1u << lane) - 1u))] = tile_entry(kt, kind);
+    count += __popc(bal);
+  }
+  if (lane == 0) {
+    a.tile_off[gw] = (int32_t)base;
+    a.tile_cnt[gw] = count;
+    if (a.work_cost) a.work_cost[gw] = count;
+  }
+}
+
+}  // namespace sa
+
+// ------------------------------------------------------------------ C ABI
+#include "api_common.h"
+
+extern "C" int sa_build_tiles(const sa_head_index* index, int hh_total, int n, int32_t* tile_off,
+                              int32_t* tile_cnt, uint32_t* tiles, void* stream) {
+  using namespace sa;
+  if (hh_total < 1 || n < 1) return fail(SA_ERR_DIMENSION, "need hh_total, n >= 1");
+  if (n > 262144) return fail(SA_ERR_DIMENSION, "n=%d exceeds the 262144-token tile-map limit", n);
+  if (!index || !tile_off || !tile_cnt || !tiles) return fail(SA_ERR_DIMENSION, "null pointer");
+  TileBuildArgs a;
+  a.n = n;
+  a.nqt = (n + kTile - 1) / kTile;
+  a.hh_total = hh_total;
+  a.idx = *index;
+  a.tile_off = tile_off;
+  a.tile_cnt = tile_cnt;
+  a.tiles = tiles;
+  a.work_cost = nullptr;
+  const long long warps = (long long)hh_total * a.nqt;
+  const int threads = 256;
+  const int grid = (int)((warps * 32 + threads - 1) / threads);
+  build_tiles_kernel<<<grid, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  return check_launch("build_tiles_kernel");
+}
