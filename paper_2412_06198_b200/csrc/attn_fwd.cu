@@ -50,6 +50,7 @@ struct AttnArgs {
   const int32_t* work;  // optional CTA -> (hh * nqt + qt) order; null = heavy-first default
   HeadIndexView idx;
   float* lse;  // optional [hh_total, n] natural-log row log-sum-exp
+  volatile int* dbg;  // optional progress trace [grid * 8] (debug builds)
 };
 
 constexpr int kThreads = 192;
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       tma_load_3d(sQ + 16384, &a.tmap_q, &bars[B_Q], 64, qt * kTile, hh);
       for (int j = 0; j < cnt; ++j) {
         const int row = (int)tile_ktile(tl[j]) * kTile;
+        if (a.dbg) a.dbg[blockIdx.x * 8 + 0] = j + 1;
         if (j > 0) mbar_wait(&bars[B_KE], (j - 1) & 1);
         mbar_arrive_expect_tx(&bars[B_KF], 32768);
         tma_load_3d(sK, &a.tmap_k, &bars[B_KF], 0, row, hkv);
@@ -199,7 +201,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       mbar_wait(&bars[B_Q], 0);
       tc_fence_after();
       for (int j = 0; j < cnt; ++j) {
+        if (a.dbg) a.dbg[blockIdx.x * 8 + 1] = j + 1;
         mbar_wait(&bars[B_KF], j & 1);
+        if (a.dbg) a.dbg[blockIdx.x * 8 + 2] = j + 1;
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -210,8 +214,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         mma_commit(&bars[B_KE]);
         mma_commit(&bars[B_SF]);
         mbar_wait(&bars[B_PF], j & 1);
+        if (a.dbg) a.dbg[blockIdx.x * 8 + 3] = j + 1;
         tc_fence_after();
         mbar_wait(&bars[B_VF], j & 1);
+        if (a.dbg) a.dbg[blockIdx.x * 8 + 4] = j + 1;
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -238,7 +244,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       uint32_t msk[4];
       if (kind != TK_FULL) build_row_mask(a, kind, hh, i, j0, qt, kt, msk);
 
+      if (a.dbg && r == 0) a.dbg[blockIdx.x * 8 + 5] = j + 1;
       mbar_wait(&bars[B_SF], j & 1);
+      if (a.dbg && r == 0) a.dbg[blockIdx.x * 8 + 6] = j + 1;
       tc_fence_after();
       uint32_t s[4][32];
 #pragma unroll
@@ -257,8 +265,12 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 #pragma unroll
         for (int t = 0; t < 32; ++t) mx = fmaxf(mx, __uint_as_float(s[c][t]));
       const float mt = mx * sl2;
-      if (mt > m_used + 8.0f) {
-        const float alpha = fast_exp2(m_used - mt);  // 0 when m_used == -inf
+      // Lazy rescale: keep a stale max until the row max grows by > 2^8.  The
+      // decision is made per row but the TMEM round trip of O is warp-wide
+      // (tcgen05.ld/st are .sync.aligned), so rows that need no rescale use 1.
+      const bool need = mt > m_used + 8.0f;
+      if (__any_sync(0xffffffffu, need)) {
+        const float alpha = need ? fast_exp2(m_used - mt) : 1.0f;  // 0 when m_used == -inf
         l *= alpha;
         if (j > 0) {
 #pragma unroll 1
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
           }
           tmem_st_wait();
         }
-        m_used = mt;
+        if (need) m_used = mt;
       }
       const float moff = (m_used == -INFINITY) ? 0.f : m_used;
       float rs0 = 0.f, rs1 = 0.f;
@@ -330,6 +342,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 // ------------------------------------------------------------------ C ABI
 #include "api_common.h"
 
+static void* sa_attn_dbg_ptr = nullptr;
+
+extern "C" int sa_attn_debug_ptr(void* p) { sa_attn_dbg_ptr = p; return 0; }
+
 extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float scale,
                               const void* q, const void* k, const void* v, void* out,
                               const sa_head_index* index, const int32_t* tile_off,
@@ -365,6 +381,7 @@ extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float s
   a.work = nullptr;
   a.idx = *index;
   a.lse = lse;
+  a.dbg = reinterpret_cast<volatile int*>(sa_attn_dbg_ptr);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
