@@ -56,8 +56,107 @@ typedef struct {
   int32_t blk_row_stride;     /* >= ceil(n / b) + 1 for every block head          */
 } sa_head_index;
 
+/* A pattern: Triangular(window=p1, sinks=p2) | VerticalSlash(k_v=p1, k_s=p2) |
+ * BlockSparse(b=p1, k_b=p2) | dense (patterns.py:59-94). */
+typedef struct {
+  int32_t family; /* sa_family */
+  int32_t p1, p2;
+} sa_pattern;
+
+typedef enum { SA_MODE_DENSE = 0, SA_MODE_FIXED = 1, SA_MODE_AUTO = 2 } sa_prefill_mode;
+
+/* One layer of runtime.prefill (runtime.py:134-206).  `cand` are the
+ * refined candidates at window scale (search.py:236-241), `full` the same
+ * candidates rescaled to n (search.py:261-273); the host computes both (pure
+ * integer math) and the device picks one per head. */
+typedef struct {
+  int32_t batch, heads, kv_heads, n;
+  float scale;           /* 1/sqrt(d_head) of the caller's head dim         */
+  int32_t mode;          /* sa_prefill_mode                                  */
+  sa_pattern fixed;      /* SA_MODE_FIXED                                    */
+  int32_t q_est;         /* estimated-scoring rows (runtime.py:170)          */
+  int32_t cal;           /* SA_MODE_AUTO: calibration window (<= 64)         */
+  int32_t ncand;         /* SA_MODE_AUTO: 1..3                               */
+  sa_pattern cand[3];
+  sa_pattern full[3];
+  int32_t preselected;   /* SA_MODE_AUTO: 1 = the caller already wrote the
+                            per-head choice into view.choice (skip the selector) */
+} sa_prefill_desc;
+
+/* Device views into a prefill workspace (valid after sa_prefill). */
+typedef struct {
+  int32_t* choice;      /* [HH] chosen candidate (auto)                      */
+  int32_t* family;      /* [HH]                                              */
+  double* errors;       /* [HH, 3] window Frobenius errors (auto)            */
+  float* col_scores;    /* [HH, n] estimated column mass (VS heads)          */
+  float* diag_scores;   /* [HH, n] estimated diagonal mass (VS heads)        */
+  int32_t* col_idx;     /* [HH, col_ld] selected columns, ascending          */
+  int32_t* diag_idx;    /* [HH, diag_ld] selected diagonals, ascending       */
+  int32_t col_ld, diag_ld;
+  sa_head_index index;  /* the realised index of every head                  */
+  int64_t blk_head_stride;
+  int32_t* tile_off;
+  int32_t* tile_cnt;
+  uint32_t* tiles;
+  int32_t nqt;
+} sa_prefill_view;
+
 const char* sa_last_error(void);
 int sa_version(void);
+
+/* ---- the whole path: runtime.prefill (runtime.py:134-206) --------------- */
+size_t sa_prefill_workspace_size(const sa_prefill_desc* desc);
+int sa_prefill_views(const sa_prefill_desc* desc, void* ws, sa_prefill_view* view);
+int sa_prefill(const sa_prefill_desc* desc, const void* q, const void* k, const void* v,
+               void* out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- selector: search.select_pattern_windowed (search.py:276-319) -------- */
+/* Candidate arrays are HOST arrays of length ncand (refined at window scale).
+ * choice_out / family_out: [HH]; err_out: [HH, 3] float64 (nullable). */
+int sa_select_windowed(int batch, int heads, int kv_heads, int n, int cal, float scale,
+                       const void* q, const void* k, int ncand, const int32_t* cand_fam_host,
+                       const int32_t* cand_p1_host, const int32_t* cand_p2_host,
+                       int32_t* choice_out, int32_t* family_out, double* err_out, void* stream);
+
+/* ---- VS estimator: patterns.score_columns / score_diagonals
+ *      (patterns.py:165-228), rows [r_lo, r_hi) with r_hi - r_lo <= 128 ----- */
+size_t sa_score_tail_workspace(int batch, int heads, int n, int r_hi);
+int sa_score_tail(int batch, int heads, int kv_heads, int n, float scale, const void* q,
+                  const void* k, int r_lo, int r_hi, float* col_out, float* diag_out,
+                  int accumulate, const int32_t* gate, int gate_val, void* ws, size_t ws_bytes,
+                  void* stream);
+
+/* ---- stable top-k: patterns._top_k_stable (patterns.py:231-234) ---------- */
+/* Bit-exact given identical fp32 scores: k largest, ties to the lower index,
+ * output ascending.  Rows are independent. */
+int sa_topk_stable_f32(const float* scores, int rows, int n, long long ld, int k, int32_t* idx_out,
+                       long long out_ld, void* stream);
+/* Segmented variant: row r uses lens[r] scores and keeps ks[r]. */
+int sa_topk_stable_rows_f32(const float* scores, int rows, long long ld, const int32_t* lens,
+                            const int32_t* ks, int32_t* idx_out, long long out_ld,
+                            int32_t* count_out, void* stream);
+
+/* ---- Block estimator: patterns.block_mean / build_block_index
+ *      (patterns.py:279-321) ------------------------------------------------ */
+/* side 0 = query operand [hi|lo|hi], 1 = key operand [hi|hi|lo]; split_out is
+ * [groups, nb, 384] bf16, mean_out (nullable) [groups, nb, 128] fp32. */
+int sa_block_pool(int groups, int n, int b, int side, const void* x, void* split_out,
+                  float* mean_out, void* stream);
+size_t sa_block_select_workspace(int n, int b, int k_b);
+/* blk_idx: [HH, nb, k_b + 1] ascending rows padded with INT32_MAX;
+ * blk_row_off: [HH, nb + 1] absolute offsets. */
+int sa_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b, float scale,
+                    const void* qp, const void* kp, int32_t* blk_idx, int32_t* blk_row_off,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* Dense [n, n] fp32 weights of head hh under `index` (need_weights=True of
+ * patterns.py:422-434, 466-467; core.py:152), rows normalised by the lse that
+ * sa_attn_sparse returned.  n <= 16384. */
+int sa_attn_weights(int heads, int kv_heads, int n, int hh, float scale, const void* q,
+                    const void* k, const float* lse, const sa_head_index* index, float* w,
+                    void* stream);
+/* fp32 block_mean of an [n, d] matrix (patterns.py:279-287). */
+int sa_block_mean_f32(const float* x, int n, int d, int b, float* out, void* stream);
 
 /* ---- index -> executed tiles (patterns.py:113-158 field semantics) ------- */
 /* Replaces the per-head structural iteration of vertical_slash_attention /
@@ -68,6 +167,7 @@ int sa_build_tiles(const sa_head_index* index, int hh_total, int n, int32_t* til
 
 /* ---- sparse attention (patterns.py:487-497 sparse_attention, need_weights=False;
  *      core.py:138-154 dense_attention when family == SA_DENSE) ------------- */
+/* lse (nullable): [HH, n] natural-log row log-sum-exp of the realised logits. */
 int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float scale, const void* q,
                    const void* k, const void* v, void* out, const sa_head_index* index,
                    const int32_t* tile_off, const int32_t* tile_cnt, const uint32_t* tiles,

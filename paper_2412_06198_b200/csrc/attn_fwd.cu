@@ -92,7 +92,8 @@ __device__ __forceinline__ void build_row_mask(const AttnArgs& a, uint32_t kind,
     for (int k = 0; k < 5; ++k) d[k] = __ldg(dr + w0 + k);
 #pragma unroll
     for (int k = 0; k < 4; ++k) m[k] = __ldg(cb + k) | __funnelshift_r(d[k], d[k + 1], sh);
-    if (diag_c >= 0 && diag_c < 128) m[diag_c >> 5] |= 1u << (diag_c & 31);  // forced diagonal
+    if (diag_c >= 0 && diag_c < 128 && a.idx.family[hh] != FAM_VS_NOEYE)
+      m[diag_c >> 5] |= 1u << (diag_c & 31);  // forced diagonal (patterns.py:378)
     if (kt == qt) {  // causal cut on the diagonal tile
       uint32_t c4[4] = {0u, 0u, 0u, 0u};
       mask_set_range(c4, 0, diag_c + 1);
@@ -107,14 +108,17 @@ __device__ __forceinline__ void build_row_mask(const AttnArgs& a, uint32_t kind,
     const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
     int lo = ro[gq], hi = ro[gq + 1];
     // first listed key block whose end lies past j0
+    // rows are ascending key-block ids, possibly padded with INT32_MAX sentinels
+    const int gfirst = j0 / b;                // first block ending after j0
+    const int kend = (j0 + 128 + b - 1) / b;  // first block starting at/after j0 + 128
     int L = lo, R = hi;
     while (L < R) {
       int mid = (L + R) >> 1;
-      if ((a.idx.blk_idx[mid] + 1) * b > j0) R = mid; else L = mid + 1;
+      if (a.idx.blk_idx[mid] >= gfirst) R = mid; else L = mid + 1;
     }
     for (int k = L; k < hi; ++k) {
       const int gk = a.idx.blk_idx[k];
-      if (gk * b >= j0 + 128) break;
+      if (gk >= kend) break;
       mask_set_range(m, gk * b - j0, (gk + 1) * b - j0);
     }
     uint32_t c4[4] = {0u, 0u, 0u, 0u};
@@ -310,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     mbar_wait(&bars[B_OF], 0);
     tc_fence_after();
     const float inv = 1.0f / l;
-    const bool valid = i < a.n;
+    const bool valid = i < a.n && cnt > 0;  // cnt == 0: query tile not requested
     __nv_bfloat16* orow = a.out + (long long)bidx * a.out_batch_stride +
                           (long long)i * a.out_row_stride + (long long)h * kHeadDim;
 #pragma unroll 1

@@ -1,0 +1,457 @@
+// estimate_block.cu — the block-sparse (Block-Cluster) pattern estimator.
+//
+// Reference: patterns.py:279-287 (block_mean) and patterns.py:290-321
+// (build_block_index): pooled logits qb . kb^T * scale over block-causal
+// pairs, row softmax, per query block the top-min(k_b, gq+1) key blocks (ties
+// to the lower block id) plus the forced diagonal block.
+//
+// Softmax is strictly increasing within a row, so the top-k of the weights is
+// the top-k of the logits; the estimator therefore selects on logits and never
+// exponentiates (single GEMM pass, no row statistics).  Pooled means are fp32
+// (not bf16-representable), so the GEMM runs on tcgen05 with a split-bf16
+// operand: x = hi + lo (hi = bf16(x), lo = bf16(x - hi)), and
+//     qb . kb ~= [qhi | qlo | qhi] . [khi | khi | klo]   (K = 3 x 128)
+// which keeps ~16 mantissa bits per product (DESIGN.md §Block estimator).
+//
+// Epilogue modes: FUSED keeps a per-row top-K list in registers (K = k_b <= 8,
+// which covers the auto-selected Block(8, 1)); MATERIALIZE writes the masked
+// fp32 logits for a segmented stable top-k (topk.cu) when k_b is large.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "api_common.h"
+#include "internal.h"
+#include "sa_types.h"
+#include "sm100_common.cuh"
+
+namespace sa {
+
+constexpr int kSplitK = 384;  // 3 x 128 split-bf16 contraction
+
+// out: [G, nb, 384] bf16 split operand; mean_out (optional): [G, nb, 128] fp32
+__global__ void block_pool_kernel(const __nv_bfloat16* __restrict__ x, int G, int n, int b,
+                                  int side, __nv_bfloat16* __restrict__ out, float* mean_out,
+                                  const int32_t* gate, int gate_val) {
+  const int nb = (n + b - 1) / b;
+  const long long gid = (long long)blockIdx.x * blockDim.y + threadIdx.y;  // (g, block)
+  if (gid >= (long long)G * nb) return;
+  const int g = (int)(gid / nb), blk = (int)(gid % nb);
+  if (gate && gate[g] != gate_val) return;
+  const int d = threadIdx.x;  // 0..127
+  const int r0 = blk * b, r1 = min(n, r0 + b);
+  const __nv_bfloat16* src = x + ((long long)g * n + r0) * kHeadDim + d;
+  float acc = 0.f;
+  for (int r = r0; r < r1; ++r, src += kHeadDim) acc += __bfloat162float(*src);
+  const float mean = acc / (float)(r1 - r0);
+  const __nv_bfloat16 hi = __float2bfloat16_rn(mean);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(mean - __bfloat162float(hi));
+  __nv_bfloat16* o = out + ((long long)g * nb + blk) * kSplitK + d;
+  o[0] = hi;
+  o[128] = side == 0 ? lo : hi;
+  o[256] = side == 0 ? hi : lo;
+  if (mean_out) mean_out[((long long)g * nb + blk) * kHeadDim + d] = mean;
+}
+
+struct BlockScoreArgs {
+  CUtensorMap tmap_qp;  // [HH, nb, 384]
+  CUtensorMap tmap_kp;  // [HK, nb, 384]
+  int nb, heads, kv_heads, hh_total;
+  int nqt;  // ceil(nb / 128)
+  float scale;
+  int k_b;
+  int b;                 // block side (stored in the index)
+  // FUSED output: fixed-stride rows of (k_b + 1) slots, INT32_MAX padded
+  int32_t* blk_idx;      // per head at hh * head_stride: [nb, k_b + 1]
+  int32_t* blk_row_off;  // per head at hh * row_stride: [nb + 1] (absolute offsets into blk_idx)
+  long long head_stride;
+  int row_stride;
+  // MATERIALIZE output
+  float* logits;         // [HH_group, nb, nb] (row-major), indexed by hh - hh_base
+  int hh_base, hh_count;
+  const int32_t* gate;
+  int gate_val;
+};
+
+constexpr int kBsThreads = 192;
+constexpr int kBsSmemA = 0;        // 6 x 16 KB
+constexpr int kBsSmemB = 98304;    // 3 x 32 KB
+constexpr int kBsSmemBar = 196608;
+constexpr int kBsSmemBytes = kBsSmemBar + 256 + 1024;
+
+enum BBar { BB_A = 0, BB_KF0, BB_KF1, BB_KF2, BB_KE0, BB_KE1, BB_KE2, BB_SF0, BB_SF1, BB_SE0, BB_SE1, BB_NUM };
+
+template <int K, bool FUSED>
+__global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid_constant__ BlockScoreArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int hh = a.hh_base + blockIdx.y;
+  if (a.gate && a.gate[hh] != a.gate_val) return;
+  const int qt = a.nqt - 1 - blockIdx.x;  // heavy tiles first
+  const int cnt = qt + 1;                  // causal key tiles
+  uint8_t* sA = smem + kBsSmemA;
+  uint8_t* sB = smem + kBsSmemB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBsSmemBar);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + BB_NUM);
+  const int warp = warp_id();
+  const int bidx = hh / a.heads;
+  const int h = hh % a.heads;
+  const int hkv = bidx * a.kv_heads + h / (a.heads / a.kv_heads);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[BB_A], 1);
+    for (int s = 0; s < 3; ++s) {
+      mbar_init(&bars[BB_KF0 + s], 1);
+      mbar_init(&bars[BB_KE0 + s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars[BB_SF0 + s], 1);
+      mbar_init(&bars[BB_SE0 + s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_holder, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+
+  if (warp == 4) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(&bars[BB_A], 98304);
+      for (int c = 0; c < 6; ++c) tma_load_3d(sA + c * 16384, &a.tmap_qp, &bars[BB_A], 64 * c, qt * kTile, hh);
+      for (int j = 0; j < cnt; ++j) {
+        for (int c = 0; c < 3; ++c) {
+          if (j > 0) mbar_wait(&bars[BB_KE0 + c], (j - 1) & 1);
+          uint8_t* dst = sB + c * 32768;
+          mbar_arrive_expect_tx(&bars[BB_KF0 + c], 32768);
+          tma_load_3d(dst, &a.tmap_kp, &bars[BB_KF0 + c], 128 * c, j * kTile, hkv);
+          tma_load_3d(dst + 16384, &a.tmap_kp, &bars[BB_KF0 + c], 128 * c + 64, j * kTile, hkv);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, 128, 0, 0);
+      const uint32_t a_addr = smem_u32(sA);
+      mbar_wait(&bars[BB_A], 0);
+      for (int j = 0; j < cnt; ++j) {
+        const int buf = j & 1;
+        if (j >= 2) mbar_wait(&bars[BB_SE0 + buf], ((j >> 1) - 1) & 1);
+        for (int c = 0; c < 3; ++c) {
+          mbar_wait(&bars[BB_KF0 + c], j & 1);
+          tc_fence_after();
+          const uint32_t b_addr = smem_u32(sB + c * 32768);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const int ka = 8 * c + kk;  // global k-step over the 384-wide A
+            const uint32_t aoff = (ka >> 2) * 16384 + (ka & 3) * 32;
+            const uint32_t boff = (kk >> 2) * 16384 + (kk & 3) * 32;
+            mma_ss(tbase + buf * 128, sdesc_sw128(a_addr + aoff, 16, 1024),
+                   sdesc_sw128(b_addr + boff, 16, 1024), idesc, (c > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&bars[BB_KE0 + c]);
+        }
+        mma_commit(&bars[BB_SF0 + buf]);
+      }
+    }
+  } else {
+    const int t = threadIdx.x;
+    const int gq = qt * kTile + t;
+    const bool valid = gq < a.nb;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    float bv[K];
+    int bi[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      bv[q] = -INFINITY;
+      bi[q] = -1;
+    }
+    for (int j = 0; j < cnt; ++j) {
+      const int buf = j & 1;
+      mbar_wait(&bars[BB_SF0 + buf], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t s[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tbase + lane_off + buf * 128 + 32 * c, s[c]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&bars[BB_SE0 + buf]);
+      if (!valid) continue;
+      const int g0 = j * kTile;
+      const int lim = gq - g0;  // block-causal: gk <= gq
+      if (FUSED) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            const int cc = 32 * c + u;
+            if (cc <= lim) {
+              const float v = __uint_as_float(s[c][u]) * a.scale;
+              if (v > bv[K - 1]) {  // strictly greater: ties keep the lower id
+                int p = K - 1;
+#pragma unroll
+                for (int q = K - 1; q > 0; --q) {
+                  if (v > bv[q - 1]) {
+                    bv[q] = bv[q - 1];
+                    bi[q] = bi[q - 1];
+                    p = q - 1;
+                  }
+                }
+                bv[p] = v;
+                bi[p] = g0 + cc;
+              }
+            }
+          }
+      } else {
+        float* row = a.logits + ((size_t)(hh - a.hh_base) * a.nb + gq) * a.nb + g0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int u = 0; u < 32; u += 4) {
+            const int cc = 32 * c + u;
+            if (g0 + cc < a.nb) {
+              float4 v;
+              v.x = (cc + 0 <= lim) ? __uint_as_float(s[c][u + 0]) * a.scale : -INFINITY;
+              v.y = (cc + 1 <= lim) ? __uint_as_float(s[c][u + 1]) * a.scale : -INFINITY;
+              v.z = (cc + 2 <= lim) ? __uint_as_float(s[c][u + 2]) * a.scale : -INFINITY;
+              v.w = (cc + 3 <= lim) ? __uint_as_float(s[c][u + 3]) * a.scale : -INFINITY;
+              if (g0 + cc + 3 < a.nb) {
+                *reinterpret_cast<float4*>(row + cc) = v;
+              } else {
+                row[cc] = v.x;
+                if (g0 + cc + 1 < a.nb) row[cc + 1] = v.y;
+                if (g0 + cc + 2 < a.nb) row[cc + 2] = v.z;
+              }
+            }
+          }
+      }
+    }
+    if (FUSED && valid) {
+      // selected ids + forced diagonal block, ascending, INT32_MAX padded
+      int ids[K + 1];
+      int m = 0;
+      bool has_diag = false;
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        if (q < a.k_b && bi[q] >= 0) {
+          ids[m++] = bi[q];
+          has_diag |= (bi[q] == gq);
+        }
+      }
+      if (!has_diag) ids[m++] = gq;
+      // insertion sort (m <= K + 1 <= 9)
+      for (int x = 1; x < m; ++x) {
+        const int v = ids[x];
+        int y = x - 1;
+        while (y >= 0 && ids[y] > v) {
+          ids[y + 1] = ids[y];
+          --y;
+        }
+        ids[y + 1] = v;
+      }
+      const int stride = a.k_b + 1;
+      int32_t* dst = a.blk_idx + (size_t)hh * a.head_stride + (size_t)gq * stride;
+      for (int q = 0; q < stride; ++q) dst[q] = q < m ? ids[q] : INT_MAX;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc(tbase, 256);
+}
+
+__global__ void fixed_row_off_kernel(int32_t* row_off, int hh_total, int nb, int stride,
+                                     int row_stride, long long head_stride, const int32_t* gate,
+                                     int gate_val) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)hh_total * (nb + 1)) return;
+  const int hh = (int)(t / (nb + 1)), g = (int)(t % (nb + 1));
+  if (gate && gate[hh] != gate_val) return;
+  row_off[(long long)hh * row_stride + g] = (int32_t)(hh * head_stride + (long long)g * stride);
+}
+
+// MATERIALIZE: per row, fold the stable top-k output (ascending ids) and the
+// forced diagonal into the fixed-stride row.
+__global__ void merge_diag_kernel(const int32_t* topk, int k_b, int nb, int32_t* blk_idx,
+                                  long long head_stride, int hh_base, int hh_count,
+                                  const int32_t* gate, int gate_val) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)hh_count * nb) return;
+  const int hl = (int)(t / nb), gq = (int)(t % nb);
+  const int hh = hh_base + hl;
+  if (gate && gate[hh] != gate_val) return;
+  const int keff = min(k_b, gq + 1);
+  const int32_t* src = topk + t * (long long)k_b;
+  int32_t* dst = blk_idx + hh * head_stride + (long long)gq * (k_b + 1);
+  int w = 0;
+  bool placed = false;
+  for (int q = 0; q < keff; ++q) {
+    const int v = src[q];
+    if (!placed && gq < v) {
+      dst[w++] = gq;
+      placed = true;
+    }
+    if (v == gq) placed = true;
+    dst[w++] = v;
+  }
+  if (!placed) dst[w++] = gq;
+  for (; w < k_b + 1; ++w) dst[w] = INT_MAX;
+}
+
+}  // namespace sa
+
+// ------------------------------------------------------------------ C ABI
+#include "sparseattn_b200.h"
+
+namespace sa {
+__global__ void seg_lens_kernel(int32_t* lens, int32_t* ks, int rows, int nb, int k_b) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows) return;
+  const int gq = t % nb;
+  lens[t] = gq + 1;
+  ks[t] = min(k_b, gq + 1);
+}
+}  // namespace sa
+
+namespace sa {
+
+int launch_block_pool(int groups, int n, int b, int side, const void* x, void* split_out,
+                      float* mean_out, const int32_t* gate, int gate_val, cudaStream_t st) {
+  if (groups < 1 || n < 1) return fail(SA_ERR_DIMENSION, "bad pool shape");
+  if (b < 1 || b > n) return fail(SA_ERR_PATTERN_PARAM, "b must be in [1, %d], got %d", n, b);
+  const int nb = (n + b - 1) / b;
+  const long long items = (long long)groups * nb;
+  dim3 block(128, 2);
+  const long long grid = (items + 1) / 2;
+  block_pool_kernel<<<(unsigned)grid, block, 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), groups, n, b, side,
+      reinterpret_cast<__nv_bfloat16*>(split_out), mean_out, gate, gate_val);
+  return check_launch("block_pool_kernel");
+}
+
+size_t block_select_ws(int n, int b, int k_b) {
+  const int nb = (n + b - 1) / b;
+  if (k_b <= 8) return 256;
+  return (size_t)nb * nb * 4 + (size_t)nb * k_b * 4 + (size_t)nb * 8 + 1024;
+}
+
+int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b, float scale,
+                        const void* qp, const void* kp, int32_t* blk_idx, long long head_stride,
+                        int32_t* blk_row_off, int row_stride, const int32_t* gate, int gate_val,
+                        void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (batch < 1 || heads < 1 || kv_heads < 1 || heads % kv_heads)
+    return fail(SA_ERR_DIMENSION, "bad head layout");
+  if (b < 1 || b > n) return fail(SA_ERR_PATTERN_PARAM, "b must be in [1, %d], got %d", n, b);
+  const int nb = (n + b - 1) / b;
+  if (k_b < 1 || k_b > nb) return fail(SA_ERR_PATTERN_PARAM, "k_b must be in [1, %d], got %d", nb, k_b);
+  if (row_stride < nb + 1 || head_stride < (long long)nb * (k_b + 1))
+    return fail(SA_ERR_DIMENSION, "block index strides too small");
+  BlockScoreArgs a;
+  memset(&a, 0, sizeof(a));
+  int rc;
+  const int hh_total = batch * heads;
+  if ((rc = make_tmap_3d_bf16(&a.tmap_qp, qp, kSplitK, nb, hh_total, kTile))) return rc;
+  if ((rc = make_tmap_3d_bf16(&a.tmap_kp, kp, kSplitK, nb, batch * kv_heads, kTile))) return rc;
+  a.nb = nb;
+  a.heads = heads;
+  a.kv_heads = kv_heads;
+  a.hh_total = hh_total;
+  a.nqt = (nb + kTile - 1) / kTile;
+  a.scale = scale;
+  a.k_b = k_b;
+  a.b = b;
+  a.blk_idx = blk_idx;
+  a.blk_row_off = blk_row_off;
+  a.head_stride = head_stride;
+  a.row_stride = row_stride;
+  a.gate = gate;
+  a.gate_val = gate_val;
+  {
+    const long long tot = (long long)hh_total * (nb + 1);
+    fixed_row_off_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+        blk_row_off, hh_total, nb, k_b + 1, row_stride, head_stride, gate, gate_val);
+    if ((rc = check_launch("fixed_row_off_kernel"))) return rc;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(block_score_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);
+    cudaFuncSetAttribute(block_score_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);
+    cudaFuncSetAttribute(block_score_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);
+    cudaFuncSetAttribute(block_score_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);
+    cudaFuncSetAttribute(block_score_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);
+    attr = true;
+  }
+  if (k_b <= 8) {
+    a.hh_base = 0;
+    a.hh_count = hh_total;
+    dim3 grid(a.nqt, hh_total);
+    if (k_b == 1) block_score_kernel<1, true><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
+    else if (k_b == 2) block_score_kernel<2, true><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
+    else if (k_b <= 4) block_score_kernel<4, true><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
+    else block_score_kernel<8, true><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
+    return check_launch("block_score_kernel<fused>");
+  }
+  // MATERIALIZE, one head at a time through the workspace
+  const size_t need = block_select_ws(n, b, k_b);
+  if (!ws || ws_bytes < need) return fail(SA_ERR_DIMENSION, "block_select workspace too small");
+  char* p = reinterpret_cast<char*>(ws);
+  float* logits = reinterpret_cast<float*>(p);
+  p += (size_t)nb * nb * 4;
+  int32_t* topk = reinterpret_cast<int32_t*>(p);
+  p += (size_t)nb * k_b * 4;
+  int32_t* lens = reinterpret_cast<int32_t*>(p);
+  int32_t* ks = lens + nb;
+  seg_lens_kernel<<<(nb + 255) / 256, 256, 0, st>>>(lens, ks, nb, nb, k_b);
+  a.logits = logits;
+  a.hh_count = 1;
+  for (int hh = 0; hh < hh_total; ++hh) {
+    a.hh_base = hh;
+    dim3 grid(a.nqt, 1);
+    block_score_kernel<1, false><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
+    if ((rc = check_launch("block_score_kernel<materialize>"))) return rc;
+    TopkArgs t{};
+    t.scores = logits;
+    t.ld = nb;
+    t.rows = nb;
+    t.n = nb;
+    t.lens = lens;
+    t.ks = ks;
+    t.idx_out = topk;
+    t.out_ld = k_b;
+    t.gate = gate ? gate + hh : nullptr;
+    t.gate_div = nb;  // every row of this head maps to gate[hh]
+    t.gate_val = gate_val;
+    if ((rc = launch_topk(t, st))) return rc;
+    merge_diag_kernel<<<(nb + 255) / 256, 256, 0, st>>>(topk, k_b, nb, blk_idx, head_stride, hh, 1,
+                                                       gate, gate_val);
+    if ((rc = check_launch("merge_diag_kernel"))) return rc;
+  }
+  return SA_OK;
+}
+
+}  // namespace sa
+
+extern "C" int sa_block_pool(int groups, int n, int b, int side, const void* x, void* split_out,
+                             float* mean_out, void* stream) {
+  return sa::launch_block_pool(groups, n, b, side, x, split_out, mean_out, nullptr, 0,
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" size_t sa_block_select_workspace(int n, int b, int k_b) {
+  return sa::block_select_ws(n, b, k_b);
+}
+
+extern "C" int sa_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b,
+                               float scale, const void* qp, const void* kp, int32_t* blk_idx,
+                               int32_t* blk_row_off, void* ws, size_t ws_bytes, void* stream) {
+  const int nb = (n + b - 1) / b;
+  return sa::launch_block_select(batch, heads, kv_heads, n, b, k_b, scale, qp, kp, blk_idx,
+                                 (long long)nb * (k_b + 1), blk_row_off, nb + 1, nullptr, 0, ws,
+                                 ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}

@@ -1,0 +1,50 @@
+// internal.h — launch structs and helpers shared between translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sa {
+
+struct TopkArgs {
+  const float* scores;
+  long long ld;          // row stride (elements)
+  int rows;
+  int n;                 // default row length
+  const int32_t* lens;   // optional per-row length
+  int k;                 // default k
+  const int32_t* ks;     // optional per-row k
+  int32_t* idx_out;      // optional [rows, out_ld]
+  long long out_ld;
+  int32_t* count_out;    // optional [rows]: number written
+  uint32_t* bits;        // optional bitmap per row: bit (base + sign*j) set for kept j
+  long long bits_ld;     // words per row
+  int bit_base;
+  int bit_neg;
+  const int32_t* gate;   // optional: process row r only if gate[r / gate_div] == gate_val
+  int gate_div;
+  int gate_val;
+};
+
+int launch_topk(const TopkArgs& a, cudaStream_t st);
+
+int launch_score_tail(int batch, int heads, int kv_heads, int n, float scale, const void* q,
+                      const void* k, int r_lo, int r_hi, float* col_out, float* diag_out,
+                      int accumulate, const int32_t* gate, int gate_val, void* ws, size_t ws_bytes,
+                      cudaStream_t st);
+size_t tail_workspace_bytes(int hh_total, int n, int r_hi, int nchunks);
+int tail_pick_chunks(int r_hi);
+
+int launch_block_pool(int groups, int n, int b, int side, const void* x, void* split_out,
+                      float* mean_out, const int32_t* gate, int gate_val, cudaStream_t st);
+size_t block_select_ws(int n, int b, int k_b);
+int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b, float scale,
+                        const void* qp, const void* kp, int32_t* blk_idx, long long head_stride,
+                        int32_t* blk_row_off, int row_stride, const int32_t* gate, int gate_val,
+                        void* ws, size_t ws_bytes, cudaStream_t st);
+int launch_select(int batch, int heads, int kv_heads, int n, int cal, float scale, const void* q,
+                  const void* k, int ncand, const int32_t* cand_fam, const int32_t* cand_p1,
+                  const int32_t* cand_p2, int32_t* choice_out, int32_t* family_out,
+                  double* err_out, cudaStream_t stream);
+
+}  // namespace sa

@@ -1,0 +1,348 @@
+// prefill.cu — the whole prefill sparse-attention path of one layer on device.
+//
+// Reference: runtime.py:134-206 (prefill).  The reference loops over
+// (batch, head): select (auto) -> build_index(estimated, q_est) -> kernel.
+// Here every stage runs for all heads at once, stream-ordered, with no host
+// synchronisation: the per-head choice lives in device memory and gates the
+// estimator launches.
+//
+//   [auto]  select_kernel            -> choice[HH], family[HH], errors[HH, 3]
+//   apply_choice_kernel              -> family / Triangular params / block side per head
+//   [VS]    score_tail (gated)       -> col[HH, n], diag[HH, n]
+//           topk (gated per cand)    -> column bitmap, reversed diagonal bitmap, id lists
+//   [Block] pool Q (gated), pool K   -> split-bf16 operands
+//           block_select (gated)     -> fixed-stride block rows
+//   build_tiles                      -> executed (q-tile, k-tile) lists
+//   attn_fwd                         -> out (B, n, H * 128)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "api_common.h"
+#include "internal.h"
+#include "sa_types.h"
+
+namespace sa {
+
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+  size_t off[32];
+  size_t total;
+};
+
+enum WsSlot {
+  W_CHOICE = 0, W_FAMILY, W_ERR, W_TRIW, W_TRIS, W_COLBITS, W_DIAGREV, W_COLSC, W_DIAGSC,
+  W_COLIDX, W_DIAGIDX, W_TAIL, W_BLKB, W_ROWOFF, W_BLKIDX, W_QP, W_KP, W_BLKWS,
+  W_TOFF, W_TCNT, W_TILES, W_NUM
+};
+
+struct Plan {
+  int hh, hk, n, nqt;
+  int ncand;
+  sa_pattern cand[3];  // patterns at full n (clamped like build_index)
+  int q_est;
+  int vs_words;
+  int any_vs, any_block;
+  int max_kv, max_ks;
+  int max_nb, blk_row_stride;
+  long long blk_head_stride;
+  size_t tail_ws, blk_ws, qp_elems, kp_elems;
+  int tail_groups;
+};
+
+static int clamp_pattern(const sa_pattern& in, int n, sa_pattern* out) {
+  // build_index clamps to n (patterns.py:324-343) and the index builders
+  // validate the clamped values (patterns.py:237-321)
+  *out = in;
+  if (in.family == SA_TRIANGULAR) {
+    out->p1 = std::min(in.p1, n);
+    out->p2 = std::min(in.p2, n);
+    if (out->p1 < 1 || out->p2 < 0)
+      return fail(SA_ERR_PATTERN_PARAM, "window must be >= 1 and sinks >= 0");
+  } else if (in.family == SA_VERTICAL_SLASH) {
+    out->p1 = std::min(in.p1, n);
+    out->p2 = std::min(in.p2, n);
+    if (out->p1 < 1 || out->p2 < 1) return fail(SA_ERR_PATTERN_PARAM, "k_v and k_s must be >= 1");
+  } else if (in.family == SA_BLOCK_SPARSE) {
+    if (in.p1 < 1 || in.p2 < 1) return fail(SA_ERR_PATTERN_PARAM, "b and k_b must be >= 1");
+    out->p1 = std::min(in.p1, n);
+    const int nb = (n + out->p1 - 1) / out->p1;
+    out->p2 = std::min(in.p2, nb);
+  } else if (in.family != SA_DENSE) {
+    return fail(SA_ERR_PATTERN_PARAM, "unknown pattern family %d", in.family);
+  }
+  return SA_OK;
+}
+
+static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
+  if (!d) return fail(SA_ERR_DIMENSION, "null descriptor");
+  if (d->batch < 1 || d->heads < 1 || d->kv_heads < 1 || d->n < 1)
+    return fail(SA_ERR_DIMENSION, "need batch, heads, kv_heads, n >= 1");
+  if (d->heads % d->kv_heads)
+    return fail(SA_ERR_DIMENSION, "heads=%d not a multiple of kv_heads=%d", d->heads, d->kv_heads);
+  if (d->n > 262144) return fail(SA_ERR_DIMENSION, "n=%d exceeds 262144", d->n);
+  if (!(d->scale > 0.f) || !std::isfinite(d->scale)) return fail(SA_ERR_DIMENSION, "bad scale");
+  memset(p, 0, sizeof(*p));
+  const int n = d->n;
+  p->hh = d->batch * d->heads;
+  p->hk = d->batch * d->kv_heads;
+  p->n = n;
+  p->nqt = (n + kTile - 1) / kTile;
+  p->vs_words = (n + 256) / 32 + 2;
+  int rc;
+  if (d->mode == SA_MODE_DENSE) {
+    p->ncand = 1;
+    p->cand[0] = sa_pattern{SA_DENSE, 0, 0};
+  } else if (d->mode == SA_MODE_FIXED) {
+    p->ncand = 1;
+    if ((rc = clamp_pattern(d->fixed, n, &p->cand[0]))) return rc;
+  } else if (d->mode == SA_MODE_AUTO) {
+    if (d->ncand < 1 || d->ncand > 3) return fail(SA_ERR_SEARCH, "candidate list must hold 1..3 patterns");
+    if (d->cal < 1 || d->cal > n) return fail(SA_ERR_SEARCH, "cal_window must be in [1, %d]", n);
+    p->ncand = d->ncand;
+    for (int c = 0; c < d->ncand; ++c) {
+      if (d->cand[c].family != d->full[c].family) return fail(SA_ERR_SEARCH, "cand/full family mismatch");
+      if ((rc = clamp_pattern(d->full[c], n, &p->cand[c]))) return rc;
+    }
+  } else {
+    return fail(SA_ERR_GENERIC, "unknown prefill mode %d", d->mode);
+  }
+  p->q_est = std::min(std::max(d->q_est, 1), n);
+  p->max_kv = p->max_ks = 1;
+  p->max_nb = 1;
+  long long head_stride = 1;
+  size_t blk_ws = 256;
+  for (int c = 0; c < p->ncand; ++c) {
+    const sa_pattern& pt = p->cand[c];
+    if (pt.family == SA_VERTICAL_SLASH) {
+      p->any_vs = 1;
+      p->max_kv = std::max(p->max_kv, pt.p1);
+      p->max_ks = std::max(p->max_ks, pt.p2);
+    } else if (pt.family == SA_BLOCK_SPARSE) {
+      p->any_block = 1;
+      const int nb = (n + pt.p1 - 1) / pt.p1;
+      p->max_nb = std::max(p->max_nb, nb);
+      head_stride = std::max(head_stride, (long long)nb * (pt.p2 + 1));
+      blk_ws = std::max(blk_ws, block_select_ws(n, pt.p1, pt.p2));
+    }
+  }
+  p->blk_row_stride = p->max_nb + 1;
+  p->blk_head_stride = head_stride;
+  p->blk_ws = blk_ws;
+  p->tail_groups = (p->q_est + 127) / 128;
+  const int r_hi_max = n;
+  p->tail_ws = p->any_vs ? tail_workspace_bytes(p->hh, n, r_hi_max, tail_pick_chunks(r_hi_max)) : 256;
+  p->qp_elems = p->any_block ? (size_t)p->hh * p->max_nb * 384 : 128;
+  p->kp_elems = p->any_block ? (size_t)p->hk * p->max_nb * 384 : 128;
+
+  size_t sz[W_NUM];
+  const size_t hh = p->hh;
+  sz[W_CHOICE] = hh * 4;
+  sz[W_FAMILY] = hh * 4;
+  sz[W_ERR] = hh * 3 * 8;
+  sz[W_TRIW] = hh * 4;
+  sz[W_TRIS] = hh * 4;
+  sz[W_COLBITS] = hh * p->vs_words * 4;
+  sz[W_DIAGREV] = hh * p->vs_words * 4;
+  sz[W_COLSC] = p->any_vs ? hh * n * 4 : 4;
+  sz[W_DIAGSC] = p->any_vs ? hh * n * 4 : 4;
+  sz[W_COLIDX] = p->any_vs ? hh * p->max_kv * 4 : 4;
+  sz[W_DIAGIDX] = p->any_vs ? hh * p->max_ks * 4 : 4;
+  sz[W_TAIL] = p->tail_ws;
+  sz[W_BLKB] = hh * 4;
+  sz[W_ROWOFF] = hh * p->blk_row_stride * 4;
+  sz[W_BLKIDX] = p->any_block ? hh * (size_t)p->blk_head_stride * 4 : 4;
+  sz[W_QP] = p->qp_elems * 2;
+  sz[W_KP] = p->kp_elems * 2;
+  sz[W_BLKWS] = p->blk_ws;
+  sz[W_TOFF] = hh * p->nqt * 4;
+  sz[W_TCNT] = hh * p->nqt * 4;
+  sz[W_TILES] = hh * (size_t)p->nqt * (p->nqt + 1) / 2 * 4;
+  size_t o = 0;
+  for (int i = 0; i < W_NUM; ++i) {
+    L->off[i] = o;
+    o += align_up(sz[i]);
+  }
+  L->total = o;
+  return SA_OK;
+}
+
+struct ApplyArgs {
+  int hh;
+  int ncand;
+  sa_pattern cand[3];
+  const int32_t* choice;  // null -> candidate 0 for every head
+  int32_t* family;
+  int32_t* tri_w;
+  int32_t* tri_s;
+  int32_t* blk_b;
+};
+
+__global__ void apply_choice_kernel(ApplyArgs a) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= a.hh) return;
+  const int c = a.choice ? a.choice[h] : 0;
+  const sa_pattern p = a.cand[c];
+  a.family[h] = p.family;
+  a.tri_w[h] = p.family == SA_TRIANGULAR ? p.p1 : 1;
+  a.tri_s[h] = p.family == SA_TRIANGULAR ? p.p2 : 0;
+  a.blk_b[h] = p.family == SA_BLOCK_SPARSE ? p.p1 : 1;
+}
+
+}  // namespace sa
+
+using namespace sa;
+
+extern "C" size_t sa_prefill_workspace_size(const sa_prefill_desc* desc) {
+  Plan p;
+  Layout L;
+  if (make_plan(desc, &p, &L)) return 0;
+  return L.total;
+}
+
+extern "C" int sa_prefill_views(const sa_prefill_desc* desc, void* ws, sa_prefill_view* v) {
+  Plan p;
+  Layout L;
+  int rc;
+  if ((rc = make_plan(desc, &p, &L))) return rc;
+  if (!v) return fail(SA_ERR_DIMENSION, "null view");
+  char* b = reinterpret_cast<char*>(ws);
+  v->choice = reinterpret_cast<int32_t*>(b + L.off[W_CHOICE]);
+  v->family = reinterpret_cast<int32_t*>(b + L.off[W_FAMILY]);
+  v->errors = reinterpret_cast<double*>(b + L.off[W_ERR]);
+  v->col_scores = reinterpret_cast<float*>(b + L.off[W_COLSC]);
+  v->diag_scores = reinterpret_cast<float*>(b + L.off[W_DIAGSC]);
+  v->col_idx = reinterpret_cast<int32_t*>(b + L.off[W_COLIDX]);
+  v->diag_idx = reinterpret_cast<int32_t*>(b + L.off[W_DIAGIDX]);
+  v->col_ld = p.max_kv;
+  v->diag_ld = p.max_ks;
+  v->index.family = v->family;
+  v->index.tri_window = reinterpret_cast<int32_t*>(b + L.off[W_TRIW]);
+  v->index.tri_sinks = reinterpret_cast<int32_t*>(b + L.off[W_TRIS]);
+  v->index.colbits = reinterpret_cast<uint32_t*>(b + L.off[W_COLBITS]);
+  v->index.diagrev = reinterpret_cast<uint32_t*>(b + L.off[W_DIAGREV]);
+  v->index.vs_words = p.vs_words;
+  v->index.blk_b = reinterpret_cast<int32_t*>(b + L.off[W_BLKB]);
+  v->index.blk_row_off = reinterpret_cast<int32_t*>(b + L.off[W_ROWOFF]);
+  v->index.blk_idx = reinterpret_cast<int32_t*>(b + L.off[W_BLKIDX]);
+  v->index.blk_row_stride = p.blk_row_stride;
+  v->blk_head_stride = p.blk_head_stride;
+  v->tile_off = reinterpret_cast<int32_t*>(b + L.off[W_TOFF]);
+  v->tile_cnt = reinterpret_cast<int32_t*>(b + L.off[W_TCNT]);
+  v->tiles = reinterpret_cast<uint32_t*>(b + L.off[W_TILES]);
+  v->nqt = p.nqt;
+  return SA_OK;
+}
+
+extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void* k, const void* v,
+                          void* out, void* ws, size_t ws_bytes, void* stream) {
+  Plan p;
+  Layout L;
+  int rc;
+  if ((rc = make_plan(desc, &p, &L))) return rc;
+  if (!q || !k || !v || !out || !ws) return fail(SA_ERR_DIMENSION, "null pointer argument");
+  if (ws_bytes < L.total) return fail(SA_ERR_DIMENSION, "workspace too small (%zu < %zu)", ws_bytes, L.total);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  sa_prefill_view V;
+  sa_prefill_views(desc, ws, &V);
+  char* b = reinterpret_cast<char*>(ws);
+  const int n = p.n;
+  const int B = desc->batch, H = desc->heads, HK = desc->kv_heads;
+
+  // 1. per-head choice
+  int32_t* choice = nullptr;
+  if (desc->mode == SA_MODE_AUTO && desc->preselected) {
+    choice = V.choice;
+  } else if (desc->mode == SA_MODE_AUTO) {
+    choice = V.choice;
+    int32_t fam[3], p1[3], p2[3];
+    for (int c = 0; c < p.ncand; ++c) {
+      fam[c] = desc->cand[c].family;
+      p1[c] = desc->cand[c].p1;
+      p2[c] = desc->cand[c].p2;
+    }
+    const int cal = std::min(desc->cal, n);
+    if ((rc = launch_select(B, H, HK, n, cal, desc->scale, q, k, p.ncand, fam, p1, p2, choice,
+                            nullptr, V.errors, st)))
+      return rc;
+  }
+  {
+    ApplyArgs a{};
+    a.hh = p.hh;
+    a.ncand = p.ncand;
+    for (int c = 0; c < p.ncand; ++c) a.cand[c] = p.cand[c];
+    a.choice = choice;
+    a.family = V.family;
+    a.tri_w = const_cast<int32_t*>(V.index.tri_window);
+    a.tri_s = const_cast<int32_t*>(V.index.tri_sinks);
+    a.blk_b = const_cast<int32_t*>(V.index.blk_b);
+    apply_choice_kernel<<<(p.hh + 127) / 128, 128, 0, st>>>(a);
+    if ((rc = check_launch("apply_choice_kernel"))) return rc;
+  }
+  // 2. vertical-slash estimator + stable top-k into bitmaps
+  if (p.any_vs) {
+    cudaMemsetAsync(const_cast<uint32_t*>(V.index.colbits), 0, (size_t)p.hh * p.vs_words * 4, st);
+    cudaMemsetAsync(const_cast<uint32_t*>(V.index.diagrev), 0, (size_t)p.hh * p.vs_words * 4, st);
+    // estimated scoring over the last q_est rows, in groups of <= 128 rows
+    const int r_first = n - p.q_est;
+    for (int g = 0; g < p.tail_groups; ++g) {
+      const int r_hi = n - g * 128;
+      const int r_lo = std::max(r_first, r_hi - 128);
+      if ((rc = launch_score_tail(B, H, HK, n, desc->scale, q, k, r_lo, r_hi, V.col_scores,
+                                  V.diag_scores, g > 0, V.family, SA_VERTICAL_SLASH,
+                                  b + L.off[W_TAIL], p.tail_ws, st)))
+        return rc;
+    }
+    for (int c = 0; c < p.ncand; ++c) {
+      if (p.cand[c].family != SA_VERTICAL_SLASH) continue;
+      TopkArgs t{};
+      t.scores = V.col_scores;
+      t.ld = n;
+      t.rows = p.hh;
+      t.n = n;
+      t.k = p.cand[c].p1;
+      t.idx_out = V.col_idx;
+      t.out_ld = p.max_kv;
+      t.bits = const_cast<uint32_t*>(V.index.colbits);
+      t.bits_ld = p.vs_words;
+      t.bit_base = 0;
+      t.bit_neg = 0;
+      t.gate = choice ? choice : V.family;
+      t.gate_div = 1;
+      t.gate_val = choice ? c : SA_VERTICAL_SLASH;
+      if ((rc = launch_topk(t, st))) return rc;
+      t.scores = V.diag_scores;
+      t.k = p.cand[c].p2;
+      t.idx_out = V.diag_idx;
+      t.out_ld = p.max_ks;
+      t.bits = const_cast<uint32_t*>(V.index.diagrev);
+      t.bit_base = n + 127;
+      t.bit_neg = 1;
+      if ((rc = launch_topk(t, st))) return rc;
+    }
+  }
+  // 3. block estimator
+  if (p.any_block) {
+    for (int c = 0; c < p.ncand; ++c) {
+      if (p.cand[c].family != SA_BLOCK_SPARSE) continue;
+      const int bs = p.cand[c].p1, kb = p.cand[c].p2;
+      const int32_t* gate = choice ? choice : V.family;
+      const int gval = choice ? c : SA_BLOCK_SPARSE;
+      if ((rc = launch_block_pool(p.hh, n, bs, 0, q, b + L.off[W_QP], nullptr, gate, gval, st))) return rc;
+      if ((rc = launch_block_pool(p.hk, n, bs, 1, k, b + L.off[W_KP], nullptr, nullptr, 0, st))) return rc;
+      if ((rc = launch_block_select(B, H, HK, n, bs, kb, desc->scale, b + L.off[W_QP],
+                                    b + L.off[W_KP], const_cast<int32_t*>(V.index.blk_idx),
+                                    p.blk_head_stride, const_cast<int32_t*>(V.index.blk_row_off),
+                                    p.blk_row_stride, gate, gval, b + L.off[W_BLKWS], p.blk_ws, st)))
+        return rc;
+    }
+  }
+  // 4. executed tiles + attention
+  if ((rc = sa_build_tiles(&V.index, p.hh, n, V.tile_off, V.tile_cnt, V.tiles, stream))) return rc;
+  return sa_attn_sparse(B, H, HK, n, desc->scale, q, k, v, out, &V.index, V.tile_off, V.tile_cnt,
+                        V.tiles, nullptr, stream);
+}

@@ -9,7 +9,8 @@ namespace sa {
 
 // Pattern families, in the reference's DEFAULT_FAMILIES order
 // (search.py:322): the selector's argmin index is the family id.
-enum Family : int32_t { FAM_TRI = 0, FAM_VS = 1, FAM_BLOCK = 2, FAM_DENSE = 3 };
+enum Family : int32_t { FAM_TRI = 0, FAM_VS = 1, FAM_BLOCK = 2, FAM_DENSE = 3,
+                        FAM_VS_NOEYE = 5 /* VS index with always_diagonal=False */ };
 
 // Per-tile mask kinds (bits 28..31 of a tile-list entry).
 enum TileKind : uint32_t {

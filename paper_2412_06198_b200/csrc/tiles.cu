@@ -71,6 +71,7 @@ __global__ void build_tiles_kernel(TileBuildArgs a) {
     for (int gq = g0; gq <= g1; ++gq) {
       for (int k = ro[gq] + lane; k < ro[gq + 1]; k += 32) {
         const int gk = a.idx.blk_idx[k];
+        if (gk >= (a.n + b - 1) / b) continue;  // sentinel padding
         const int t0 = (gk * b) / kTile;
         const int t1 = min((gk + 1) * b - 1, a.n - 1) / kTile;
         for (int t = t0; t <= t1 && t <= qt; ++t) atomicOr(&blk_mark[t >> 5], 1u << (t & 31));
@@ -95,7 +96,7 @@ __global__ void build_tiles_kernel(TileBuildArgs a) {
         inc = band || sink || kt == qt;
         const bool full = (kt < qt) && ((i1 - j0 < w) || (j1 < s));
         kind = full ? TK_FULL : TK_BAND;
-      } else if (fam == FAM_VS) {
+      } else if (fam == FAM_VS || fam == FAM_VS_NOEYE) {
         const uint32_t* cb = a.idx.colbits + (size_t)hh * a.idx.vs_words;
         const uint32_t* dr = a.idx.diagrev + (size_t)hh * a.idx.vs_words;
         inc = (kt == qt) || popc_range(cb, j0, min(j1, a.n - 1) + 1) > 0;

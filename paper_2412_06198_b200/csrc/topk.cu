@@ -1,0 +1,213 @@
+// topk.cu — stable top-k of fp32 score rows, bit-exact with the reference's
+// _top_k_stable (patterns.py:231-234): the k largest scores, ties resolved to
+// the LOWER index, returned in ascending index order.
+//
+// Per row (one CTA): map each score to a 32-bit preference key (larger key =
+// preferred; -0.0 == +0.0; NaN least preferred, matching numpy's argsort which
+// sorts NaN last), radix-select the k-th largest key T with four 8-bit MSB
+// passes, then one ordered compaction keeps every key > T plus the first
+// (k - #{key > T}) keys == T in index order.  The result is the exact set the
+// stable sort would return, independent of thread scheduling.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "api_common.h"
+#include "internal.h"
+#include "sa_types.h"
+
+namespace sa {
+
+constexpr int kTopkThreads = 1024;
+
+__device__ __forceinline__ uint32_t pref_key(float f) {
+  uint32_t b = __float_as_uint(f);
+  if ((b & 0x7fffffffu) > 0x7f800000u) return 0u;  // NaN
+  if ((b & 0x7fffffffu) == 0u) b = 0u;               // -0.0 -> +0.0
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// Exclusive block-wide scan of one int per thread (1024 threads).
+__device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = warp_tot[lane];
+    int s = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    warp_tot[lane] = s - t;  // exclusive warp offsets
+    if (lane == 31) warp_tot[32] = s;
+  }
+  __syncthreads();
+  const int r = warp_tot[w] + x - v;
+  total = warp_tot[32];
+  __syncthreads();
+  return r;
+}
+
+
+
+__global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
+  const int r = blockIdx.x;
+  if (a.gate && a.gate[r / a.gate_div] != a.gate_val) return;
+  const int len = a.lens ? a.lens[r] : a.n;
+  int k = a.ks ? a.ks[r] : a.k;
+  k = k < len ? k : len;
+  const float* s = a.scores + (long long)r * a.ld;
+  __shared__ int hist[256];
+  __shared__ int warp_tot[33];
+  __shared__ uint32_t sh_digit;
+  __shared__ int sh_remaining;
+
+  uint32_t prefix = 0u, mask = 0u;
+  int remaining = k;
+  bool take_all = (k >= len);
+  if (!take_all && k > 0) {
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0;
+      __syncthreads();
+      for (int j = threadIdx.x; j < len; j += blockDim.x) {
+        const uint32_t key = pref_key(s[j]);
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        // lane l owns digits [255 - 8l - 7, 255 - 8l]; find the digit where the
+        // running count from the top reaches `remaining`.
+        const int lane = threadIdx.x;
+        int c[8];
+        int tot = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          c[q] = hist[255 - 8 * lane - q];
+          tot += c[q];
+        }
+        int incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int excl = incl - tot;  // count strictly above this lane's digits
+        if (excl < remaining && incl >= remaining) {
+          int run = excl;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (run + c[q] >= remaining) {
+              sh_digit = 255u - 8u * lane - q;
+              sh_remaining = remaining - run;
+              break;
+            }
+            run += c[q];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= sh_digit << shift;
+      mask |= 255u << shift;
+      remaining = sh_remaining;
+      __syncthreads();
+    }
+  }
+  const uint32_t T = prefix;
+  const int need_eq = remaining;  // keys == T to keep, lowest indices first
+
+  // Ordered compaction: thread t owns the contiguous segment [b0, b1).
+  const int per = (len + blockDim.x - 1) / blockDim.x;
+  const int b0 = min(len, (int)threadIdx.x * per), b1 = min(len, b0 + per);
+  int n_eq = 0, n_gt = 0;
+  if (!take_all && k > 0) {
+    for (int j = b0; j < b1; ++j) {
+      const uint32_t key = pref_key(s[j]);
+      n_gt += key > T;
+      n_eq += key == T;
+    }
+  }
+  int tot_eq;
+  const int eq_before = block_excl_scan(n_eq, warp_tot, tot_eq);
+  int keep_eq = need_eq - eq_before;
+  keep_eq = keep_eq < 0 ? 0 : (keep_eq > n_eq ? n_eq : keep_eq);
+  const int mine = take_all ? (b1 - b0) : (k > 0 ? n_gt + keep_eq : 0);
+  int total;
+  int pos = block_excl_scan(mine, warp_tot, total);
+  if (mine > 0) {
+    int eq_seen = 0;
+    for (int j = b0; j < b1; ++j) {
+      bool keep;
+      if (take_all) {
+        keep = true;
+      } else {
+        const uint32_t key = pref_key(s[j]);
+        keep = key > T;
+        if (key == T) {
+          keep = eq_seen < keep_eq;
+          ++eq_seen;
+        }
+      }
+      if (keep) {
+        if (a.idx_out) a.idx_out[(long long)r * a.out_ld + pos] = j;
+        if (a.bits) {
+          const int bp = a.bit_neg ? a.bit_base - j : a.bit_base + j;
+          atomicOr(a.bits + (long long)r * a.bits_ld + (bp >> 5), 1u << (bp & 31));
+        }
+        ++pos;
+      }
+    }
+  }
+  if (threadIdx.x == 0 && a.count_out) a.count_out[r] = total;
+}
+
+int launch_topk(const TopkArgs& a, cudaStream_t st) {
+  if (a.rows <= 0) return SA_OK;
+  topk_rows_kernel<<<a.rows, kTopkThreads, 0, st>>>(a);
+  return check_launch("topk_rows_kernel");
+}
+
+}  // namespace sa
+
+extern "C" int sa_topk_stable_f32(const float* scores, int rows, int n, long long ld, int k,
+                                  int32_t* idx_out, long long out_ld, void* stream) {
+  using namespace sa;
+  if (rows < 0 || n < 1 || ld < n) return fail(SA_ERR_DIMENSION, "bad topk shape");
+  if (k < 1 || k > n) return fail(SA_ERR_PATTERN_PARAM, "k must be in [1, %d], got %d", n, k);
+  if (!scores || !idx_out || out_ld < k) return fail(SA_ERR_DIMENSION, "bad topk output");
+  TopkArgs a{};
+  a.scores = scores;
+  a.ld = ld;
+  a.rows = rows;
+  a.n = n;
+  a.k = k;
+  a.idx_out = idx_out;
+  a.out_ld = out_ld;
+  return launch_topk(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sa_topk_stable_rows_f32(const float* scores, int rows, long long ld,
+                                       const int32_t* lens, const int32_t* ks, int32_t* idx_out,
+                                       long long out_ld, int32_t* count_out, void* stream) {
+  using namespace sa;
+  if (rows < 0 || !scores || !lens || !ks || !idx_out)
+    return fail(SA_ERR_DIMENSION, "bad segmented topk arguments");
+  TopkArgs a{};
+  a.scores = scores;
+  a.ld = ld;
+  a.rows = rows;
+  a.lens = lens;
+  a.ks = ks;
+  a.idx_out = idx_out;
+  a.out_ld = out_ld;
+  a.count_out = count_out;
+  return launch_topk(a, reinterpret_cast<cudaStream_t>(stream));
+}

@@ -21,7 +21,8 @@ import torch
 
 from . import _lib
 
-FAM_TRI, FAM_VS, FAM_BLOCK, FAM_DENSE = 0, 1, 2, 3
+FAM_TRI, FAM_VS, FAM_BLOCK, FAM_DENSE, FAM_VS_NOEYE = 0, 1, 2, 3, 5
+HEAD_DIM = 128
 
 
 def vs_words(n: int) -> int:

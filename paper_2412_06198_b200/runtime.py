@@ -1,0 +1,435 @@
+"""Multi-head prefill runtime on the B200 kernels (reference: runtime.py).
+
+``prefill`` runs one whole layer on device in two C-ABI calls: the selector
+(auto mode, timed as ``select_s``) and ``sa_prefill`` (estimators, top-k,
+index encodings, tile lists and the tcgen05 attention), with no host
+synchronisation until the outputs are returned.  Inputs may be numpy arrays
+(the reference's types; outputs come back as numpy) or torch tensors (outputs
+stay on device).  As a strict extension of runtime.py:119-131, k and v may
+carry fewer heads than q (GQA: query head h reads kv head h // (H // HK)).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _lib
+from .errors import CacheOverflowError, DimensionError, NonFiniteError, SparseAttnError
+from .patterns import BlockSparse, Triangular, VerticalSlash
+from .search import (
+    DENSE_EVAL_CAP,
+    SELECTOR_CAL_MAX,
+    SearchResult,
+    SearchSpace,
+    _rescale_to_full,
+    default_search_space,
+    estimate_flops,
+    pattern_params,
+    refined_candidates,
+)
+
+__all__ = [
+    "CacheOverflowError",
+    "ModelConfig",
+    "KvCache",
+    "HeadPlan",
+    "PrefillResult",
+    "DecodeResult",
+    "prefill",
+    "decode_step",
+]
+
+MODE_DENSE, MODE_FIXED, MODE_AUTO = 0, 1, 2
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """Head layout: d_model must equal n_heads * d_head (runtime.py:39-54)."""
+
+    n_heads: int
+    d_model: int
+    d_head: int
+    max_context: int
+
+    def __post_init__(self) -> None:
+        if min(self.n_heads, self.d_model, self.d_head, self.max_context) < 1:
+            raise DimensionError("all ModelConfig fields must be >= 1")
+        if self.d_model != self.n_heads * self.d_head:
+            raise DimensionError(f"d_model={self.d_model} != n_heads*d_head={self.n_heads * self.d_head}")
+
+
+class KvCache:
+    """Append-only per-head key/value rows, resident on the GPU (runtime.py:57-90).
+
+    ``kv_heads`` (default n_heads) sizes the cache for GQA inputs.  ``keys()`` /
+    ``values()`` return numpy when the appended rows were numpy, else tensors."""
+
+    def __init__(self, batch: int, n_heads: int, d_head: int, capacity: int, dtype=np.float32,
+                 kv_heads: int | None = None):
+        dev = D.require_cuda()
+        tdt = dtype if isinstance(dtype, torch.dtype) else torch.from_numpy(np.zeros(0, dtype)).dtype
+        h = n_heads if kv_heads is None else kv_heads
+        self._k = torch.zeros((batch, h, capacity, d_head), dtype=tdt, device=dev)
+        self._v = torch.zeros((batch, h, capacity, d_head), dtype=tdt, device=dev)
+        self._np = not isinstance(dtype, torch.dtype)
+        self.length = 0
+
+    @property
+    def capacity(self) -> int:
+        return self._k.shape[2]
+
+    def append(self, k_rows, v_rows) -> None:
+        """Append (batch, heads, t, d_head) rows to both caches."""
+        if tuple(k_rows.shape) != tuple(v_rows.shape):
+            raise DimensionError(f"key/value shapes differ: {tuple(k_rows.shape)} vs {tuple(v_rows.shape)}")
+        if tuple(k_rows.shape[:2]) != tuple(self._k.shape[:2]) or k_rows.shape[3] != self._k.shape[3]:
+            raise DimensionError(f"rows shaped {tuple(k_rows.shape)} do not fit cache {tuple(self._k.shape)}")
+        t = k_rows.shape[2]
+        if self.length + t > self.capacity:
+            raise CacheOverflowError(f"cache of capacity {self.capacity} cannot hold {self.length + t} rows")
+        kk = torch.as_tensor(k_rows) if not D.is_torch(k_rows) else k_rows
+        vv = torch.as_tensor(v_rows) if not D.is_torch(v_rows) else v_rows
+        self._k[:, :, self.length:self.length + t] = kk.to(self._k.device, self._k.dtype)
+        self._v[:, :, self.length:self.length + t] = vv.to(self._v.device, self._v.dtype)
+        self._np = not D.is_torch(k_rows)
+        self.length += t
+
+    def _out(self, t):
+        return t.cpu().numpy() if self._np else t
+
+    def keys(self):
+        return self._out(self._k[:, :, : self.length])
+
+    def values(self):
+        return self._out(self._v[:, :, : self.length])
+
+
+@dataclass(frozen=True)
+class HeadPlan:
+    """Per-head execution choice: a sparse pattern or dense (None) (runtime.py:93-99)."""
+
+    head: int
+    pattern: object
+    search: SearchResult | None = None
+
+
+@dataclass
+class PrefillResult:
+    outputs: object  # (batch, length, d_model)
+    cache: KvCache
+    plans: list
+    elapsed_s: float  # selection + index building + kernels (+ cache fill)
+    select_s: float
+    kernel_s: float
+
+
+@dataclass
+class DecodeResult:
+    output: object  # (batch, 1, d_model)
+    cache: KvCache
+    elapsed_s: float
+
+
+def _check_qkv(q, k, v, cfg: ModelConfig):
+    """runtime.py:119-131, extended to k/v with H // g heads."""
+    for name, x in (("q", q), ("k", k), ("v", v)):
+        if len(x.shape) != 4:
+            raise DimensionError(f"{name} must be (batch, n_heads, length, d_head), got {tuple(x.shape)}")
+    if tuple(k.shape) != tuple(v.shape):
+        raise DimensionError(f"q/k/v shapes differ: {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+    batch, heads, length, d_head = (int(s) for s in q.shape)
+    kb, kh, kl, kd = (int(s) for s in k.shape)
+    if (kb, kl, kd) != (batch, length, d_head) or kh < 1 or heads % kh != 0:
+        raise DimensionError(f"q/k/v shapes differ: {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+    if heads != cfg.n_heads or d_head != cfg.d_head:
+        raise DimensionError(
+            f"inputs have (heads, d_head)=({heads}, {d_head}), config expects ({cfg.n_heads}, {cfg.d_head})"
+        )
+    return batch, length, kh
+
+
+def _pat(fam: int, p1: int, p2: int):
+    return (Triangular(p1, p2), VerticalSlash(p1, p2), BlockSparse(p1, p2))[fam]
+
+
+_WS_CACHE: dict = {}
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    key = device
+    buf = _WS_CACHE.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = buf
+    return buf
+
+
+class PrefillPlan:
+    """Host half of one prefill call: validated shapes, the C descriptor and
+    the candidate bookkeeping needed to report plans (reused by bench.py)."""
+
+    def __init__(self, batch, heads, kv_heads, length, d_head, mode, *, search=None, fixed_pattern=None,
+                 cal_window=64, q_est=64):
+        if mode not in ("dense", "auto", "fixed"):
+            raise SparseAttnError(f"unknown prefill mode {mode!r}")
+        if mode == "fixed" and fixed_pattern is None:
+            raise SparseAttnError("mode 'fixed' requires fixed_pattern")
+        self.batch, self.heads, self.kv_heads, self.length, self.d_head = batch, heads, kv_heads, length, d_head
+        self.mode = mode
+        self.scale = 1.0 / math.sqrt(d_head)
+        self.cal = min(cal_window, length)
+        self.q_est = min(q_est, length)
+        d = _lib.sa_prefill_desc()
+        d.batch, d.heads, d.kv_heads, d.n = batch, heads, kv_heads, length
+        d.scale = self.scale
+        d.q_est = self.q_est
+        d.cal = self.cal
+        self.refined = None
+        self.full = None
+        self.fixed_pattern = fixed_pattern
+        if mode == "dense":
+            d.mode = MODE_DENSE
+        elif mode == "fixed":
+            d.mode = MODE_FIXED
+            f, p1, p2 = pattern_params(fixed_pattern)
+            d.fixed.family, d.fixed.p1, d.fixed.p2 = f, p1, p2
+        else:
+            d.mode = MODE_AUTO
+            space = search if search is not None else default_search_space(self.cal, d_head)
+            if len(space.candidates) > 3:
+                raise SparseAttnError("the device selector supports up to 3 candidates")
+            # select_pattern(scoring="exact") refines with cost_q_est = 0 (search.py:235)
+            self.refined = refined_candidates(space, self.cal, d_head, 0)
+            if self.cal == length:
+                self.full = [rc.pattern for rc in self.refined]
+            else:
+                self.full = [_rescale_to_full(rc.pattern, length / self.cal, length) for rc in self.refined]
+            d.ncand = len(self.refined)
+            for c, (rc, fp) in enumerate(zip(self.refined, self.full)):
+                d.cand[c].family, d.cand[c].p1, d.cand[c].p2 = pattern_params(rc.pattern)
+                d.full[c].family, d.full[c].p1, d.full[c].p2 = pattern_params(fp)
+            d.preselected = 1
+        self.desc = d
+        self.ws_bytes = int(_lib.load().sa_prefill_workspace_size(d))
+        if self.ws_bytes == 0:
+            _lib.check(1 if "exceeds" in _lib.load().sa_last_error().decode() else 4)
+
+    @property
+    def hh(self) -> int:
+        return self.batch * self.heads
+
+    def views(self, ws: torch.Tensor) -> _lib.sa_prefill_view:
+        v = _lib.sa_prefill_view()
+        _lib.call("sa_prefill_views", self.desc, ws.data_ptr(), v)
+        return v
+
+    def select(self, q: torch.Tensor, k: torch.Tensor, ws: torch.Tensor) -> None:
+        """Per-head selection into the workspace's choice slot (auto mode)."""
+        v = self.views(ws)
+        if self.cal <= SELECTOR_CAL_MAX:
+            fam = (_ct_i32 * 3)()
+            p1 = (_ct_i32 * 3)()
+            p2 = (_ct_i32 * 3)()
+            for c, rc in enumerate(self.refined):
+                fam[c], p1[c], p2[c] = pattern_params(rc.pattern)
+            _lib.call("sa_select_windowed", self.batch, self.heads, self.kv_heads, self.length, self.cal,
+                      self.scale, q.data_ptr(), k.data_ptr(), len(self.refined), fam, p1, p2, v.choice,
+                      None, v.errors, D.stream())
+            return
+        # wide calibration windows: composed device selection per head
+        from .core import AttnMatrices, dense_attention, frob_norm_diff
+        from .patterns import build_index, sparse_attention
+
+        g = self.heads // self.kv_heads
+        choices = []
+        for hh in range(self.hh):
+            b, h = divmod(hh, self.heads)
+            kvh = b * self.kv_heads + h // g
+            sub = AttnMatrices(q[hh, -self.cal:, : self.d_head], k[kvh, -self.cal:, : self.d_head],
+                               k[kvh, -self.cal:, : self.d_head])
+            dw, _ = dense_attention(sub)
+            best, best_err = 0, math.inf
+            for c, rc in enumerate(self.refined):
+                w, _ = sparse_attention(sub, build_index(sub, rc.pattern, mode="exact"))
+                e = frob_norm_diff(w, dw)
+                if e < best_err:  # strict <: the earlier candidate wins ties (search.py:249)
+                    best, best_err = c, e
+            choices.append(best)
+        _copy_into(v.choice, torch.tensor(choices, dtype=torch.int32, device=q.device))
+
+    def run(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor, ws: torch.Tensor) -> None:
+        _lib.call("sa_prefill", self.desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                  ws.data_ptr(), ws.numel(), D.stream())
+
+    def plans(self, ws: torch.Tensor, with_search: bool = True):
+        """Per (batch, head) HeadPlan list from the device choice (one small D2H)."""
+        v = self.views(ws)
+        hh = self.hh
+        if self.mode == "dense":
+            return [[HeadPlan(head=h, pattern=None) for h in range(self.heads)] for _ in range(self.batch)]
+        if self.mode == "fixed":
+            return [[HeadPlan(head=h, pattern=self.fixed_pattern) for h in range(self.heads)]
+                    for _ in range(self.batch)]
+        choice = _read_i32(v.choice, hh)
+        errs = _read_f64(v.errors, hh * 3).reshape(hh, 3)
+        out = []
+        for b in range(self.batch):
+            row = []
+            for h in range(self.heads):
+                c = int(choice[b * self.heads + h])
+                rc, fp = self.refined[c], self.full[c]
+                res = None
+                if with_search:
+                    res = SearchResult(chosen=fp, realized_flops=estimate_flops(fp, self.length, self.d_head, 0).total,
+                                       error=float(errs[b * self.heads + h, c]), iterations_used=rc.iterations,
+                                       converged=rc.converged)
+                row.append(HeadPlan(head=h, pattern=fp, search=res))
+            out.append(row)
+        return out
+
+
+import ctypes as _ct  # noqa: E402
+
+_ct_i32 = _ct.c_int32
+
+
+def _wrap(ptr: int, count: int, dtype) -> torch.Tensor:
+    """Device tensor view of `count` elements at raw pointer `ptr` (workspace slice)."""
+    esize = torch.empty(0, dtype=dtype).element_size()
+    base = _WS_OWNER_FIND(ptr)
+    off = ptr - base.data_ptr()
+    return base[off: off + count * esize].view(dtype)
+
+
+def _WS_OWNER_FIND(ptr: int) -> torch.Tensor:
+    for buf in _WS_CACHE.values():
+        if buf.data_ptr() <= ptr < buf.data_ptr() + buf.numel():
+            return buf
+    raise RuntimeError("pointer outside the prefill workspace")
+
+
+def _read_i32(ptr, count):
+    return _wrap(ptr, count, torch.int32).cpu().numpy()
+
+
+def _read_f64(ptr, count):
+    return _wrap(ptr, count, torch.float64).cpu().numpy()
+
+
+def _copy_into(ptr, src: torch.Tensor):
+    _wrap(ptr, src.numel(), src.dtype).copy_(src.reshape(-1))
+
+
+def stage_layer(q, k, v):
+    """(B, H, L, d) numpy/torch -> (B*H, L, 128), (B*HK, L, 128), ... bf16 cuda."""
+    B, H, L, d = (int(s) for s in q.shape)
+    HK = int(k.shape[1])
+    qd = D.stage_heads(_flat(q, B * H, L, d), "q")
+    kd = D.stage_heads(_flat(k, B * HK, L, d), "k")
+    vd = D.stage_heads(_flat(v, B * HK, L, d), "v")
+    return qd, kd, vd
+
+
+def _flat(x, g, L, d):
+    if D.is_torch(x):
+        return x.reshape(g, L, d)
+    return np.ascontiguousarray(x).reshape(g, L, d)
+
+
+def prefill(q, k, v, cfg: ModelConfig, search: SearchSpace | None = None, mode: str = "dense", *,
+            fixed_pattern=None, cal_window: int = 64, q_est: int = 64, dense_cap: int = DENSE_EVAL_CAP) -> PrefillResult:
+    """Process all prompt tokens at once; the TTFT analog is elapsed_s (runtime.py:134-206)."""
+    batch, length, kv_heads = _check_qkv(q, k, v, cfg)
+    if length > cfg.max_context:
+        raise DimensionError(f"length {length} exceeds max_context {cfg.max_context}")
+    if mode not in ("dense", "auto", "fixed"):
+        raise SparseAttnError(f"unknown prefill mode {mode!r}")
+    if mode == "fixed" and fixed_pattern is None:
+        raise SparseAttnError("mode 'fixed' requires fixed_pattern")
+    if mode == "auto" and min(cal_window, length) > dense_cap:
+        from .errors import SearchError
+
+        raise SearchError(f"cal_window {cal_window} exceeds the dense evaluation cap {dense_cap}")
+    dev = D.require_cuda()
+    t0 = time.perf_counter()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    qd, kd, vd = stage_layer(q, k, v)
+    for name, x in (("q", qd), ("k", kd), ("v", vd)):
+        if not bool(torch.isfinite(x).all().item()):
+            raise NonFiniteError(f"{name} contains NaN or Inf")
+    plan = PrefillPlan(batch, cfg.n_heads, kv_heads, length, cfg.d_head, mode, search=search,
+                       fixed_pattern=fixed_pattern, cal_window=cal_window, q_est=q_est)
+    ws = _workspace(plan.ws_bytes, dev)
+    out = torch.empty((batch, length, cfg.n_heads * D.HEAD_DIM), dtype=torch.bfloat16, device=dev)
+    ev[1].record()
+    if mode == "auto":
+        plan.select(qd, kd, ws)
+    ev[2].record()
+    plan.run(qd, kd, vd, out, ws)
+    y = out
+    if cfg.d_head < D.HEAD_DIM:
+        y = out.view(batch, length, cfg.n_heads, D.HEAD_DIM)[..., : cfg.d_head].reshape(batch, length, cfg.d_model)
+    outputs = D.to_host_or_keep(y, q)
+    cache = KvCache(batch, cfg.n_heads, cfg.d_head, cfg.max_context,
+                    dtype=(q.dtype if D.is_torch(q) else np.asarray(q).dtype), kv_heads=kv_heads)
+    cache.append(k, v)
+    ev_end = torch.cuda.Event(enable_timing=True)
+    ev_end.record()
+    plans = plan.plans(ws)
+    torch.cuda.synchronize()
+    elapsed = time.perf_counter() - t0
+    select_s = ev[1].elapsed_time(ev[2]) / 1e3
+    kernel_s = ev[2].elapsed_time(ev_end) / 1e3
+    return PrefillResult(outputs=outputs, cache=cache, plans=plans, elapsed_s=elapsed,
+                         select_s=select_s, kernel_s=kernel_s)
+
+
+def decode_step(q_new, k_new, v_new, cache: KvCache, cfg: ModelConfig) -> DecodeResult:
+    """Append one token's k/v and attend its query over the whole cache (runtime.py:209-242).
+
+    Decode is outside the prefill hot path.  It reuses the tcgen05
+    attention kernel with a dense causal index whose tile list holds only the
+    last query tile of each head; the new query sits at row n - 1."""
+    from . import device_index as DI
+
+    batch, length, kv_heads = _check_qkv(q_new, k_new, v_new, cfg)
+    if length != 1:
+        raise DimensionError(f"decode consumes exactly one token, got length {length}")
+    if cache.length < 1:
+        raise SparseAttnError("decode requires a non-empty cache; run prefill first")
+    t0 = time.perf_counter()
+    cache.append(k_new, v_new)
+    n = cache.length
+    H, d = cfg.n_heads, cfg.d_head
+    hh = batch * H
+    qd = D.stage_heads(_flat(q_new, hh, 1, d), "q")
+    dev = qd.device
+    qfull = torch.zeros((hh, n, D.HEAD_DIM), dtype=torch.bfloat16, device=dev)
+    qfull[:, n - 1] = qd[:, 0]
+    kd = D.stage_heads(cache._k[:, :, :n].reshape(batch * kv_heads, n, d), "k")
+    vd = D.stage_heads(cache._v[:, :, :n].reshape(batch * kv_heads, n, d), "v")
+    b = DI.HostIndexBuilder(n, hh)
+    idx = b.upload(dev)  # every head dense
+    nqt = DI.num_qtiles(n)
+    cnt = torch.zeros((hh, nqt), dtype=torch.int32)
+    cnt[:, nqt - 1] = nqt
+    off = torch.zeros((hh, nqt), dtype=torch.int32)
+    off[:, nqt - 1] = torch.arange(hh, dtype=torch.int32) * nqt
+    tiles = torch.arange(nqt, dtype=torch.int32).repeat(hh)
+    tiles.view(hh, nqt)[:, nqt - 1] |= 1 << 28  # diagonal tile: causal mask
+    cnt, off, tiles = cnt.to(dev), off.to(dev), tiles.to(dev)
+    out = torch.empty((batch, n, H * D.HEAD_DIM), dtype=torch.bfloat16, device=dev)
+    _lib.call("sa_attn_sparse", batch, H, kv_heads, n, 1.0 / math.sqrt(d), qfull.data_ptr(), kd.data_ptr(),
+              vd.data_ptr(), out.data_ptr(), idx.view(), off.data_ptr(), cnt.data_ptr(), tiles.data_ptr(),
+              None, D.stream())
+    y = out[:, n - 1:n].reshape(batch, 1, H, D.HEAD_DIM)[..., :d].reshape(batch, 1, H * d)
+    output = D.to_host_or_keep(y, q_new)
+    torch.cuda.synchronize()
+    return DecodeResult(output=output, cache=cache, elapsed_s=time.perf_counter() - t0)

@@ -1,0 +1,262 @@
+"""The drop-in API on a B200, mirroring the reference's own tests
+(pkg/tests/test_patterns.py, test_search.py, test_runtime.py, test_acceptance.py)
+with the bf16 tolerances of the north star, plus the reference-generated
+golden prefill cases (tests/golden/)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import sparse_oracle as O  # noqa: E402
+from tests.golden_io import load, uniform  # noqa: E402
+
+MAX_ABS, MEAN_ABS = 2e-2, 2e-3
+
+
+@pytest.fixture(scope="module")
+def sa():
+    import paper_2412_06198_b200 as m
+
+    return m
+
+
+def bf(x):
+    return O.bf16_round(np.asarray(x, np.float32)).astype(np.float64)
+
+
+def mats(sa, seed, n, d=4):
+    q, k, v = (bf(x) for x in uniform(seed, n, d))
+    return sa.AttnMatrices(q, k, v), (q, k, v)
+
+
+def close(a, b):
+    err = np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64))
+    assert err.max() <= MAX_ABS and err.mean() <= MEAN_ABS, (err.max(), err.mean())
+
+
+# ---- scoring / indices (test_patterns.py:44-127) -------------------------------
+
+def test_zero_logit_scores(sa):
+    z = np.zeros((2, 2))
+    m = sa.AttnMatrices(z, z, z)
+    np.testing.assert_allclose(sa.score_columns(m), [1.5, 0.5], atol=1e-6)
+    np.testing.assert_allclose(sa.score_diagonals(m), [1.5, 0.5], atol=1e-6)
+    z1 = np.zeros((1, 2))
+    np.testing.assert_allclose(sa.score_diagonals(sa.AttnMatrices(z1, z1, z1)), [1.0], atol=1e-6)
+
+
+def test_scores_match_oracle(sa):
+    m, (q, k, _) = mats(sa, 6, 40, 8)
+    cs, ds = O.vs_scores(q, k, "estimated", 9)
+    np.testing.assert_allclose(sa.score_columns(m, "estimated", 9), cs, rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(sa.score_diagonals(m, "estimated", 9), ds, rtol=1e-5, atol=1e-7)
+
+
+def test_bad_scoring_args(sa):
+    m, _ = mats(sa, 8, 4)
+    with pytest.raises(sa.PatternParamError):
+        sa.score_columns(m, "bogus")
+    with pytest.raises(sa.PatternParamError):
+        sa.score_columns(m, "estimated", q_est=0)
+    with pytest.raises(sa.PatternParamError):
+        sa.score_columns(m, "estimated", q_est=5)
+
+
+def test_vs_index_ties_and_zero_logits(sa):
+    z = np.zeros((6, 3))
+    idx = sa.build_vertical_slash_index(sa.AttnMatrices(z, z, z), 1, 1)
+    assert idx.diagonals == (0,)
+    z = np.zeros((4, 2))
+    idx = sa.build_vertical_slash_index(sa.AttnMatrices(z, z, z), 2, 2)
+    assert idx.columns == (0, 1) and idx.diagonals == (0, 1)
+
+
+def test_vs_index_matches_oracle(sa):
+    m, (q, k, _) = mats(sa, 11, 64, 8)
+    idx = sa.build_vertical_slash_index(m, 5, 7)
+    o = O.vs_index(q, k, 5, 7)
+    assert list(idx.columns) == o.columns.tolist() and list(idx.diagonals) == o.diagonals.tolist()
+
+
+def test_block_index_matches_oracle(sa):
+    m, (q, k, _) = mats(sa, 24, 16, 4)
+    idx = sa.build_block_index(m, 4, 2)
+    o = O.block_index(q, k, 4, 2)
+    want = [(g, int(x)) for g, r in enumerate(o.block_rows) for x in r]
+    assert list(idx.blocks) == want
+    z = np.zeros((4, 2))
+    zi = sa.build_block_index(sa.AttnMatrices(z, z, z), 2, 1)
+    assert (0, 0) in zi.blocks and (1, 1) in zi.blocks
+
+
+def test_block_mean(sa):
+    x = np.arange(8, dtype=float).reshape(4, 2)
+    np.testing.assert_allclose(sa.block_mean(x, 2), [(x[0] + x[1]) / 2, (x[2] + x[3]) / 2])
+    x = np.random.default_rng(21).random((5, 2))
+    out = sa.block_mean(x, 2)
+    assert out.shape == (3, 2)
+    np.testing.assert_allclose(out[2], x[4], rtol=1e-6)
+
+
+# ---- kernels (test_patterns.py:130-268, test_acceptance.py:87-183) -------------
+
+@pytest.mark.parametrize("n", [1, 2, 3, 8, 33, 64])
+def test_full_coverage_equals_dense(sa, n):
+    m, (q, k, v) = mats(sa, 100 + n, n, 4)
+    w_d, y_d = sa.dense_attention(m)
+    idx = sa.build_vertical_slash_index(m, n, n)
+    w, y = sa.vertical_slash_attention(m, idx)
+    close(y, y_d)
+    close(w, w_d)
+    close(y_d, O.dense_attention(q, k, v)[1])
+
+
+def test_diagonal_only_is_identity(sa):
+    m, (q, k, v) = mats(sa, 14, 7)
+    w, y = sa.vertical_slash_attention(m, sa.SparseIndex(n=7, always_diagonal=True))
+    np.testing.assert_allclose(w, np.eye(7), atol=1e-6)
+    np.testing.assert_allclose(y, v, atol=1e-2)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_kernels_match_mask_then_dense(sa, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 65))
+    m, (q, k, v) = mats(sa, 200 + seed, n, int(rng.integers(2, 9)))
+    k_v, k_s = int(rng.integers(1, n + 1)), int(rng.integers(1, n + 1))
+    b = int(rng.integers(1, n + 1))
+    nb = -(-n // b)
+    for idx, oidx in (
+        (sa.build_vertical_slash_index(m, k_v, k_s), O.vs_index(q, k, k_v, k_s)),
+        (sa.build_block_index(m, b, int(rng.integers(1, nb + 1))), None),
+        (sa.build_triangular_index(n, max(1, n // 3), min(2, n)), O.tri_index(n, max(1, n // 3), min(2, n))),
+    ):
+        w, y = sa.sparse_attention(m, idx)
+        if oidx is None:
+            rows = [[] for _ in range(-(-n // idx.block_size))]
+            for gq, gk in idx.blocks:
+                rows[gq].append(gk)
+            oidx = O.Index(n, np.zeros(0, np.int64), np.zeros(0, np.int64), idx.block_size,
+                           [np.array(r) for r in rows])
+        allowed = O.index_mask_rows(oidx, 0, n)
+        assert (np.asarray(w)[~allowed] == 0).all()
+        np.testing.assert_allclose(np.asarray(w).sum(axis=1), 1.0, atol=1e-5)
+        close(y, O.masked_attention(q, k, v, oidx))
+        assert sa.realized_size(idx, n) == int(allowed.sum())
+
+
+def test_work_bound(sa):
+    m, _ = mats(sa, 32, 17)
+    idx = sa.build_vertical_slash_index(m, 3, 4)
+    c = sa.MacCounter()
+    sa.sparse_attention(m, idx, counter=c)
+    assert c.logit_macs == sa.realized_size(idx, 17) * m.d_head == c.output_macs
+
+
+def test_kernel_rejections(sa):
+    m, _ = mats(sa, 17, 8)
+    with pytest.raises(sa.PatternParamError):
+        sa.vertical_slash_attention(m, sa.build_block_index(m, 4, 1))
+    with pytest.raises(sa.PatternParamError):
+        sa.block_sparse_attention(m, sa.build_triangular_index(8, 2, 1))
+    with pytest.raises(sa.DimensionError):
+        sa.vertical_slash_attention(m, sa.SparseIndex(n=5))
+    bad = np.array([[np.nan, 0.0], [0.0, 0.0]])
+    with pytest.raises(sa.NonFiniteError):
+        sa.AttnMatrices(bad, bad, bad)
+
+
+# ---- search (test_search.py) -----------------------------------------------------
+
+def test_select_pattern_matches_oracle(sa):
+    _, meta = load()
+    for c in meta["cases"]["select"]:
+        q, k, v = (bf(x) for x in uniform(c["seed"], c["n"], c["d"]))
+        m = sa.AttnMatrices(q, k, v)
+        res = sa.select_pattern(m, sa.default_search_space(c["n"], c["d"]))
+        o = O.select(q, k, v, O.default_space(c["n"], c["d"]))
+        assert type(res.chosen).__name__[0] == type(o[0]).__name__[0]
+        assert abs(res.error - o[2]) <= 1e-3 * max(1.0, o[2])
+
+
+def test_windowed_rescale(sa):
+    m, _ = mats(sa, 77, 256, 8)
+    res = sa.select_pattern_windowed(m, sa.default_search_space(64, 8), 64)
+    assert res.chosen.__class__ in (sa.Triangular, sa.VerticalSlash, sa.BlockSparse)
+    if isinstance(res.chosen, sa.BlockSparse):
+        assert res.chosen.b == 8
+
+
+# ---- runtime (test_runtime.py, golden prefill) -----------------------------------
+
+def test_single_token_output_is_v(sa):
+    rng = np.random.default_rng(60)
+    cfg = sa.ModelConfig(n_heads=2, d_model=6, d_head=3, max_context=4)
+    q, k, v = (rng.uniform(-1, 1, (1, 2, 1, 3)) for _ in range(3))
+    for mode, kw in (("dense", {}), ("fixed", {"fixed_pattern": sa.Triangular(1)}), ("auto", {})):
+        res = sa.prefill(q, k, v, cfg, mode=mode, **kw)
+        np.testing.assert_allclose(res.outputs[0, 0], v[0, :, 0, :].reshape(6), atol=1e-2)
+        assert res.cache.length == 1
+
+
+def test_fixed_full_window_equals_dense(sa):
+    rng = np.random.default_rng(61)
+    cfg = sa.ModelConfig(n_heads=2, d_model=8, d_head=4, max_context=32)
+    q, k, v = (rng.uniform(-1, 1, (1, 2, 32, 4)) for _ in range(3))
+    dense = sa.prefill(q, k, v, cfg, mode="dense")
+    fixed = sa.prefill(q, k, v, cfg, mode="fixed", fixed_pattern=sa.Triangular(window=32))
+    np.testing.assert_allclose(fixed.outputs, dense.outputs, atol=1e-6)
+
+
+def test_prefill_rejections(sa):
+    cfg = sa.ModelConfig(n_heads=2, d_model=8, d_head=4, max_context=8)
+    x = np.zeros((1, 2, 16, 4))
+    with pytest.raises(sa.DimensionError):
+        sa.prefill(x, x, x, cfg)
+    x = np.zeros((1, 2, 8, 4))
+    with pytest.raises(sa.SparseAttnError):
+        sa.prefill(x, x, x, cfg, mode="fixed")
+    with pytest.raises(sa.SparseAttnError):
+        sa.prefill(x, x, x, cfg, mode="bogus")
+
+
+def test_decode_consistent_with_prefill(sa):
+    rng = np.random.default_rng(62)
+    cfg = sa.ModelConfig(n_heads=2, d_model=16, d_head=8, max_context=40)
+    q, k, v = (rng.uniform(-1, 1, (1, 2, 33, 8)) for _ in range(3))
+    full = sa.prefill(q, k, v, cfg, mode="dense")
+    part = sa.prefill(q[:, :, :32], k[:, :, :32], v[:, :, :32], cfg, mode="dense")
+    dec = sa.decode_step(q[:, :, 32:], k[:, :, 32:], v[:, :, 32:], part.cache, cfg)
+    close(dec.output[0, 0], full.outputs[0, 32])
+    assert dec.cache.length == 33
+
+
+def pat_from(js):
+    fam, a, b = js
+    return {"triangular": O.Tri, "vertical-slash": O.VS, "block-sparse": O.Blk}[fam](a, b)
+
+
+@pytest.mark.parametrize("cid", range(8))
+def test_golden_prefill(sa, cid):
+    arr, meta = load()
+    c = meta["cases"]["prefill"][cid]
+    if c["H"] == c["HK"]:
+        q, k, v = O.synth_qkv(c["seed"], c["ctx"], c["H"], 128)
+    else:
+        q, k, v = O.synth_qkv_gqa(c["seed"], c["ctx"], c["H"], c["HK"], 128)
+    q, k, v = (O.bf16_round(x) for x in (q, k, v))
+    cfg = sa.ModelConfig(n_heads=c["H"], d_model=c["H"] * 128, d_head=128, max_context=c["ctx"])
+    kw = {}
+    if c["mode"] == "fixed":
+        p = O.fixed_pattern_for(c["fixed"], c["ctx"])
+        kw["fixed_pattern"] = {O.Tri: sa.Triangular, O.VS: sa.VerticalSlash, O.Blk: sa.BlockSparse}[type(p)](
+            *p.__dict__.values())
+    res = sa.prefill(q, k, v, cfg, mode=c["mode"], **kw)
+    got_plans = [hp.pattern for hp in res.plans[0]]
+    want = [pat_from(p) if p else None for p in c["plans"]]
+    conv = lambda p: None if p is None else (type(p).__name__[0], *p.__dict__.values())  # noqa: E731
+    assert [conv(p) for p in got_plans] == [conv(p) for p in want]
+    step = max(1, c["ctx"] // 64)
+    close(res.outputs[0, ::step], arr[f"prefill_{cid}_rows"])
