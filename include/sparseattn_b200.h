@@ -81,6 +81,9 @@ typedef struct {
   sa_pattern full[3];
   int32_t preselected;   /* SA_MODE_AUTO: 1 = the caller already wrote the
                             per-head choice into view.choice (skip the selector) */
+  void* stage_events[6]; /* optional cudaEvent_t, recorded on `stream` after:
+                            [0] selection, [1] VS estimator + top-k, [2] block
+                            estimator, [3] tile lists, [4] attention, [5] unused */
 } sa_prefill_desc;
 
 /* Device views into a prefill workspace (valid after sa_prefill). */

@@ -62,6 +62,7 @@ class sa_prefill_desc(ctypes.Structure):
         ("cand", sa_pattern * 3),
         ("full", sa_pattern * 3),
         ("preselected", ctypes.c_int32),
+        ("stage_events", ctypes.c_void_p * 6),
     ]
 
 

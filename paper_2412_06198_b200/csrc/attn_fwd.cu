@@ -70,6 +70,10 @@ __device__ __forceinline__ void build_row_mask(const AttnArgs& a, uint32_t kind,
                                                int j0, int qt, int kt, uint32_t (&m)[4]) {
   m[0] = m[1] = m[2] = m[3] = 0u;
   const int diag_c = i - j0;  // column (within tile) of the main diagonal
+  if (kind == TK_CAUSAL || i >= a.n) {  // padding rows past n: any non-empty mask, never stored
+    mask_set_range(m, 0, diag_c + 1);
+    return;
+  }
   if (kind == TK_CAUSAL) {
     mask_set_range(m, 0, diag_c + 1);
     return;

@@ -283,6 +283,10 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
     apply_choice_kernel<<<(p.hh + 127) / 128, 128, 0, st>>>(a);
     if ((rc = check_launch("apply_choice_kernel"))) return rc;
   }
+  auto mark = [&](int e) {
+    if (desc->stage_events[e]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(desc->stage_events[e]), st);
+  };
+  mark(0);
   // 2. vertical-slash estimator + stable top-k into bitmaps
   if (p.any_vs) {
     cudaMemsetAsync(const_cast<uint32_t*>(V.index.colbits), 0, (size_t)p.hh * p.vs_words * 4, st);
@@ -325,6 +329,7 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
       if ((rc = launch_topk(t, st))) return rc;
     }
   }
+  mark(1);
   // 3. block estimator
   if (p.any_block) {
     for (int c = 0; c < p.ncand; ++c) {
@@ -341,8 +346,12 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
         return rc;
     }
   }
+  mark(2);
   // 4. executed tiles + attention
   if ((rc = sa_build_tiles(&V.index, p.hh, n, V.tile_off, V.tile_cnt, V.tiles, stream))) return rc;
-  return sa_attn_sparse(B, H, HK, n, desc->scale, q, k, v, out, &V.index, V.tile_off, V.tile_cnt,
-                        V.tiles, nullptr, stream);
+  mark(3);
+  rc = sa_attn_sparse(B, H, HK, n, desc->scale, q, k, v, out, &V.index, V.tile_off, V.tile_cnt,
+                      V.tiles, nullptr, stream);
+  mark(4);
+  return rc;
 }

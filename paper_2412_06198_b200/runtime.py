@@ -378,8 +378,11 @@ def prefill(q, k, v, cfg: ModelConfig, search: SearchSpace | None = None, mode: 
         y = out.view(batch, length, cfg.n_heads, D.HEAD_DIM)[..., : cfg.d_head].reshape(batch, length, cfg.d_model)
     outputs = D.to_host_or_keep(y, q)
     cache = KvCache(batch, cfg.n_heads, cfg.d_head, cfg.max_context,
-                    dtype=(q.dtype if D.is_torch(q) else np.asarray(q).dtype), kv_heads=kv_heads)
-    cache.append(k, v)
+                    dtype=(k.dtype if D.is_torch(k) else np.asarray(k).dtype), kv_heads=kv_heads)
+    # fill from the staged device copies (no second host->device transfer)
+    cache.append(kd.view(batch, kv_heads, length, D.HEAD_DIM)[..., : cfg.d_head],
+                 vd.view(batch, kv_heads, length, D.HEAD_DIM)[..., : cfg.d_head])
+    cache._np = not D.is_torch(k)
     ev_end = torch.cuda.Event(enable_timing=True)
     ev_end.record()
     plans = plan.plans(ws)

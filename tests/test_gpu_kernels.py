@@ -43,8 +43,9 @@ def run_index(sa, q, k, v, builder, H, HK):
     off, cnt, tiles = DI.build_tiles(idx)
     out = torch.empty(n, H * 128, dtype=torch.bfloat16, device="cuda")
     lse = torch.empty(H, n, dtype=torch.float32, device="cuda")
-    _lib.call("sa_attn_sparse", 1, H, HK, n, 1 / np.sqrt(128), to_dev(q).data_ptr(), to_dev(k).data_ptr(),
-              to_dev(v).data_ptr(), out.data_ptr(), idx.view(), off.data_ptr(), cnt.data_ptr(),
+    qd, kd, vd = to_dev(q), to_dev(k), to_dev(v)  # keep alive across the async launch
+    _lib.call("sa_attn_sparse", 1, H, HK, n, 1 / np.sqrt(128), qd.data_ptr(), kd.data_ptr(),
+              vd.data_ptr(), out.data_ptr(), idx.view(), off.data_ptr(), cnt.data_ptr(),
               tiles.data_ptr(), lse.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     return out.float().cpu().numpy().reshape(n, H, 128).transpose(1, 0, 2), cnt
