@@ -141,8 +141,8 @@ int sa_topk_stable_rows_f32(const float* scores, int rows, long long ld, const i
 
 /* ---- Block estimator: patterns.block_mean / build_block_index
  *      (patterns.py:279-321) ------------------------------------------------ */
-/* side 0 = query operand [hi|lo|hi], 1 = key operand [hi|hi|lo]; split_out is
- * [groups, nb, 384] bf16, mean_out (nullable) [groups, nb, 128] fp32. */
+/* side 0 = query operand [hi|lo|hi] ([groups, nb, 384] bf16), side 1 = key
+ * operand [hi|lo] ([groups, nb, 256] bf16); mean_out (nullable) [groups, nb, 128] fp32. */
 int sa_block_pool(int groups, int n, int b, int side, const void* x, void* split_out,
                   float* mean_out, void* stream);
 size_t sa_block_select_workspace(int n, int b, int k_b);

@@ -149,9 +149,15 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
   int item;
   if (a.work != nullptr) {
     item = a.work[blockIdx.x];
-  } else {  // heaviest query tiles (most causal key tiles) first
-    const int qt = a.nqt - 1 - blockIdx.x / a.hh_total;
-    item = (blockIdx.x % a.hh_total) * a.nqt + qt;
+  } else {
+    // kv-group-major (the group's K/V stays L2-resident while its CTAs run),
+    // heaviest query tiles first inside a group, the group's q-heads adjacent
+    const int gs = a.heads / a.kv_heads;
+    const int per_group = a.nqt * gs;
+    const int g = blockIdx.x / per_group, r = blockIdx.x % per_group;
+    const int qt = a.nqt - 1 - r / gs;
+    const int hh_ = (g / a.kv_heads) * a.heads + (g % a.kv_heads) * gs + r % gs;
+    item = hh_ * a.nqt + qt;
   }
   const int hh = item / a.nqt;
   const int qt = item % a.nqt;
@@ -260,7 +266,6 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(tbase + lane_off + kColS + 32 * c, s[c]);
       tmem_ld_wait();
-      float mx = -INFINITY;
       if (kind != TK_FULL) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -268,10 +273,17 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
           for (int t = 0; t < 32; ++t)
             if (!((msk[c] >> t) & 1u)) s[c][t] = __float_as_uint(-INFINITY);
       }
+      // row max: four independent FMNMX3 chains
+      float mx;
+      {
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int t = 0; t < 32; ++t) mx = fmaxf(mx, __uint_as_float(s[c][t]));
+          for (int t = 0; t < 32; t += 2)
+            m4[c] = fmax3(m4[c], __uint_as_float(s[c][t]), __uint_as_float(s[c][t + 1]));
+        mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+      }
       const float mt = mx * sl2;
       // Lazy rescale: keep a stale max until the row max grows by > 2^8.  The
       // decision is made per row but the TMEM round trip of O is warp-wide
@@ -295,19 +307,27 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         if (need) m_used = mt;
       }
       const float moff = (m_used == -INFINITY) ? 0.f : m_used;
-      float rs0 = 0.f, rs1 = 0.f;
+      // p = exp2(s * scale_log2 - m): FFMA2 + two MUFU.EX2; row sum in four FADD2 chains
+      const float2 sc2 = make_float2(sl2, sl2);
+      const float2 mo2 = make_float2(-moff, -moff);
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                       make_float2(0.f, 0.f)};
       uint32_t p[2][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int t = 0; t < 32; t += 2) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(s[c][t]), sl2, -moff));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(s[c][t + 1]), sl2, -moff));
-          rs0 += p0;
-          rs1 += p1;
-          p[c >> 1][(c & 1) * 16 + (t >> 1)] = pack_bf16(p0, p1);
+          float2 x = ffma2(make_float2(__uint_as_float(s[c][t]), __uint_as_float(s[c][t + 1])), sc2, mo2);
+          x.x = fast_exp2(x.x);
+          x.y = fast_exp2(x.y);
+          acc[(t >> 1) & 3] = fadd2(acc[(t >> 1) & 3], x);
+          p[c >> 1][(c & 1) * 16 + (t >> 1)] = pack_bf16(x.x, x.y);
         }
-      l += rs0 + rs1;
+      {
+        const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+        const float2 a = fadd2(a01, a23);
+        l += a.x + a.y;
+      }
       tmem_st32(tbase + lane_off + kColP, p[0]);
       tmem_st32(tbase + lane_off + kColP + 32, p[1]);
       tmem_st_wait();

@@ -10,8 +10,10 @@
 // exponentiates (single GEMM pass, no row statistics).  Pooled means are fp32
 // (not bf16-representable), so the GEMM runs on tcgen05 with a split-bf16
 // operand: x = hi + lo (hi = bf16(x), lo = bf16(x - hi)), and
-//     qb . kb ~= [qhi | qlo | qhi] . [khi | khi | klo]   (K = 3 x 128)
-// which keeps ~16 mantissa bits per product (DESIGN.md §Block estimator).
+//     qb . kb ~= qhi.khi + qlo.khi + qhi.klo   (three K=128 passes)
+// which keeps ~16 mantissa bits per product (DESIGN.md §Block estimator).  The
+// query operand is stored [qhi | qlo | qhi] (384 wide), the key operand
+// [khi | klo] (256 wide); khi feeds two passes from one shared-memory stage.
 //
 // Epilogue modes: FUSED keeps a per-row top-K list in registers (K = k_b <= 8,
 // which covers the auto-selected Block(8, 1)); MATERIALIZE writes the masked
@@ -32,7 +34,8 @@
 
 namespace sa {
 
-constexpr int kSplitK = 384;  // 3 x 128 split-bf16 contraction
+constexpr int kSplitQ = 384;  // query operand [hi | lo | hi]
+constexpr int kSplitKey = 256;  // key operand [hi | lo]
 
 // out: [G, nb, 384] bf16 split operand; mean_out (optional): [G, nb, 128] fp32
 __global__ void block_pool_kernel(const __nv_bfloat16* __restrict__ x, int G, int n, int b,
@@ -51,16 +54,22 @@ __global__ void block_pool_kernel(const __nv_bfloat16* __restrict__ x, int G, in
   const float mean = acc / (float)(r1 - r0);
   const __nv_bfloat16 hi = __float2bfloat16_rn(mean);
   const __nv_bfloat16 lo = __float2bfloat16_rn(mean - __bfloat162float(hi));
-  __nv_bfloat16* o = out + ((long long)g * nb + blk) * kSplitK + d;
-  o[0] = hi;
-  o[128] = side == 0 ? lo : hi;
-  o[256] = side == 0 ? hi : lo;
+  if (side == 0) {
+    __nv_bfloat16* o = out + ((long long)g * nb + blk) * kSplitQ + d;
+    o[0] = hi;
+    o[128] = lo;
+    o[256] = hi;
+  } else {
+    __nv_bfloat16* o = out + ((long long)g * nb + blk) * kSplitKey + d;
+    o[0] = hi;
+    o[128] = lo;
+  }
   if (mean_out) mean_out[((long long)g * nb + blk) * kHeadDim + d] = mean;
 }
 
 struct BlockScoreArgs {
   CUtensorMap tmap_qp;  // [HH, nb, 384]
-  CUtensorMap tmap_kp;  // [HK, nb, 384]
+  CUtensorMap tmap_kp;  // [HK, nb, 256]
   int nb, heads, kv_heads, hh_total;
   int nqt;  // ceil(nb / 128)
   float scale;
@@ -79,12 +88,12 @@ struct BlockScoreArgs {
 };
 
 constexpr int kBsThreads = 192;
-constexpr int kBsSmemA = 0;        // 6 x 16 KB
-constexpr int kBsSmemB = 98304;    // 3 x 32 KB
-constexpr int kBsSmemBar = 196608;
+constexpr int kBsSmemA = 0;        // 6 x 16 KB query operand
+constexpr int kBsSmemB = 98304;    // 4 x 32 KB key-chunk ring (two key tiles in flight)
+constexpr int kBsSmemBar = 229376;
 constexpr int kBsSmemBytes = kBsSmemBar + 256 + 1024;
 
-enum BBar { BB_A = 0, BB_KF0, BB_KF1, BB_KF2, BB_KE0, BB_KE1, BB_KE2, BB_SF0, BB_SF1, BB_SE0, BB_SE1, BB_NUM };
+enum BBar { BB_A = 0, BB_KF0, BB_KF1, BB_KF2, BB_KF3, BB_KE0, BB_KE1, BB_KE2, BB_KE3, BB_SF0, BB_SF1, BB_SE0, BB_SE1, BB_NUM };
 
 template <int K, bool FUSED>
 __global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid_constant__ BlockScoreArgs a) {
@@ -106,7 +115,7 @@ __global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[BB_A], 1);
-    for (int s = 0; s < 3; ++s) {
+    for (int s = 0; s < 4; ++s) {
       mbar_init(&bars[BB_KF0 + s], 1);
       mbar_init(&bars[BB_KE0 + s], 1);
     }
@@ -127,12 +136,13 @@ __global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid
       mbar_arrive_expect_tx(&bars[BB_A], 98304);
       for (int c = 0; c < 6; ++c) tma_load_3d(sA + c * 16384, &a.tmap_qp, &bars[BB_A], 64 * c, qt * kTile, hh);
       for (int j = 0; j < cnt; ++j) {
-        for (int c = 0; c < 3; ++c) {
-          if (j > 0) mbar_wait(&bars[BB_KE0 + c], (j - 1) & 1);
-          uint8_t* dst = sB + c * 32768;
-          mbar_arrive_expect_tx(&bars[BB_KF0 + c], 32768);
-          tma_load_3d(dst, &a.tmap_kp, &bars[BB_KF0 + c], 128 * c, j * kTile, hkv);
-          tma_load_3d(dst + 16384, &a.tmap_kp, &bars[BB_KF0 + c], 128 * c + 64, j * kTile, hkv);
+        for (int c = 0; c < 2; ++c) {  // c = 0: khi, c = 1: klo
+          const int slot = 2 * (j & 1) + c;
+          if (j >= 2) mbar_wait(&bars[BB_KE0 + slot], ((j >> 1) - 1) & 1);
+          uint8_t* dst = sB + slot * 32768;
+          mbar_arrive_expect_tx(&bars[BB_KF0 + slot], 32768);
+          tma_load_3d(dst, &a.tmap_kp, &bars[BB_KF0 + slot], 128 * c, j * kTile, hkv);
+          tma_load_3d(dst + 16384, &a.tmap_kp, &bars[BB_KF0 + slot], 128 * c + 64, j * kTile, hkv);
         }
       }
     }
@@ -144,19 +154,24 @@ __global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid
       for (int j = 0; j < cnt; ++j) {
         const int buf = j & 1;
         if (j >= 2) mbar_wait(&bars[BB_SE0 + buf], ((j >> 1) - 1) & 1);
-        for (int c = 0; c < 3; ++c) {
-          mbar_wait(&bars[BB_KF0 + c], j & 1);
-          tc_fence_after();
-          const uint32_t b_addr = smem_u32(sB + c * 32768);
+        // passes: (A chunk 0 = qhi, khi), (A chunk 1 = qlo, khi), (A chunk 2 = qhi, klo)
+        for (int pass = 0; pass < 3; ++pass) {
+          const int c = pass < 2 ? 0 : 1;
+          const int slot = 2 * (j & 1) + c;
+          if (pass != 1) {
+            mbar_wait(&bars[BB_KF0 + slot], (j >> 1) & 1);
+            tc_fence_after();
+          }
+          const uint32_t b_addr = smem_u32(sB + slot * 32768);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const int ka = 8 * c + kk;  // global k-step over the 384-wide A
+            const int ka = 8 * pass + kk;  // k-step over the 384-wide A
             const uint32_t aoff = (ka >> 2) * 16384 + (ka & 3) * 32;
             const uint32_t boff = (kk >> 2) * 16384 + (kk & 3) * 32;
             mma_ss(tbase + buf * 128, sdesc_sw128(a_addr + aoff, 16, 1024),
-                   sdesc_sw128(b_addr + boff, 16, 1024), idesc, (c > 0 || kk > 0) ? 1u : 0u);
+                   sdesc_sw128(b_addr + boff, 16, 1024), idesc, (pass > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&bars[BB_KE0 + c]);
+          if (pass != 0) mma_commit(&bars[BB_KE0 + slot]);
         }
         mma_commit(&bars[BB_SF0 + buf]);
       }
@@ -356,8 +371,8 @@ int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_
   memset(&a, 0, sizeof(a));
   int rc;
   const int hh_total = batch * heads;
-  if ((rc = make_tmap_3d_bf16(&a.tmap_qp, qp, kSplitK, nb, hh_total, kTile))) return rc;
-  if ((rc = make_tmap_3d_bf16(&a.tmap_kp, kp, kSplitK, nb, batch * kv_heads, kTile))) return rc;
+  if ((rc = make_tmap_3d_bf16(&a.tmap_qp, qp, kSplitQ, nb, hh_total, kTile))) return rc;
+  if ((rc = make_tmap_3d_bf16(&a.tmap_kp, kp, kSplitKey, nb, batch * kv_heads, kTile))) return rc;
   a.nb = nb;
   a.heads = heads;
   a.kv_heads = kv_heads;

@@ -24,6 +24,16 @@ struct TopkArgs {
   const int32_t* gate;   // optional: process row r only if gate[r / gate_div] == gate_val
   int gate_div;
   int gate_val;
+  // optional second row set: rows r >= split use (scores2, k2, idx_out2, bits2,
+  // bit_base2, bit_neg2) with local row r - split (same ld / out_ld / bits_ld)
+  int split;
+  const float* scores2;
+  int k2;
+  int32_t* idx_out2;
+  long long out_ld2;
+  uint32_t* bits2;
+  int bit_base2;
+  int bit_neg2;
 };
 
 int launch_topk(const TopkArgs& a, cudaStream_t st);

@@ -137,7 +137,7 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
   const int r_hi_max = n;
   p->tail_ws = p->any_vs ? tail_workspace_bytes(p->hh, n, r_hi_max, tail_pick_chunks(r_hi_max)) : 256;
   p->qp_elems = p->any_block ? (size_t)p->hh * p->max_nb * 384 : 128;
-  p->kp_elems = p->any_block ? (size_t)p->hk * p->max_nb * 384 : 128;
+  p->kp_elems = p->any_block ? (size_t)p->hk * p->max_nb * 256 : 128;
 
   size_t sz[W_NUM];
   const size_t hh = p->hh;
@@ -318,14 +318,15 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
       t.gate = choice ? choice : V.family;
       t.gate_div = 1;
       t.gate_val = choice ? c : SA_VERTICAL_SLASH;
-      if ((rc = launch_topk(t, st))) return rc;
-      t.scores = V.diag_scores;
-      t.k = p.cand[c].p2;
-      t.idx_out = V.diag_idx;
-      t.out_ld = p.max_ks;
-      t.bits = const_cast<uint32_t*>(V.index.diagrev);
-      t.bit_base = n + 127;
-      t.bit_neg = 1;
+      // diagonal rows in the same launch (rows >= hh)
+      t.split = p.hh;
+      t.scores2 = V.diag_scores;
+      t.k2 = p.cand[c].p2;
+      t.idx_out2 = V.diag_idx;
+      t.out_ld2 = p.max_ks;
+      t.bits2 = const_cast<uint32_t*>(V.index.diagrev);
+      t.bit_base2 = n + 127;
+      t.bit_neg2 = 1;
       if ((rc = launch_topk(t, st))) return rc;
     }
   }

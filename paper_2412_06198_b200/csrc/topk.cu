@@ -59,12 +59,28 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
 
 
 __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
-  const int r = blockIdx.x;
+  int r = blockIdx.x;
+  const float* scores = a.scores;
+  int kk = a.k;
+  int32_t* idx_out = a.idx_out;
+  long long out_ld = a.out_ld;
+  uint32_t* bits = a.bits;
+  int bit_base = a.bit_base, bit_neg = a.bit_neg;
+  if (a.split > 0 && r >= a.split) {
+    r -= a.split;
+    scores = a.scores2;
+    kk = a.k2;
+    idx_out = a.idx_out2;
+    out_ld = a.out_ld2;
+    bits = a.bits2;
+    bit_base = a.bit_base2;
+    bit_neg = a.bit_neg2;
+  }
   if (a.gate && a.gate[r / a.gate_div] != a.gate_val) return;
   const int len = a.lens ? a.lens[r] : a.n;
-  int k = a.ks ? a.ks[r] : a.k;
+  int k = a.ks ? a.ks[r] : kk;
   k = k < len ? k : len;
-  const float* s = a.scores + (long long)r * a.ld;
+  const float* s = scores + (long long)r * a.ld;
   __shared__ int hist[256];
   __shared__ int warp_tot[33];
   __shared__ uint32_t sh_digit;
@@ -78,9 +94,16 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
       const int shift = 24 - 8 * pass;
       for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0;
       __syncthreads();
-      for (int j = threadIdx.x; j < len; j += blockDim.x) {
-        const uint32_t key = pref_key(s[j]);
-        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+      // warp-aggregated histogram: scores of similar magnitude share their top
+      // bits, so lanes are matched on the bin and one leader adds the count
+      const int len_pad = (len + 31) & ~31;
+      for (int j = threadIdx.x; j < len_pad; j += blockDim.x) {
+        const bool in = j < len;
+        const uint32_t key = in ? pref_key(s[j]) : 0u;
+        const bool hit = in && ((key & mask) == prefix);
+        const uint32_t bin = hit ? ((key >> shift) & 255u) : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+        if (hit && (threadIdx.x & 31) == (__ffs(peers) - 1)) atomicAdd(&hist[bin], __popc(peers));
       }
       __syncthreads();
       if (threadIdx.x < 32) {
@@ -157,21 +180,22 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
         }
       }
       if (keep) {
-        if (a.idx_out) a.idx_out[(long long)r * a.out_ld + pos] = j;
-        if (a.bits) {
-          const int bp = a.bit_neg ? a.bit_base - j : a.bit_base + j;
-          atomicOr(a.bits + (long long)r * a.bits_ld + (bp >> 5), 1u << (bp & 31));
+        if (idx_out) idx_out[(long long)r * out_ld + pos] = j;
+        if (bits) {
+          const int bp = bit_neg ? bit_base - j : bit_base + j;
+          atomicOr(bits + (long long)r * a.bits_ld + (bp >> 5), 1u << (bp & 31));
         }
         ++pos;
       }
     }
   }
-  if (threadIdx.x == 0 && a.count_out) a.count_out[r] = total;
+  if (threadIdx.x == 0 && a.count_out) a.count_out[blockIdx.x] = total;
 }
 
 int launch_topk(const TopkArgs& a, cudaStream_t st) {
-  if (a.rows <= 0) return SA_OK;
-  topk_rows_kernel<<<a.rows, kTopkThreads, 0, st>>>(a);
+  const int rows = a.split > 0 ? 2 * a.split : a.rows;
+  if (rows <= 0) return SA_OK;
+  topk_rows_kernel<<<rows, kTopkThreads, 0, st>>>(a);
   return check_launch("topk_rows_kernel");
 }
 

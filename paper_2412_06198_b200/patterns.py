@@ -314,7 +314,7 @@ def _block_rows(m: AttnMatrices, b: int, k_b: int) -> list[list[int]]:
     q, k, _ = m.staged()
     nb = _num_blocks(n, b)
     qp = torch.empty((1, nb, 384), dtype=torch.bfloat16, device=q.device)
-    kp = torch.empty((1, nb, 384), dtype=torch.bfloat16, device=q.device)
+    kp = torch.empty((1, nb, 256), dtype=torch.bfloat16, device=q.device)
     st = D.stream()
     _lib.call("sa_block_pool", 1, n, b, 0, q.data_ptr(), qp.data_ptr(), None, st)
     _lib.call("sa_block_pool", 1, n, b, 1, k.data_ptr(), kp.data_ptr(), None, st)

@@ -210,7 +210,7 @@ def device_block_rows(q, k, b, k_b):
     st = torch.cuda.current_stream().cuda_stream
     qd, kd = to_dev(q[None]), to_dev(k[None])
     qp = torch.empty((1, nb, 384), dtype=torch.bfloat16, device="cuda")
-    kp = torch.empty((1, nb, 384), dtype=torch.bfloat16, device="cuda")
+    kp = torch.empty((1, nb, 256), dtype=torch.bfloat16, device="cuda")
     _lib.call("sa_block_pool", 1, n, b, 0, qd.data_ptr(), qp.data_ptr(), None, st)
     _lib.call("sa_block_pool", 1, n, b, 1, kd.data_ptr(), kp.data_ptr(), None, st)
     idx = torch.empty((nb, k_b + 1), dtype=torch.int32, device="cuda")
