@@ -37,34 +37,63 @@ namespace sa {
 constexpr int kSplitQ = 384;  // query operand [hi | lo | hi]
 constexpr int kSplitKey = 256;  // key operand [hi | lo]
 
-// out: [G, nb, 384] bf16 split operand; mean_out (optional): [G, nb, 128] fp32
+// One warp per (group, block): lane l pools d = 4l .. 4l+3 over the block's
+// rows with 8-byte loads (a 256-byte coalesced row per warp step), fp32 sums.
+// out: side 0 -> [G, nb, 384] = [hi | lo | hi]; side 1 -> [G, nb, 256] = [hi | lo].
 __global__ void block_pool_kernel(const __nv_bfloat16* __restrict__ x, int G, int n, int b,
                                   int side, __nv_bfloat16* __restrict__ out, float* mean_out,
                                   const int32_t* gate, int gate_val) {
   const int nb = (n + b - 1) / b;
-  const long long gid = (long long)blockIdx.x * blockDim.y + threadIdx.y;  // (g, block)
+  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // (g, block)
+  const int lane = threadIdx.x & 31;
   if (gid >= (long long)G * nb) return;
   const int g = (int)(gid / nb), blk = (int)(gid % nb);
   if (gate && gate[g] != gate_val) return;
-  const int d = threadIdx.x;  // 0..127
   const int r0 = blk * b, r1 = min(n, r0 + b);
-  const __nv_bfloat16* src = x + ((long long)g * n + r0) * kHeadDim + d;
-  float acc = 0.f;
-  for (int r = r0; r < r1; ++r, src += kHeadDim) acc += __bfloat162float(*src);
-  const float mean = acc / (float)(r1 - r0);
-  const __nv_bfloat16 hi = __float2bfloat16_rn(mean);
-  const __nv_bfloat16 lo = __float2bfloat16_rn(mean - __bfloat162float(hi));
-  if (side == 0) {
-    __nv_bfloat16* o = out + ((long long)g * nb + blk) * kSplitQ + d;
-    o[0] = hi;
-    o[128] = lo;
-    o[256] = hi;
-  } else {
-    __nv_bfloat16* o = out + ((long long)g * nb + blk) * kSplitKey + d;
-    o[0] = hi;
-    o[128] = lo;
+  const uint2* src = reinterpret_cast<const uint2*>(x + ((long long)g * n + r0) * kHeadDim) + lane;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  int r = r0;
+  for (; r + 4 <= r1; r += 4) {
+    uint2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(src + (size_t)(r - r0 + u) * (kHeadDim / 4));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const __nv_bfloat162 lo2 = *reinterpret_cast<const __nv_bfloat162*>(&v[u].x);
+      const __nv_bfloat162 hi2 = *reinterpret_cast<const __nv_bfloat162*>(&v[u].y);
+      acc[0] += __low2float(lo2);
+      acc[1] += __high2float(lo2);
+      acc[2] += __low2float(hi2);
+      acc[3] += __high2float(hi2);
+    }
   }
-  if (mean_out) mean_out[((long long)g * nb + blk) * kHeadDim + d] = mean;
+  for (; r < r1; ++r) {
+    const uint2 v = __ldg(src + (size_t)(r - r0) * (kHeadDim / 4));
+    const __nv_bfloat162 lo2 = *reinterpret_cast<const __nv_bfloat162*>(&v.x);
+    const __nv_bfloat162 hi2 = *reinterpret_cast<const __nv_bfloat162*>(&v.y);
+    acc[0] += __low2float(lo2);
+    acc[1] += __high2float(lo2);
+    acc[2] += __low2float(hi2);
+    acc[3] += __high2float(hi2);
+  }
+  const float inv_cnt = 1.0f / (float)(r1 - r0);
+  __nv_bfloat16 hi[4], lo[4];
+  float mean[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    mean[u] = acc[u] * inv_cnt;
+    hi[u] = __float2bfloat16_rn(mean[u]);
+    lo[u] = __float2bfloat16_rn(mean[u] - __bfloat162float(hi[u]));
+  }
+  const int width = side == 0 ? kSplitQ : kSplitKey;
+  __nv_bfloat16* o = out + ((long long)g * nb + blk) * width + 4 * lane;
+  *reinterpret_cast<uint2*>(o) = *reinterpret_cast<uint2*>(hi);
+  *reinterpret_cast<uint2*>(o + 128) = *reinterpret_cast<uint2*>(lo);
+  if (side == 0) *reinterpret_cast<uint2*>(o + 256) = *reinterpret_cast<uint2*>(hi);
+  if (mean_out) {
+    float* mo = mean_out + ((long long)g * nb + blk) * kHeadDim + 4 * lane;
+    *reinterpret_cast<float4*>(mo) = make_float4(mean[0], mean[1], mean[2], mean[3]);
+  }
 }
 
 struct BlockScoreArgs {
@@ -201,7 +230,32 @@ __global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid
       if (!valid) continue;
       const int g0 = j * kTile;
       const int lim = gq - g0;  // block-causal: gk <= gq
-      if (FUSED) {
+      if (FUSED && K == 1) {
+        // tile max by an FMNMX3 tree, then the first column holding it (lowest
+        // id wins ties, as does the strict > against the running best)
+        float v[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int u = 0; u < 32; ++u)
+            v[32 * c + u] = (32 * c + u <= lim) ? __uint_as_float(s[c][u]) * a.scale : -INFINITY;
+        float m8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float m = v[16 * q];
+#pragma unroll
+          for (int u = 1; u < 16; u += 2) m = fmax3(m, v[16 * q + u], v[16 * q + u + 1 < 16 * q + 16 ? 16 * q + u + 1 : 16 * q + u]);
+          m8[q] = m;
+        }
+        const float tm = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+        if (tm > bv[0]) {
+          int first = 127;
+#pragma unroll
+          for (int c = 127; c >= 0; --c) first = (v[c] == tm) ? c : first;
+          bv[0] = tm;
+          bi[0] = g0 + first;
+        }
+      } else if (FUSED) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -341,10 +395,9 @@ int launch_block_pool(int groups, int n, int b, int side, const void* x, void* s
   if (groups < 1 || n < 1) return fail(SA_ERR_DIMENSION, "bad pool shape");
   if (b < 1 || b > n) return fail(SA_ERR_PATTERN_PARAM, "b must be in [1, %d], got %d", n, b);
   const int nb = (n + b - 1) / b;
-  const long long items = (long long)groups * nb;
-  dim3 block(128, 2);
-  const long long grid = (items + 1) / 2;
-  block_pool_kernel<<<(unsigned)grid, block, 0, st>>>(
+  const long long items = (long long)groups * nb;  // one warp each
+  const long long grid = (items * 32 + 255) / 256;
+  block_pool_kernel<<<(unsigned)grid, 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), groups, n, b, side,
       reinterpret_cast<__nv_bfloat16*>(split_out), mean_out, gate, gate_val);
   return check_launch("block_pool_kernel");

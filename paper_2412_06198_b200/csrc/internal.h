@@ -34,6 +34,7 @@ struct TopkArgs {
   uint32_t* bits2;
   int bit_base2;
   int bit_neg2;
+  int smem_keys;  // set by launch_topk: rows up to this length are cached in shared memory
 };
 
 int launch_topk(const TopkArgs& a, cudaStream_t st);

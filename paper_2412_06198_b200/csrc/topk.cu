@@ -19,6 +19,7 @@
 namespace sa {
 
 constexpr int kTopkThreads = 1024;
+constexpr int kTopkSmemKeys = 53248;  // 208 KB of cached keys per row
 
 __device__ __forceinline__ uint32_t pref_key(float f) {
   uint32_t b = __float_as_uint(f);
@@ -81,6 +82,28 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
   int k = a.ks ? a.ks[r] : kk;
   k = k < len ? k : len;
   const float* s = scores + (long long)r * a.ld;
+  // Rows that fit are staged once into shared memory as preference keys
+  // (coalesced, many loads in flight); every radix pass and the compaction
+  // then read shared memory instead of re-walking global memory.
+  extern __shared__ uint32_t kcache[];
+  const bool cached = len <= a.smem_keys;
+  if (cached) {
+    for (int j0 = threadIdx.x; j0 < len; j0 += 4 * blockDim.x) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u * blockDim.x;
+        v[u] = j < len ? s[j] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u * blockDim.x;
+        if (j < len) kcache[j] = pref_key(v[u]);
+      }
+    }
+    __syncthreads();
+  }
+  auto key_at = [&](int j) -> uint32_t { return cached ? kcache[j] : pref_key(__ldg(s + j)); };
   __shared__ int hist[256];
   __shared__ int warp_tot[33];
   __shared__ uint32_t sh_digit;
@@ -99,7 +122,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
       const int len_pad = (len + 31) & ~31;
       for (int j = threadIdx.x; j < len_pad; j += blockDim.x) {
         const bool in = j < len;
-        const uint32_t key = in ? pref_key(s[j]) : 0u;
+        const uint32_t key = in ? key_at(j) : 0u;
         const bool hit = in && ((key & mask) == prefix);
         const uint32_t bin = hit ? ((key >> shift) & 255u) : 256u;
         const uint32_t peers = __match_any_sync(0xffffffffu, bin);
@@ -153,7 +176,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
   int n_eq = 0, n_gt = 0;
   if (!take_all && k > 0) {
     for (int j = b0; j < b1; ++j) {
-      const uint32_t key = pref_key(s[j]);
+      const uint32_t key = key_at(j);
       n_gt += key > T;
       n_eq += key == T;
     }
@@ -172,7 +195,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
       if (take_all) {
         keep = true;
       } else {
-        const uint32_t key = pref_key(s[j]);
+        const uint32_t key = key_at(j);
         keep = key > T;
         if (key == T) {
           keep = eq_seen < keep_eq;
@@ -195,7 +218,14 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
 int launch_topk(const TopkArgs& a, cudaStream_t st) {
   const int rows = a.split > 0 ? 2 * a.split : a.rows;
   if (rows <= 0) return SA_OK;
-  topk_rows_kernel<<<rows, kTopkThreads, 0, st>>>(a);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(topk_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopkSmemKeys * 4);
+    attr = true;
+  }
+  TopkArgs b = a;
+  b.smem_keys = kTopkSmemKeys;
+  topk_rows_kernel<<<rows, kTopkThreads, kTopkSmemKeys * 4, st>>>(b);
   return check_launch("topk_rows_kernel");
 }
 
