@@ -244,13 +244,14 @@ def run_ours(args):
     from paper_2412_06198_b200 import _lib, runtime as R
     from paper_2412_06198_b200.patterns import BlockSparse, Triangular, VerticalSlash
 
+    from paper_2412_06198_b200.multigpu import gather_heads, shard_heads
+
     n = args.ctx
     hk_l = HK // world
     h_l = H // world
     q, k, v = synth_inputs(args.seed, n)
-    qs = q[rank * h_l:(rank + 1) * h_l]
-    ks = k[rank * hk_l:(rank + 1) * hk_l]
-    vs = v[rank * hk_l:(rank + 1) * hk_l]
+    q_sl, kv_sl = shard_heads(rank, world, H, HK)
+    qs, ks, vs = q[q_sl], k[kv_sl], v[kv_sl]
     # pinned host copies (e2e) and resident device copies (value)
     q_h = torch.from_numpy(np.ascontiguousarray(qs)).bfloat16().pin_memory()
     k_h = torch.from_numpy(np.ascontiguousarray(ks)).bfloat16().pin_memory()
@@ -268,8 +269,7 @@ def run_ours(args):
     plan = R.PrefillPlan(1, h_l, hk_l, n, D, mode, fixed_pattern=fixed)
     ws = R._workspace(plan.ws_bytes, dev)
     out = torch.empty((1, n, h_l * D), dtype=torch.bfloat16, device=dev)
-    gathered = torch.empty((world, n, h_l * D), dtype=torch.bfloat16, device=dev) if world > 1 else None
-    final = torch.empty((1, n, H * D), dtype=torch.bfloat16, device=dev) if world > 1 else None
+    final = torch.empty((n, H * D), dtype=torch.bfloat16, device=dev) if world > 1 else None
 
     def step(events=None):
         if events is not None:
@@ -284,8 +284,7 @@ def run_ours(args):
             for i in range(5):
                 plan.desc.stage_events[i] = None
         if world > 1:
-            dist.all_gather_into_tensor(gathered, out[0])
-            final.view(n, world, h_l * D).copy_(gathered.permute(1, 0, 2))
+            gather_heads(out[0], world, out=final)
         if events is not None:
             events[6].record()
 
