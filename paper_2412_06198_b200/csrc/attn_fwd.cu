@@ -11,14 +11,17 @@
 // exactly 0" (patterns.py:353-435 docstring) and the column-wins dedupe
 // (a position is one element of the union, evaluated once).
 //
-// Per CTA: one (head, 128-row query tile).  192 threads:
+// Per CTA: one (head, 128-row query tile); every listed 128-key tile is
+// processed as two 64-key sub-tiles u.  192 threads:
 //   warps 0-3  softmax: thread r owns query row r (TMEM lane r)
-//   warp  4    TMA producer: Q once, then K_j / V_j into two 32 KB slots
+//   warp  4    TMA producer: Q once, then K_u / V_u through a 5-slot 16 KB ring
 //   warp  5    TMEM allocator + single-thread tcgen05.mma issuer
-// TMEM (256 columns): S = Q K^T fp32 at col 0 (P = bf16(softmax) aliased
-// over cols 0..63), O accumulator at col 128.  Two CTAs co-reside per SM
-// (96 KB smem, 256 TMEM columns each), so one CTA's softmax overlaps the
-// other CTA's MMAs.
+// TMEM (256 columns): S double buffer (2 x 64 fp32 columns, P = bf16 softmax
+// aliased over the first 32 columns of its buffer) and O (128 columns).  The
+// MMA warp issues QK(u+2) right after PV(u), so the tensor core computes the
+// next logits while the softmax warps work on the current ones; two CTAs
+// co-reside per SM (113 KB smem, 256 TMEM columns each) and hide each other's
+// prologue/epilogue.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -33,8 +36,8 @@ namespace sa {
 
 struct AttnArgs {
   CUtensorMap tmap_q;  // [HH, n, 128] bf16, box {64, 128, 1}, SW128
-  CUtensorMap tmap_k;  // [HK, n, 128]
-  CUtensorMap tmap_v;  // [HK, n, 128]
+  CUtensorMap tmap_k;  // [HK, n, 128], box {64, 64, 1}
+  CUtensorMap tmap_v;  // [HK, n, 128], box {64, 64, 1}
   __nv_bfloat16* out;
   long long out_batch_stride;  // elements between batches
   long long out_row_stride;    // elements between rows (H * 128 for (B, L, H*d))
@@ -55,16 +58,26 @@ struct AttnArgs {
 
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kColS = 0;
-constexpr uint32_t kColP = 0;
+constexpr uint32_t kColS = 0;    // S buffers at 0 and 64 (P aliased at their first 32 columns)
 constexpr uint32_t kColO = 128;
+constexpr int kSub = 64;         // keys per sub-tile
+constexpr int kRing = 5;         // K/V ring slots of 16 KB
+constexpr int kSlotBytes = 16384;
 constexpr int kSmemQ = 0;
-constexpr int kSmemK = 32768;
-constexpr int kSmemV = 65536;
-constexpr int kSmemBar = 98304;
-constexpr int kSmemBytes = kSmemBar + 128 + 1024;  // + barriers + alignment slack
+constexpr int kSmemRing = 32768;
+constexpr int kSmemBar = kSmemRing + kRing * kSlotBytes;           // 114688
+constexpr int kSmemBytes = kSmemBar + 256;  // + barriers; base is 1024-aligned (two CTAs per SM must fit)
 
-enum Bar { B_Q = 0, B_KF, B_KE, B_VF, B_VE, B_SF, B_PF, B_OF, B_NUM };
+enum Bar {
+  B_Q = 0,
+  B_FULL0 = 1,                 // kRing
+  B_EMPTY0 = B_FULL0 + kRing,  // kRing
+  B_SF0 = B_EMPTY0 + kRing,    // 2
+  B_PF0 = B_SF0 + 2,           // 2
+  B_OD = B_PF0 + 2,            // O updated by PV(u)
+  B_OF = B_OD + 1,             // final O
+  B_NUM = B_OF + 1
+};
 
 __device__ __forceinline__ void build_row_mask(const AttnArgs& a, uint32_t kind, int hh, int i,
                                                int j0, int qt, int kt, uint32_t (&m)[4]) {
@@ -136,12 +149,11 @@ __device__ __forceinline__ void build_row_mask(const AttnArgs& a, uint32_t kind,
 }
 
 __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem) & 1023u) != 0u) __trap();  // SWIZZLE_128B tiles need 1024-byte alignment
   uint8_t* sQ = smem + kSmemQ;
-  uint8_t* sK = smem + kSmemK;
-  uint8_t* sV = smem + kSmemV;
+  uint8_t* sRing = smem + kSmemRing;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + B_NUM);
 
@@ -165,16 +177,20 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
   const int h = hh % a.heads;
   const int hkv = bidx * a.kv_heads + h / (a.heads / a.kv_heads);
   const int cnt = a.tile_cnt[item];
+  const int nsub = 2 * cnt;
   const uint32_t* tl = a.tiles + a.tile_off[item];
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[B_Q], 1);
-    mbar_init(&bars[B_KF], 1);
-    mbar_init(&bars[B_KE], 1);
-    mbar_init(&bars[B_VF], 1);
-    mbar_init(&bars[B_VE], 1);
-    mbar_init(&bars[B_SF], 1);
-    mbar_init(&bars[B_PF], 128);
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&bars[B_FULL0 + i], 1);
+      mbar_init(&bars[B_EMPTY0 + i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars[B_SF0 + i], 1);
+      mbar_init(&bars[B_PF0 + i], 128);
+    }
+    mbar_init(&bars[B_OD], 1);
     mbar_init(&bars[B_OF], 1);
     fence_barrier_init();
   }
@@ -193,52 +209,60 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       mbar_arrive_expect_tx(&bars[B_Q], 32768);
       tma_load_3d(sQ, &a.tmap_q, &bars[B_Q], 0, qt * kTile, hh);
       tma_load_3d(sQ + 16384, &a.tmap_q, &bars[B_Q], 64, qt * kTile, hh);
-      for (int j = 0; j < cnt; ++j) {
-        const int row = (int)tile_ktile(tl[j]) * kTile;
-        if (a.dbg) a.dbg[blockIdx.x * 8 + 0] = j + 1;
-        if (j > 0) mbar_wait(&bars[B_KE], (j - 1) & 1);
-        mbar_arrive_expect_tx(&bars[B_KF], 32768);
-        tma_load_3d(sK, &a.tmap_k, &bars[B_KF], 0, row, hkv);
-        tma_load_3d(sK + 16384, &a.tmap_k, &bars[B_KF], 64, row, hkv);
-        if (j > 0) mbar_wait(&bars[B_VE], (j - 1) & 1);
-        mbar_arrive_expect_tx(&bars[B_VF], 32768);
-        tma_load_3d(sV, &a.tmap_v, &bars[B_VF], 0, row, hkv);
-        tma_load_3d(sV + 16384, &a.tmap_v, &bars[B_VF], 64, row, hkv);
+      // ring sequence: K_0, V_0, K_1, V_1, ... (sub-tiles u = 2 j + half)
+      for (int i = 0; i < 2 * nsub; ++i) {
+        const int u = i >> 1;
+        const int slot = i % kRing;
+        if (i >= kRing) mbar_wait(&bars[B_EMPTY0 + slot], ((i / kRing) - 1) & 1);
+        const int row = (int)tile_ktile(tl[u >> 1]) * kTile + (u & 1) * kSub;
+        const CUtensorMap* map = (i & 1) ? &a.tmap_v : &a.tmap_k;
+        uint8_t* dst = sRing + slot * kSlotBytes;
+        mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
+        tma_load_3d(dst, map, &bars[B_FULL0 + slot], 0, row, hkv);
+        tma_load_3d(dst + 8192, map, &bars[B_FULL0 + slot], 64, row, hkv);
       }
     }
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
-      constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(128, kSub, 0, 0);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
-      const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+      const uint32_t q_addr = smem_u32(sQ);
+      const uint32_t ring_addr = smem_u32(sRing);
+      auto issue_qk = [&](int u) {
+        const int i = 2 * u, slot = i % kRing;
+        mbar_wait(&bars[B_FULL0 + slot], (i / kRing) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = ring_addr + slot * kSlotBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          mma_ss(tbase + kColS + (u & 1) * kSub,
+                 sdesc_sw128(q_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                 sdesc_sw128(k_addr + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_qk,
+                 kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&bars[B_EMPTY0 + slot]);
+        mma_commit(&bars[B_SF0 + (u & 1)]);
+      };
       mbar_wait(&bars[B_Q], 0);
       tc_fence_after();
-      for (int j = 0; j < cnt; ++j) {
-        if (a.dbg) a.dbg[blockIdx.x * 8 + 1] = j + 1;
-        mbar_wait(&bars[B_KF], j & 1);
-        if (a.dbg) a.dbg[blockIdx.x * 8 + 2] = j + 1;
+      issue_qk(0);
+      if (nsub > 1) issue_qk(1);
+      for (int u = 0; u < nsub; ++u) {
+        mbar_wait(&bars[B_PF0 + (u & 1)], (u >> 1) & 1);
+        const int i = 2 * u + 1, slot = i % kRing;
+        mbar_wait(&bars[B_FULL0 + slot], (i / kRing) & 1);
         tc_fence_after();
+        const uint32_t v_addr = ring_addr + slot * kSlotBytes;
+        const uint32_t p_addr = tbase + kColS + (u & 1) * kSub;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          mma_ss(tbase + kColS, sdesc_sw128(q_addr + off, 16, 1024),
-                 sdesc_sw128(k_addr + off, 16, 1024), idesc_qk, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk) {
+          mma_ts(tbase + kColO, p_addr + kk * 8, sdesc_sw128(v_addr + kk * 2048, 8192, 1024),
+                 idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
         }
-        mma_commit(&bars[B_KE]);
-        mma_commit(&bars[B_SF]);
-        mbar_wait(&bars[B_PF], j & 1);
-        if (a.dbg) a.dbg[blockIdx.x * 8 + 3] = j + 1;
-        tc_fence_after();
-        mbar_wait(&bars[B_VF], j & 1);
-        if (a.dbg) a.dbg[blockIdx.x * 8 + 4] = j + 1;
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_ts(tbase + kColO, tbase + kColP + kk * 8, sdesc_sw128(v_addr + kk * 2048, 16384, 1024),
-                 idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        mma_commit(&bars[B_VE]);
+        mma_commit(&bars[B_EMPTY0 + slot]);
+        mma_commit(&bars[B_OD]);
+        if (u + 2 < nsub) issue_qk(u + 2);
       }
       mma_commit(&bars[B_OF]);
     }
@@ -250,56 +274,68 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     const float sl2 = a.scale_log2;
     float m_used = -INFINITY;
     float l = 0.f;
-    for (int j = 0; j < cnt; ++j) {
-      const uint32_t e = tl[j];
-      const uint32_t kind = tile_kind(e);
-      const int kt = (int)tile_ktile(e);
-      const int j0 = kt * kTile;
-      uint32_t msk[4];
-      if (kind != TK_FULL) build_row_mask(a, kind, hh, i, j0, qt, kt, msk);
-
-      if (a.dbg && r == 0) a.dbg[blockIdx.x * 8 + 5] = j + 1;
-      mbar_wait(&bars[B_SF], j & 1);
-      if (a.dbg && r == 0) a.dbg[blockIdx.x * 8 + 6] = j + 1;
+    uint32_t msk[4] = {0u, 0u, 0u, 0u};
+    uint32_t kind = TK_FULL;
+    for (int u = 0; u < nsub; ++u) {
+      const int half = u & 1;
+      if (half == 0) {
+        const uint32_t e = tl[u >> 1];
+        kind = tile_kind(e);
+        const int kt = (int)tile_ktile(e);
+        if (kind != TK_FULL) build_row_mask(a, kind, hh, i, kt * kTile, qt, kt, msk);
+      }
+      mbar_wait(&bars[B_SF0 + half], (u >> 1) & 1);
       tc_fence_after();
-      uint32_t s[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tbase + lane_off + kColS + 32 * c, s[c]);
+      uint32_t s[2][32];
+      const uint32_t s_col = tbase + lane_off + kColS + half * kSub;
+      tmem_ld32(s_col, s[0]);
+      tmem_ld32(s_col + 32, s[1]);
       tmem_ld_wait();
       if (kind != TK_FULL) {
+        const uint32_t m0 = msk[2 * half], m1 = msk[2 * half + 1];
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (!((msk[c] >> t) & 1u)) s[c][t] = __float_as_uint(-INFINITY);
+        for (int t = 0; t < 32; ++t) {
+          if (!((m0 >> t) & 1u)) s[0][t] = __float_as_uint(-INFINITY);
+          if (!((m1 >> t) & 1u)) s[1][t] = __float_as_uint(-INFINITY);
+        }
       }
       // row max: four independent FMNMX3 chains
       float mx;
       {
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-          for (int t = 0; t < 32; t += 2)
-            m4[c] = fmax3(m4[c], __uint_as_float(s[c][t]), __uint_as_float(s[c][t + 1]));
+          for (int t = 0; t < 32; t += 4) {
+            m4[2 * c] = fmax3(m4[2 * c], __uint_as_float(s[c][t]), __uint_as_float(s[c][t + 1]));
+            m4[2 * c + 1] = fmax3(m4[2 * c + 1], __uint_as_float(s[c][t + 2]), __uint_as_float(s[c][t + 3]));
+          }
         mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
       }
       const float mt = mx * sl2;
       // Lazy rescale: keep a stale max until the row max grows by > 2^8.  The
-      // decision is made per row but the TMEM round trip of O is warp-wide
-      // (tcgen05.ld/st are .sync.aligned), so rows that need no rescale use 1.
+      // decision is per row but the TMEM round trip of O is warp-wide
+      // (tcgen05.ld/st are .sync.aligned), so rows that need none use 1.
       const bool need = mt > m_used + 8.0f;
       if (__any_sync(0xffffffffu, need)) {
         const float alpha = need ? fast_exp2(m_used - mt) : 1.0f;  // 0 when m_used == -inf
         l *= alpha;
-        if (j > 0) {
+        if (u > 0) {
+          // PV(u-1) may still be accumulating into O (PV(u-2) completed before S_u)
+          mbar_wait(&bars[B_OD], (u - 1) & 1);
+          tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             uint32_t o[32];
             tmem_ld32(tbase + lane_off + kColO + 32 * c, o);
             tmem_ld_wait();
 #pragma unroll
-            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+            for (int t = 0; t < 32; t += 2) {
+              const float2 v = fmul2(make_float2(__uint_as_float(o[t]), __uint_as_float(o[t + 1])),
+                                     make_float2(alpha, alpha));
+              o[t] = __float_as_uint(v.x);
+              o[t + 1] = __float_as_uint(v.y);
+            }
             tmem_st32(tbase + lane_off + kColO + 32 * c, o);
           }
           tmem_st_wait();
@@ -312,27 +348,26 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       const float2 mo2 = make_float2(-moff, -moff);
       float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                        make_float2(0.f, 0.f)};
-      uint32_t p[2][32];
+      uint32_t p[32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int t = 0; t < 32; t += 2) {
           float2 x = ffma2(make_float2(__uint_as_float(s[c][t]), __uint_as_float(s[c][t + 1])), sc2, mo2);
           x.x = fast_exp2(x.x);
           x.y = fast_exp2(x.y);
           acc[(t >> 1) & 3] = fadd2(acc[(t >> 1) & 3], x);
-          p[c >> 1][(c & 1) * 16 + (t >> 1)] = pack_bf16(x.x, x.y);
+          p[c * 16 + (t >> 1)] = pack_bf16(x.x, x.y);
         }
       {
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
-        const float2 a = fadd2(a01, a23);
-        l += a.x + a.y;
+        const float2 t2 = fadd2(a01, a23);
+        l += t2.x + t2.y;
       }
-      tmem_st32(tbase + lane_off + kColP, p[0]);
-      tmem_st32(tbase + lane_off + kColP + 32, p[1]);
+      tmem_st32(s_col, p);  // P (bf16 pairs) over the first 32 columns of this S buffer
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&bars[B_PF]);
+      mbar_arrive(&bars[B_PF0 + half]);
     }
     // ------------------------------------------------------------ epilogue
     mbar_wait(&bars[B_OF], 0);
@@ -392,8 +427,8 @@ extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float s
   memset(&a, 0, sizeof(a));
   int st;
   if ((st = make_tmap_3d_bf16(&a.tmap_q, q, kHeadDim, n, batch * heads, kTile))) return st;
-  if ((st = make_tmap_3d_bf16(&a.tmap_k, k, kHeadDim, n, batch * kv_heads, kTile))) return st;
-  if ((st = make_tmap_3d_bf16(&a.tmap_v, v, kHeadDim, n, batch * kv_heads, kTile))) return st;
+  if ((st = make_tmap_3d_bf16(&a.tmap_k, k, kHeadDim, n, batch * kv_heads, kSub))) return st;
+  if ((st = make_tmap_3d_bf16(&a.tmap_v, v, kHeadDim, n, batch * kv_heads, kSub))) return st;
   a.out = reinterpret_cast<__nv_bfloat16*>(out);
   a.out_row_stride = (long long)heads * kHeadDim;
   a.out_batch_stride = (long long)n * heads * kHeadDim;
@@ -409,7 +444,7 @@ extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float s
   a.work = nullptr;
   a.idx = *index;
   a.lse = lse;
-  a.dbg = reinterpret_cast<volatile int*>(sa_attn_dbg_ptr);
+  a.dbg = nullptr;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
