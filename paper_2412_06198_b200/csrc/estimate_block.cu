@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -403,10 +404,20 @@ int launch_block_pool(int groups, int n, int b, int side, const void* x, void* s
   return check_launch("block_pool_kernel");
 }
 
-size_t block_select_ws(int n, int b, int k_b) {
+// MATERIALIZE path: logits of up to kMatHeads heads at a time (<= ~1 GB).
+static int mat_heads(int nb, int hh_total) {
+  const long long per = (long long)nb * nb * 4 + (long long)nb * 64;
+  long long g = (1ll << 30) / per;
+  if (g < 1) g = 1;
+  if (g > hh_total) g = hh_total;
+  return (int)g;
+}
+
+size_t block_select_ws(int n, int b, int k_b, int hh_total) {
   const int nb = (n + b - 1) / b;
   if (k_b <= 8) return 256;
-  return (size_t)nb * nb * 4 + (size_t)nb * k_b * 4 + (size_t)nb * 8 + 1024;
+  const long long g = mat_heads(nb, hh_total);
+  return (size_t)g * ((size_t)nb * nb * 4 + (size_t)nb * k_b * 4 + (size_t)nb * 8) + 1024;
 }
 
 int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b, float scale,
@@ -465,39 +476,41 @@ int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_
     else block_score_kernel<8, true><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
     return check_launch("block_score_kernel<fused>");
   }
-  // MATERIALIZE, one head at a time through the workspace
-  const size_t need = block_select_ws(n, b, k_b);
+  // MATERIALIZE, heads in groups of G through the workspace
+  const int G = mat_heads(nb, hh_total);
+  const size_t need = block_select_ws(n, b, k_b, hh_total);
   if (!ws || ws_bytes < need) return fail(SA_ERR_DIMENSION, "block_select workspace too small");
   char* p = reinterpret_cast<char*>(ws);
   float* logits = reinterpret_cast<float*>(p);
-  p += (size_t)nb * nb * 4;
+  p += (size_t)G * nb * nb * 4;
   int32_t* topk = reinterpret_cast<int32_t*>(p);
-  p += (size_t)nb * k_b * 4;
+  p += (size_t)G * nb * k_b * 4;
   int32_t* lens = reinterpret_cast<int32_t*>(p);
-  int32_t* ks = lens + nb;
-  seg_lens_kernel<<<(nb + 255) / 256, 256, 0, st>>>(lens, ks, nb, nb, k_b);
+  int32_t* ks = lens + (size_t)G * nb;
+  seg_lens_kernel<<<(G * nb + 255) / 256, 256, 0, st>>>(lens, ks, G * nb, nb, k_b);
   a.logits = logits;
-  a.hh_count = 1;
-  for (int hh = 0; hh < hh_total; ++hh) {
-    a.hh_base = hh;
-    dim3 grid(a.nqt, 1);
+  for (int h0 = 0; h0 < hh_total; h0 += G) {
+    const int cnt = std::min(G, hh_total - h0);
+    a.hh_base = h0;
+    a.hh_count = cnt;
+    dim3 grid(a.nqt, cnt);
     block_score_kernel<1, false><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
     if ((rc = check_launch("block_score_kernel<materialize>"))) return rc;
     TopkArgs t{};
     t.scores = logits;
     t.ld = nb;
-    t.rows = nb;
+    t.rows = cnt * nb;
     t.n = nb;
     t.lens = lens;
     t.ks = ks;
     t.idx_out = topk;
     t.out_ld = k_b;
-    t.gate = gate ? gate + hh : nullptr;
-    t.gate_div = nb;  // every row of this head maps to gate[hh]
+    t.gate = gate ? gate + h0 : nullptr;
+    t.gate_div = nb;  // row r belongs to head h0 + r / nb
     t.gate_val = gate_val;
     if ((rc = launch_topk(t, st))) return rc;
-    merge_diag_kernel<<<(nb + 255) / 256, 256, 0, st>>>(topk, k_b, nb, blk_idx, head_stride, hh, 1,
-                                                       gate, gate_val);
+    merge_diag_kernel<<<(cnt * nb + 255) / 256, 256, 0, st>>>(topk, k_b, nb, blk_idx, head_stride, h0,
+                                                              cnt, gate, gate_val);
     if ((rc = check_launch("merge_diag_kernel"))) return rc;
   }
   return SA_OK;
@@ -512,7 +525,7 @@ extern "C" int sa_block_pool(int groups, int n, int b, int side, const void* x, 
 }
 
 extern "C" size_t sa_block_select_workspace(int n, int b, int k_b) {
-  return sa::block_select_ws(n, b, k_b);
+  return sa::block_select_ws(n, b, k_b, 1);
 }
 
 extern "C" int sa_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b,

@@ -48,7 +48,7 @@ int tail_pick_chunks(int r_hi);
 
 int launch_block_pool(int groups, int n, int b, int side, const void* x, void* split_out,
                       float* mean_out, const int32_t* gate, int gate_val, cudaStream_t st);
-size_t block_select_ws(int n, int b, int k_b);
+size_t block_select_ws(int n, int b, int k_b, int hh_total);
 int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b, float scale,
                         const void* qp, const void* kp, int32_t* blk_idx, long long head_stride,
                         int32_t* blk_row_off, int row_stride, const int32_t* gate, int gate_val,

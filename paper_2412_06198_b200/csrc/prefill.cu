@@ -127,7 +127,7 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
       const int nb = (n + pt.p1 - 1) / pt.p1;
       p->max_nb = std::max(p->max_nb, nb);
       head_stride = std::max(head_stride, (long long)nb * (pt.p2 + 1));
-      blk_ws = std::max(blk_ws, block_select_ws(n, pt.p1, pt.p2));
+      blk_ws = std::max(blk_ws, block_select_ws(n, pt.p1, pt.p2, p->hh));
     }
   }
   p->blk_row_stride = p->max_nb + 1;

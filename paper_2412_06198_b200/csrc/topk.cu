@@ -2,12 +2,22 @@
 // _top_k_stable (patterns.py:231-234): the k largest scores, ties resolved to
 // the LOWER index, returned in ascending index order.
 //
-// Per row (one CTA): map each score to a 32-bit preference key (larger key =
-// preferred; -0.0 == +0.0; NaN least preferred, matching numpy's argsort which
-// sorts NaN last), radix-select the k-th largest key T with four 8-bit MSB
-// passes, then one ordered compaction keeps every key > T plus the first
-// (k - #{key > T}) keys == T in index order.  The result is the exact set the
-// stable sort would return, independent of thread scheduling.
+// Every score maps to a 32-bit preference key (larger key = preferred;
+// -0.0 == +0.0; NaN least preferred, as numpy's argsort puts NaN last) and a
+// row element to the 64-bit composite (key << 32 | ~index), which is unique
+// and orders exactly like the stable sort.  Per row (one CTA) the k-th largest
+// composite T is found without sorting the row:
+//   1. one coalesced pass takes the key range [kmin, kmax];
+//   2. a 4096-bin histogram over that range (bins are monotone in the key, so
+//      scores of similar magnitude spread over many bins instead of colliding
+//      on a few radix digits) locates the bin holding the k-th key;
+//   3. that bin's composites (m of them) are gathered to shared memory; if
+//      m > 1024 the bin is split once more by a second 4096-bin histogram;
+//   4. the exact rank of each gathered composite is counted in parallel and
+//      the one with rank k - above is T.
+// Rows whose candidates stay above 1024 after two levels (massive exact ties)
+// use an exact 4 x 8-bit radix select.  Output: every j with composite >= T,
+// in index order, by a warp-ballot ordered compaction.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -19,7 +29,9 @@
 namespace sa {
 
 constexpr int kTopkThreads = 1024;
-constexpr int kTopkSmemKeys = 53248;  // 208 KB of cached keys per row
+constexpr int kBins = 4096;
+constexpr int kCand = 1024;
+constexpr int kTopkSmem = kBins * 4 + kCand * 8;  // 24 KB dynamic
 
 __device__ __forceinline__ uint32_t pref_key(float f) {
   uint32_t b = __float_as_uint(f);
@@ -28,7 +40,16 @@ __device__ __forceinline__ uint32_t pref_key(float f) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-// Exclusive block-wide scan of one int per thread (1024 threads).
+__device__ __forceinline__ uint64_t composite(uint32_t key, int j) {
+  return (static_cast<uint64_t>(key) << 32) | static_cast<uint32_t>(0xffffffffu - (uint32_t)j);
+}
+
+// bin of `key` in [lo, lo + span) split into kBins equal key intervals (monotone)
+__device__ __forceinline__ int key_bin(uint32_t key, uint32_t lo, uint64_t span) {
+  return (int)(((uint64_t)(key - lo) * kBins) / span);
+}
+
+// Exclusive block-wide scan of one int per thread (any warp count <= 32).
 __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int x = v;
@@ -40,14 +61,14 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
   if (lane == 31) warp_tot[w] = x;
   __syncthreads();
   if (w == 0) {
-    int t = warp_tot[lane];
+    int t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
     int s = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int y = __shfl_up_sync(0xffffffffu, s, o);
       if (lane >= o) s += y;
     }
-    warp_tot[lane] = s - t;  // exclusive warp offsets
+    warp_tot[lane] = s - t;
     if (lane == 31) warp_tot[32] = s;
   }
   __syncthreads();
@@ -57,7 +78,52 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
   return r;
 }
 
-
+// Histogram of the keys inside [lo, lo + span) into kBins bins; returns the bin
+// holding the `want`-th largest of them and the count in higher bins.
+__device__ void hist_locate(const float* s, int len, uint32_t lo, uint64_t span, int want,
+                            int* hist, int* warp_tot, int* sh_pair, int& bin_out, int& above_out) {
+  const int tid = threadIdx.x;
+  for (int t = tid; t < kBins; t += blockDim.x) hist[t] = 0;
+  __syncthreads();
+  for (int j0 = tid; j0 < len; j0 += 8 * blockDim.x) {
+    uint32_t key[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + u * blockDim.x;
+      key[u] = j < len ? pref_key(__ldg(s + j)) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + u * blockDim.x;
+      if (j < len && key[u] >= lo && (uint64_t)(key[u] - lo) < span)
+        atomicAdd(&hist[key_bin(key[u], lo, span)], 1);
+    }
+  }
+  __syncthreads();
+  // suffix counts: thread t owns bins [kBins - (t+1)*per, kBins - t*per), scanned from the top
+  const int per = kBins / blockDim.x;
+  const int b_hi = kBins - tid * per;
+  int mine = 0;
+  for (int q = 1; q <= per; ++q) mine += hist[b_hi - q];
+  int tot;
+  const int before = block_excl_scan(mine, warp_tot, tot);  // keys in higher bins
+  if (before < want && before + mine >= want) {
+    int run = before;
+    for (int q = 1; q <= per; ++q) {
+      const int b = b_hi - q;
+      if (run + hist[b] >= want) {
+        sh_pair[0] = b;
+        sh_pair[1] = run;
+        sh_pair[2] = hist[b];
+        break;
+      }
+      run += hist[b];
+    }
+  }
+  __syncthreads();
+  bin_out = sh_pair[0];
+  above_out = sh_pair[1];
+}
 
 __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
   int r = blockIdx.x;
@@ -82,150 +148,194 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
   int k = a.ks ? a.ks[r] : kk;
   k = k < len ? k : len;
   const float* s = scores + (long long)r * a.ld;
-  // Rows that fit are staged once into shared memory as preference keys
-  // (coalesced, many loads in flight); every radix pass and the compaction
-  // then read shared memory instead of re-walking global memory.
-  extern __shared__ uint32_t kcache[];
-  const bool cached = len <= a.smem_keys;
-  if (cached) {
-    for (int j0 = threadIdx.x; j0 < len; j0 += 4 * blockDim.x) {
-      float v[4];
+
+  extern __shared__ __align__(16) uint8_t tk_smem[];
+  int* hist = reinterpret_cast<int*>(tk_smem);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(tk_smem + kBins * 4);
+  __shared__ int warp_tot[33];
+  __shared__ uint32_t sh_min, sh_max;
+  __shared__ int sh_m;
+  __shared__ int sh_pair[3];
+  __shared__ uint64_t sh_T;
+  __shared__ uint32_t sh_digit;
+  __shared__ int sh_rem;
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool take_all = k >= len;
+  uint64_t T = 0;  // keep j iff composite(j) >= T
+  if (!take_all && k > 0) {
+    // 1. key range
+    uint32_t mn = 0xffffffffu, mx = 0u;
+    for (int j0 = tid; j0 < len; j0 += 8 * blockDim.x) {
+      float v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int j = j0 + u * blockDim.x;
-        v[u] = j < len ? s[j] : 0.f;
+        v[u] = j < len ? __ldg(s + j) : 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = j0 + u * blockDim.x;
-        if (j < len) kcache[j] = pref_key(v[u]);
+      for (int u = 0; u < 8; ++u) {
+        if (j0 + u * (int)blockDim.x < len) {
+          const uint32_t key = pref_key(v[u]);
+          mn = min(mn, key);
+          mx = max(mx, key);
+        }
       }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (tid == 0) {
+      sh_min = 0xffffffffu;
+      sh_max = 0u;
+    }
     __syncthreads();
-  }
-  auto key_at = [&](int j) -> uint32_t { return cached ? kcache[j] : pref_key(__ldg(s + j)); };
-  __shared__ int hist[256];
-  __shared__ int warp_tot[33];
-  __shared__ uint32_t sh_digit;
-  __shared__ int sh_remaining;
-
-  uint32_t prefix = 0u, mask = 0u;
-  int remaining = k;
-  bool take_all = (k >= len);
-  if (!take_all && k > 0) {
-    for (int pass = 0; pass < 4; ++pass) {
-      const int shift = 24 - 8 * pass;
-      for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0;
+    if (lane == 0) {
+      atomicMin(&sh_min, mn);
+      atomicMax(&sh_max, mx);
+    }
+    __syncthreads();
+    uint32_t lo = sh_min;
+    uint64_t span = (uint64_t)(sh_max - sh_min) + 1;
+    int want = k;  // rank (1-based) of T among the keys in [lo, lo + span)
+    bool located = false;
+    for (int level = 0; level < 2 && !located; ++level) {
+      int bin, above;
+      hist_locate(s, len, lo, span, want, hist, warp_tot, sh_pair, bin, above);
+      const int m = sh_pair[2];
+      want -= above;
+      // narrow the key range to the bin: keys with key_bin == bin
+      const uint64_t b0 = ((uint64_t)bin * span + kBins - 1) / kBins;
+      const uint64_t b1 = ((uint64_t)(bin + 1) * span + kBins - 1) / kBins;
+      lo = lo + (uint32_t)b0;
+      span = b1 - b0;
+      if (m > kCand) continue;
+      // 3. gather the bin's composites
+      if (tid == 0) sh_m = 0;
       __syncthreads();
-      // warp-aggregated histogram: scores of similar magnitude share their top
-      // bits, so lanes are matched on the bin and one leader adds the count
-      const int len_pad = (len + 31) & ~31;
-      for (int j = threadIdx.x; j < len_pad; j += blockDim.x) {
-        const bool in = j < len;
-        const uint32_t key = in ? key_at(j) : 0u;
-        const bool hit = in && ((key & mask) == prefix);
-        const uint32_t bin = hit ? ((key >> shift) & 255u) : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-        if (hit && (threadIdx.x & 31) == (__ffs(peers) - 1)) atomicAdd(&hist[bin], __popc(peers));
-      }
-      __syncthreads();
-      if (threadIdx.x < 32) {
-        // lane l owns digits [255 - 8l - 7, 255 - 8l]; find the digit where the
-        // running count from the top reaches `remaining`.
-        const int lane = threadIdx.x;
-        int c[8];
-        int tot = 0;
+      for (int j0 = tid; (j0 & ~31) < len; j0 += 8 * blockDim.x) {  // warp-uniform trip count
+        float v[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          c[q] = hist[255 - 8 * lane - q];
-          tot += c[q];
+        for (int u = 0; u < 8; ++u) {
+          const int j = j0 + u * blockDim.x;
+          v[u] = j < len ? __ldg(s + j) : 0.f;
         }
-        int incl = tot;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int excl = incl - tot;  // count strictly above this lane's digits
-        if (excl < remaining && incl >= remaining) {
-          int run = excl;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            if (run + c[q] >= remaining) {
-              sh_digit = 255u - 8u * lane - q;
-              sh_remaining = remaining - run;
-              break;
-            }
-            run += c[q];
+        for (int u = 0; u < 8; ++u) {
+          const int j = j0 + u * blockDim.x;
+          const uint32_t key = pref_key(v[u]);
+          const bool hit = j < len && key >= lo && (uint64_t)(key - lo) < span;
+          const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+          if (bal) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&sh_m, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (hit) cand[base + __popc(bal & ((1u << lane) - 1u))] = composite(key, j);
           }
         }
       }
       __syncthreads();
-      prefix |= sh_digit << shift;
-      mask |= 255u << shift;
-      remaining = sh_remaining;
+      // 4. exact rank of every candidate; rank want - 1 (0-based) is T
+      for (int c = tid; c < m; c += blockDim.x) {
+        const uint64_t me = cand[c];
+        int rank = 0;
+        for (int o = 0; o < m; ++o) rank += cand[o] > me;
+        if (rank == want - 1) sh_T = me;
+      }
       __syncthreads();
+      T = sh_T;
+      located = true;
     }
-  }
-  const uint32_t T = prefix;
-  const int need_eq = remaining;  // keys == T to keep, lowest indices first
-
-  // Ordered compaction: thread t owns the contiguous segment [b0, b1).
-  const int per = (len + blockDim.x - 1) / blockDim.x;
-  const int b0 = min(len, (int)threadIdx.x * per), b1 = min(len, b0 + per);
-  int n_eq = 0, n_gt = 0;
-  if (!take_all && k > 0) {
-    for (int j = b0; j < b1; ++j) {
-      const uint32_t key = key_at(j);
-      n_gt += key > T;
-      n_eq += key == T;
-    }
-  }
-  int tot_eq;
-  const int eq_before = block_excl_scan(n_eq, warp_tot, tot_eq);
-  int keep_eq = need_eq - eq_before;
-  keep_eq = keep_eq < 0 ? 0 : (keep_eq > n_eq ? n_eq : keep_eq);
-  const int mine = take_all ? (b1 - b0) : (k > 0 ? n_gt + keep_eq : 0);
-  int total;
-  int pos = block_excl_scan(mine, warp_tot, total);
-  if (mine > 0) {
-    int eq_seen = 0;
-    for (int j = b0; j < b1; ++j) {
-      bool keep;
-      if (take_all) {
-        keep = true;
-      } else {
-        const uint32_t key = key_at(j);
-        keep = key > T;
-        if (key == T) {
-          keep = eq_seen < keep_eq;
-          ++eq_seen;
+    if (!located) {
+      // exact fallback (massive exact ties): 4 x 8-bit radix select, then the
+      // remaining-th equal key in index order fixes the composite threshold
+      uint32_t prefix = 0u, mask = 0u;
+      int remaining = k;
+      for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        for (int t = tid; t < 256; t += blockDim.x) hist[t] = 0;
+        __syncthreads();
+        for (int j = tid; j < len; j += blockDim.x) {
+          const uint32_t key = pref_key(__ldg(s + j));
+          if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          int run = 0;
+          for (int d = 255; d >= 0; --d) {
+            if (run + hist[d] >= remaining) {
+              sh_digit = (uint32_t)d;
+              sh_rem = remaining - run;
+              break;
+            }
+            run += hist[d];
+          }
+        }
+        __syncthreads();
+        prefix |= sh_digit << shift;
+        mask |= 255u << shift;
+        remaining = sh_rem;
+        __syncthreads();
+      }
+      const int per = (len + blockDim.x - 1) / blockDim.x;
+      const int b0 = min(len, tid * per), b1 = min(len, b0 + per);
+      int eq = 0;
+      for (int j = b0; j < b1; ++j) eq += pref_key(__ldg(s + j)) == prefix;
+      int tot;
+      const int before = block_excl_scan(eq, warp_tot, tot);
+      if (before < remaining && before + eq >= remaining) {
+        int seen = before;
+        for (int j = b0; j < b1; ++j) {
+          if (pref_key(__ldg(s + j)) == prefix && ++seen == remaining) {
+            sh_T = composite(prefix, j);
+            break;
+          }
         }
       }
+      __syncthreads();
+      T = sh_T;
+    }
+  }
+
+  // ordered compaction: warp w owns the contiguous range [w0, w1), read 32 at a
+  // time (coalesced); a ballot orders the kept elements inside each chunk
+  const int nw = blockDim.x >> 5, w = tid >> 5;
+  const int wlen = (((len + nw - 1) / nw) + 31) & ~31;
+  const int w0 = min(len, w * wlen), w1 = min(len, w0 + wlen);
+  int mine = 0;
+  for (int j = w0 + lane; (j - lane) < w1; j += 32) {
+    const bool keep = j < w1 && (take_all || (k > 0 && composite(pref_key(__ldg(s + j)), j) >= T));
+    mine += __popc(__ballot_sync(0xffffffffu, keep));
+  }
+  int total;
+  const int wbase = block_excl_scan(lane == 0 ? mine : 0, warp_tot, total);
+  int pos = __shfl_sync(0xffffffffu, wbase, 0);
+  if (mine > 0) {
+    for (int j = w0 + lane; (j - lane) < w1; j += 32) {
+      const bool keep = j < w1 && (take_all || (k > 0 && composite(pref_key(__ldg(s + j)), j) >= T));
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
       if (keep) {
-        if (idx_out) idx_out[(long long)r * out_ld + pos] = j;
+        const int p = pos + __popc(bal & ((1u << lane) - 1u));
+        if (idx_out) idx_out[(long long)r * out_ld + p] = j;
         if (bits) {
           const int bp = bit_neg ? bit_base - j : bit_base + j;
           atomicOr(bits + (long long)r * a.bits_ld + (bp >> 5), 1u << (bp & 31));
         }
-        ++pos;
       }
+      pos += __popc(bal);
     }
   }
-  if (threadIdx.x == 0 && a.count_out) a.count_out[blockIdx.x] = total;
+  if (tid == 0 && a.count_out) a.count_out[blockIdx.x] = total;
 }
 
 int launch_topk(const TopkArgs& a, cudaStream_t st) {
   const int rows = a.split > 0 ? 2 * a.split : a.rows;
   if (rows <= 0) return SA_OK;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(topk_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopkSmemKeys * 4);
-    attr = true;
-  }
-  TopkArgs b = a;
-  b.smem_keys = kTopkSmemKeys;
-  topk_rows_kernel<<<rows, kTopkThreads, kTopkSmemKeys * 4, st>>>(b);
+  // short segmented rows (block estimator) use 256 threads per row
+  const int threads = (a.lens != nullptr && a.n <= 4096) ? 256 : kTopkThreads;
+  topk_rows_kernel<<<rows, threads, kTopkSmem, st>>>(a);
   return check_launch("topk_rows_kernel");
 }
 
