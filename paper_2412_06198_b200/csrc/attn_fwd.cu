@@ -38,6 +38,8 @@ struct AttnArgs {
   CUtensorMap tmap_q;  // [HH, n, 128] bf16, box {64, 128, 1}, SW128
   CUtensorMap tmap_k;  // [HK, n, 128], box {64, 64, 1}
   CUtensorMap tmap_v;  // [HK, n, 128], box {64, 64, 1}
+  CUtensorMap tmap_k8;  // same tensors, box {64, 8, 1}: one swizzle atom per gathered block row group
+  CUtensorMap tmap_v8;
   __nv_bfloat16* out;
   long long out_batch_stride;  // elements between batches
   long long out_row_stride;    // elements between rows (H * 128 for (B, L, H*d))
@@ -81,14 +83,32 @@ enum Bar {
 
 __device__ __forceinline__ void build_row_mask(const AttnArgs& a, uint32_t kind, int hh, int i,
                                                int j0, int qt, int kt, uint32_t (&m)[4]) {
+  if (i >= a.n) {  // padding rows past n: any non-empty mask (finite logits), never stored
+    m[0] = m[1] = m[2] = m[3] = 0xffffffffu;
+    return;
+  }
   m[0] = m[1] = m[2] = m[3] = 0u;
   const int diag_c = i - j0;  // column (within tile) of the main diagonal
-  if (kind == TK_CAUSAL || i >= a.n) {  // padding rows past n: any non-empty mask, never stored
+  if (kind == TK_CAUSAL) {
     mask_set_range(m, 0, diag_c + 1);
     return;
   }
-  if (kind == TK_CAUSAL) {
-    mask_set_range(m, 0, diag_c + 1);
+  if (kind == TK_GATHER) {
+    // kt is the rank g; the row's query block owns slot s = gq - qt * 128 / b,
+    // filled iff the block row has a g-th off-diagonal entry (all causal)
+    const int b = a.idx.blk_b[hh];
+    const int gq = i / b;
+    const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
+    const int k = ro[gq] + kt;
+    if (k < ro[gq + 1] && a.idx.blk_idx[k] < gq) {
+      const int s = gq - qt * (kTile / b);
+      mask_set_range(m, s * b, s * b + b);
+    }
+    return;
+  }
+  if (kind == TK_BLOCKDIAG) {
+    const int b = a.idx.blk_b[hh];
+    mask_set_range(m, (i / b) * b - j0, diag_c + 1);
     return;
   }
   if (kind == TK_BAND) {
@@ -202,24 +222,57 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 
   if (warp == 4) {
     // ------------------------------------------------------------ TMA producer
-    if (elect_one()) {
+    const int lane = lane_id();
+    if (lane == 0) {
       tma_prefetch(&a.tmap_q);
       tma_prefetch(&a.tmap_k);
       tma_prefetch(&a.tmap_v);
       mbar_arrive_expect_tx(&bars[B_Q], 32768);
       tma_load_3d(sQ, &a.tmap_q, &bars[B_Q], 0, qt * kTile, hh);
       tma_load_3d(sQ + 16384, &a.tmap_q, &bars[B_Q], 64, qt * kTile, hh);
-      // ring sequence: K_0, V_0, K_1, V_1, ... (sub-tiles u = 2 j + half)
-      for (int i = 0; i < 2 * nsub; ++i) {
-        const int u = i >> 1;
-        const int slot = i % kRing;
-        if (i >= kRing) mbar_wait(&bars[B_EMPTY0 + slot], ((i / kRing) - 1) & 1);
-        const int row = (int)tile_ktile(tl[u >> 1]) * kTile + (u & 1) * kSub;
-        const CUtensorMap* map = (i & 1) ? &a.tmap_v : &a.tmap_k;
-        uint8_t* dst = sRing + slot * kSlotBytes;
-        mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
-        tma_load_3d(dst, map, &bars[B_FULL0 + slot], 0, row, hkv);
-        tma_load_3d(dst + 8192, map, &bars[B_FULL0 + slot], 64, row, hkv);
+    }
+    const int bsz = a.idx.blk_b[hh];
+    int slot_gk = 0;  // gather tiles: key block of slot `lane` (0 = placeholder, masked)
+    // ring sequence: K_0, V_0, K_1, V_1, ... (sub-tiles u = 2 j + half)
+    for (int i = 0; i < 2 * nsub; ++i) {
+      const int u = i >> 1;
+      const int slot = i % kRing;
+      const uint32_t e = tl[u >> 1];
+      const uint32_t kind = tile_kind(e);
+      if (kind == TK_GATHER && (i & 3) == 0) {
+        const int gq = qt * (kTile / bsz) + lane;
+        const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
+        int gk = 0;
+        if (lane < kTile / bsz && gq * bsz < a.n) {
+          const int k = ro[gq] + (int)tile_ktile(e);
+          if (k < ro[gq + 1]) {
+            const int x = a.idx.blk_idx[k];
+            if (x < gq) gk = x;
+          }
+        }
+        slot_gk = gk;
+      }
+      if (i >= kRing) mbar_wait(&bars[B_EMPTY0 + slot], ((i / kRing) - 1) & 1);
+      uint8_t* dst = sRing + slot * kSlotBytes;
+      if (kind != TK_GATHER) {
+        if (lane == 0) {
+          const int row = (int)tile_ktile(e) * kTile + (u & 1) * kSub;
+          const CUtensorMap* map = (i & 1) ? &a.tmap_v : &a.tmap_k;
+          mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
+          tma_load_3d(dst, map, &bars[B_FULL0 + slot], 0, row, hkv);
+          tma_load_3d(dst + 8192, map, &bars[B_FULL0 + slot], 64, row, hkv);
+        }
+      } else {
+        // 64 gathered keys = 8 boxes of 8 rows x 2 d-halves; lane -> (box, half)
+        const int bx = lane & 7, dh = (lane >> 3) & 1;
+        const int key = (u & 1) * kSub + bx * 8;
+        const int gk = __shfl_sync(0xffffffffu, slot_gk, key / bsz);
+        const CUtensorMap* map = (i & 1) ? &a.tmap_v8 : &a.tmap_k8;
+        if (lane == 0) mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
+        __syncwarp();
+        if (lane < 16)
+          tma_load_3d(dst + dh * 8192 + bx * 1024, map, &bars[B_FULL0 + slot], dh * 64,
+                      gk * bsz + key % bsz, hkv);
       }
     }
   } else if (warp == 5) {
@@ -429,6 +482,8 @@ extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float s
   if ((st = make_tmap_3d_bf16(&a.tmap_q, q, kHeadDim, n, batch * heads, kTile))) return st;
   if ((st = make_tmap_3d_bf16(&a.tmap_k, k, kHeadDim, n, batch * kv_heads, kSub))) return st;
   if ((st = make_tmap_3d_bf16(&a.tmap_v, v, kHeadDim, n, batch * kv_heads, kSub))) return st;
+  if ((st = make_tmap_3d_bf16(&a.tmap_k8, k, kHeadDim, n, batch * kv_heads, 8))) return st;
+  if ((st = make_tmap_3d_bf16(&a.tmap_v8, v, kHeadDim, n, batch * kv_heads, 8))) return st;
   a.out = reinterpret_cast<__nv_bfloat16*>(out);
   a.out_row_stride = (long long)heads * kHeadDim;
   a.out_batch_stride = (long long)n * heads * kHeadDim;

@@ -19,7 +19,15 @@ enum TileKind : uint32_t {
   TK_BAND = 2,    // Triangular: (i - j < window || j < sinks) && j <= i
   TK_VS = 3,      // column bitmap | diagonal bitmap | i == j, && j <= i
   TK_BLOCK = 4,   // (i/b, j/b) in the block list of the row's query block, && j <= i
+  // Block-Cluster gather mode (b in {8,16,32,64}): the query tile's 128/b query
+  // blocks each contribute one b-key slot to a gathered 128-key tile.
+  TK_GATHER = 5,     // ktile field = rank g: slot s holds the g-th off-diagonal block of query block s
+  TK_BLOCKDIAG = 6,  // kt == qt: only the row's own (diagonal) block, j <= i
 };
+
+// Gather mode applies to block sides whose blocks are whole 8-row swizzle atoms
+// and tile the 128-row query tile exactly.
+__host__ __device__ inline bool block_gather_ok(int b) { return b >= 8 && b < 128 && 128 % b == 0; }
 
 constexpr int kTile = 128;   // query rows and key rows per tile
 constexpr int kHeadDim = 128;

@@ -79,6 +79,30 @@ __global__ void build_tiles_kernel(TileBuildArgs a) {
     }
     __syncwarp();
   }
+  // Gather mode: G gathered tiles (slot s = g-th off-diagonal block of query
+  // block s) + the diagonal tile restricted to each row's own block.  Needs
+  // every row ascending with its diagonal block last (patterns.py:319).
+  int gather_g = -1;
+  if (fam == FAM_BLOCK && block_gather_ok(b)) {
+    const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
+    const int gq = i0 / b + lane;
+    int c = 0;
+    bool ok = true;
+    if (lane < kTile / b && gq <= i1v / b) {
+      int prev = -1;
+      bool diag = false;
+      for (int k = ro[gq]; k < ro[gq + 1]; ++k) {
+        const int gk = a.idx.blk_idx[k];
+        if (gk > gq) break;  // sentinel padding
+        ok = ok && gk > prev && !diag;
+        prev = gk;
+        if (gk == gq) diag = true; else ++c;
+      }
+      ok = ok && diag;
+    }
+    const int G = __reduce_max_sync(0xffffffffu, c);
+    if (__all_sync(0xffffffffu, ok)) gather_g = G;
+  }
 
   for (int kt0 = 0; kt0 <= qt; kt0 += 32) {
     const int kt = kt0 + lane;
@@ -116,6 +140,12 @@ __global__ void build_tiles_kernel(TileBuildArgs a) {
     const uint32_t bal = __ballot_sync(0xffffffffu, inc);
     if (inc) out[count + __popc(bal & ((1u << lane) - 1u))] = tile_entry(kt, kind);
     count += __popc(bal);
+  }
+  if (gather_g >= 0 && gather_g + 1 < count) {
+    __syncwarp();
+    for (int g = lane; g <= gather_g; g += 32)
+      out[g] = (g < gather_g) ? tile_entry(g, TK_GATHER) : tile_entry(qt, TK_BLOCKDIAG);
+    count = gather_g + 1;
   }
   if (lane == 0) {
     a.tile_off[gw] = (int32_t)base;

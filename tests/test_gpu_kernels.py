@@ -114,8 +114,52 @@ def test_executed_tiles_equal_touched_tiles(sa):
     for h in range(H):
         pad = np.zeros((nqt * 128, nqt * 128), bool)
         pad[:n, :n] = masks[h]
-        touched = pad.reshape(nqt, 128, nqt, 128).any(axis=(1, 3))
-        np.testing.assert_array_equal(cnt[h], touched.sum(axis=1))
+        touched = pad.reshape(nqt, 128, nqt, 128).any(axis=(1, 3)).sum(axis=1)
+        if h == 2:  # Block-Cluster b=16: gather mode wherever it executes fewer tiles
+            touched = np.minimum(touched, gather_tiles(ix.block_rows, 16, n))
+        np.testing.assert_array_equal(cnt[h], touched)
+
+
+def gather_tiles(rows, b, n):
+    """Tiles per query tile in Block-Cluster gather mode: max off-diagonal blocks
+    over the tile's 128/b query blocks, plus the diagonal tile (sa_types.h TK_GATHER)."""
+    nqt = -(-n // 128)
+    per = 128 // b
+    out = np.zeros(nqt, np.int64)
+    for qt in range(nqt):
+        g = [int(np.sum(np.asarray(rows[gq]) < gq)) for gq in range(qt * per, min((qt + 1) * per, len(rows)))]
+        out[qt] = max(g) + 1
+    return out
+
+
+@pytest.mark.parametrize("n,b,k_b", [(1000, 8, 1), (4096, 8, 1), (4100, 8, 2), (2049, 16, 3), (3000, 32, 2),
+                                     (4096, 64, 4), (777, 8, 5), (300, 16, 1)])
+def test_block_gather_vs_oracle(sa, n, b, k_b):
+    """Block-Cluster heads through the gathered-tile path: outputs against the
+    oracle's block kernel, and the tile counts the gather cost model implies."""
+    from paper_2412_06198_b200 import device_index as DI
+
+    H, HK = 4, 2
+    q, k, v = rand_heads(20 + n, H, n), rand_heads(21 + n, HK, n), rand_heads(22 + n, HK, n)
+    bld = DI.HostIndexBuilder(n, H)
+    idxs = []
+    for h in range(H):
+        ix = O.block_index(q[h].astype(np.float64), k[h // 2].astype(np.float64), b, k_b)
+        bld.set_block(h, b, [r.astype(np.int32) for r in ix.block_rows])
+        idxs.append(ix)
+    got, cnt = run_index(sa, q, k, v, bld, H, HK)
+    cnt = cnt.cpu().numpy().reshape(H, -1)
+    nqt = -(-n // 128)
+    for h in range(H):
+        want = O.masked_attention(q[h].astype(np.float64), k[h // 2].astype(np.float64),
+                                  v[h // 2].astype(np.float64), idxs[h])
+        err = np.abs(got[h] - want)
+        assert err.max() <= MAX_ABS and err.mean() <= MEAN_ABS, (h, err.max(), err.mean())
+        m = O.index_mask_rows(idxs[h], 0, n)
+        pad = np.zeros((nqt * 128, nqt * 128), bool)
+        pad[:n, :n] = m
+        touched = pad.reshape(nqt, 128, nqt, 128).any(axis=(1, 3)).sum(axis=1)
+        np.testing.assert_array_equal(cnt[h], np.minimum(touched, gather_tiles(idxs[h].block_rows, b, n)))
 
 
 def device_topk(scores32: np.ndarray, k: int) -> np.ndarray:
