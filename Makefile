@@ -3,7 +3,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Ipaper_2412_06198_b200/csrc \
-           --expt-relaxed-constexpr -Xptxas -v
+           --expt-relaxed-constexpr -Xptxas -v $(EXTRA)
 SRC := $(wildcard paper_2412_06198_b200/csrc/*.cu)
 HDR := $(wildcard paper_2412_06198_b200/csrc/*.cuh paper_2412_06198_b200/csrc/*.h include/*.h)
 OBJ := $(patsubst paper_2412_06198_b200/csrc/%.cu,build/%.o,$(SRC))
@@ -18,7 +18,17 @@ build/%.o: paper_2412_06198_b200/csrc/%.cu $(HDR)
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart_static
 
+# profiling variant: phase cycle counters in attn_fwd_kernel (tools/attn_prof.py)
+PROF_LIB := paper_2412_06198_b200/_sa_b200_prof.so
+PROF_OBJ := $(patsubst paper_2412_06198_b200/csrc/%.cu,build/prof/%.o,$(SRC))
+build/prof/%.o: paper_2412_06198_b200/csrc/%.cu $(HDR)
+	@mkdir -p build/prof
+	$(NVCC) $(NVFLAGS) -DSA_ATTN_PROF -c $< -o $@ 2> build/prof/$*.ptxas.txt || (cat build/prof/$*.ptxas.txt; false)
+$(PROF_LIB): $(PROF_OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(PROF_OBJ) -lcudart_static
+prof: $(PROF_LIB)
+
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean
+.PHONY: all clean prof

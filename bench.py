@@ -344,36 +344,33 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e:
+        # the public API on HOST tensors: prefill streams the layer through the GPU
+        # (H2D of q/k/v, kernels, D2H of the (1, n, H*d) output) and returns host outputs
         cfg = R.ModelConfig(n_heads=h_l, d_model=h_l * D, d_head=D, max_context=n)
-        o_h = torch.empty((1, n, h_l * D), dtype=torch.bfloat16).pin_memory()
         qh4, kh4, vh4 = q_h[None], k_h[None], v_h[None]
         kw = {"fixed_pattern": fixed} if fixed is not None else {}
         for _ in range(2):
             res = R.prefill(qh4, kh4, vh4, cfg, mode=plan.mode, **kw)
-            o_h.copy_(res.outputs)
+        assert not res.outputs.is_cuda
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        reps = max(2, min(args.steps, 5))
-        t0 = time.perf_counter()
-        e0.record()
+        reps = max(3, min(args.steps, 5))
+        walls = []
         for _ in range(reps):
+            t0 = time.perf_counter()
             res = R.prefill(qh4, kh4, vh4, cfg, mode=plan.mode, **kw)
-            o_h.copy_(res.outputs, non_blocking=True)
-        e1.record()
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / reps
-        wall_e2e = (time.perf_counter() - t0) * 1e3 / reps
+            walls.append((time.perf_counter() - t0) * 1e3)
+        e2e_ms = statistics.median(walls)
         if world > 1:
             t = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": round(e2e_ms, 3), "unit": "ms/layer",
                "h2d_bytes_per_step": int(q_h.numel() * 2 + k_h.numel() * 2 + v_h.numel() * 2),
-               "d2h_bytes_per_step": int(o_h.numel() * 2), "wall_ms": round(wall_e2e, 3),
-               "path": "paper_2412_06198_b200.prefill(pinned host torch tensors) + output D2H"}
+               "d2h_bytes_per_step": int(res.outputs.numel() * 2), "reps": reps, "timer": "wall, median",
+               "path": "paper_2412_06198_b200.prefill(pinned host bf16 torch tensors) -> host outputs "
+                       "(per-kv-group H2D / kernels / D2H streams overlapped)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -84,6 +84,9 @@ typedef struct {
   void* stage_events[6]; /* optional cudaEvent_t, recorded on `stream` after:
                             [0] selection, [1] VS estimator + top-k, [2] block
                             estimator, [3] tile lists, [4] attention, [5] unused */
+  int64_t out_ld;        /* elements between output rows; 0 = heads * 128 (the
+                            (B, L, H*d) layout of runtime.py:194).  A larger
+                            value writes a head group into a wider layer output. */
 } sa_prefill_desc;
 
 /* Device views into a prefill workspace (valid after sa_prefill). */
@@ -112,6 +115,14 @@ size_t sa_prefill_workspace_size(const sa_prefill_desc* desc);
 int sa_prefill_views(const sa_prefill_desc* desc, void* ws, sa_prefill_view* view);
 int sa_prefill(const sa_prefill_desc* desc, const void* q, const void* k, const void* v,
                void* out, void* ws, size_t ws_bytes, void* stream);
+
+/* AttnMatrices' finiteness check (core.py:72-74) on device: sets *flag to 1
+ * if any of `count` bf16 values is NaN or Inf (flag is not cleared). */
+int sa_check_finite_bf16(const void* x, long long count, int32_t* flag, void* stream);
+/* cudaMemcpy2DAsync passthrough (kind = cudaMemcpyDefault) so host code can
+ * move a head group's output columns without torch strided copies. */
+int sa_memcpy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                      size_t height, void* stream);
 
 /* ---- selector: search.select_pattern_windowed (search.py:276-319) -------- */
 /* Candidate arrays are HOST arrays of length ncand (refined at window scale).
@@ -171,6 +182,10 @@ int sa_build_tiles(const sa_head_index* index, int hh_total, int n, int32_t* til
 /* ---- sparse attention (patterns.py:487-497 sparse_attention, need_weights=False;
  *      core.py:138-154 dense_attention when family == SA_DENSE) ------------- */
 /* lse (nullable): [HH, n] natural-log row log-sum-exp of the realised logits. */
+/* Launch order for sa_attn_sparse's CTAs: work[r] = index (into tile_cnt) of
+ * the item with the r-th largest tile count (longest-processing-time first).
+ * No reference counterpart: the reference runs heads serially (runtime.py:174). */
+int sa_order_work(const int32_t* tile_cnt, int items, int max_cnt, int32_t* work, void* stream);
 int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float scale, const void* q,
                    const void* k, const void* v, void* out, const sa_head_index* index,
                    const int32_t* tile_off, const int32_t* tile_cnt, const uint32_t* tiles,

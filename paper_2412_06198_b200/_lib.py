@@ -14,7 +14,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_sa_b200.so")
+# SA_B200_LIB selects a tool build (e.g. the SA_ATTN_PROF variant); default is the product .so
+LIB_PATH = os.environ.get("SA_B200_LIB") or os.path.join(_HERE, "_sa_b200.so")
 
 _lib = None
 _lock = threading.Lock()
@@ -63,6 +64,7 @@ class sa_prefill_desc(ctypes.Structure):
         ("full", sa_pattern * 3),
         ("preselected", ctypes.c_int32),
         ("stage_events", ctypes.c_void_p * 6),
+        ("out_ld", ctypes.c_int64),
     ]
 
 
@@ -109,6 +111,9 @@ _SIGNATURES = {
     "sa_attn_weights": (ctypes.c_int, [_I, _I, _I, _I, _F, _P, _P, _P, _IDX, _P, _P]),
     "sa_block_mean_f32": (ctypes.c_int, [_P, _I, _I, _I, _P, _P]),
     "sa_build_tiles": (ctypes.c_int, [_IDX, _I, _I, _P, _P, _P, _P]),
+    "sa_check_finite_bf16": (ctypes.c_int, [_P, _LL, _P, _P]),
+    "sa_memcpy2d_async": (ctypes.c_int, [_P, _SZ, _P, _SZ, _SZ, _SZ, _P]),
+    "sa_order_work": (ctypes.c_int, [_P, _I, _I, _P, _P]),
     "sa_attn_sparse": (ctypes.c_int, [_I, _I, _I, _I, _F, _P, _P, _P, _P, _IDX, _P, _P, _P, _P,
                                       _P]),
 }

@@ -15,9 +15,6 @@
 
 namespace sa {
 
-struct AttnArgs;
-int launch_attn(const AttnArgs& a, int grid, cudaStream_t stream);
-struct TileBuildArgs;
 
 static thread_local std::string g_last_error;
 

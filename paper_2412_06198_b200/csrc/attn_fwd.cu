@@ -28,6 +28,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sa_types.h"
 #include "sm100_common.cuh"
@@ -55,10 +56,21 @@ struct AttnArgs {
   const int32_t* work;  // optional CTA -> (hh * nqt + qt) order; null = heavy-first default
   HeadIndexView idx;
   float* lse;  // optional [hh_total, n] natural-log row log-sum-exp
-  volatile int* dbg;  // optional progress trace [grid * 8] (debug builds)
+  unsigned long long* prof;  // SA_ATTN_PROF builds: per-role phase cycle counters [3 * 16]
 };
 
 constexpr int kThreads = 192;
+constexpr int kDefaultPoly = 4;
+#ifdef SA_ATTN_PROF
+constexpr bool kProf = true;
+#else
+constexpr bool kProf = false;
+#endif
+// phase timer: PT(k) adds the cycles since the previous mark to counter k
+#define PT_INIT long long pt_last = kProf ? clock64() : 0; unsigned long long pc[16] = {0};
+#define PT(k) do { if (kProf) { long long t_ = clock64(); pc[k] += t_ - pt_last; pt_last = t_; } } while (0)
+#define PT_FLUSH(base) do { if (kProf && a.prof && lane_id() == 0) { \
+    for (int k_ = 0; k_ < 16; ++k_) atomicAdd(a.prof + (base) + k_, pc[k_]); } } while (0)
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kColS = 0;    // S buffers at 0 and 64 (P aliased at their first 32 columns)
 constexpr uint32_t kColO = 128;
@@ -81,79 +93,105 @@ enum Bar {
   B_NUM = B_OF + 1
 };
 
-__device__ __forceinline__ void build_row_mask(const AttnArgs& a, uint32_t kind, int hh, int i,
-                                               int j0, int qt, int kt, uint32_t (&m)[4]) {
+// Per-row constants of the mask builders, loaded once per CTA.
+struct RowConst {
+  int b;             // Block-Cluster block side
+  int ro_lo, ro_hi;  // the row's query-block entries in blk_idx
+  int w, s;          // Triangular window / sinks
+  bool eye;          // VS forced diagonal (patterns.py:378)
+};
+
+__device__ __forceinline__ RowConst row_const(const AttnArgs& a, int hh, int i) {
+  RowConst c;
+  const int fam = a.idx.family[hh];
+  c.b = a.idx.blk_b[hh];
+  c.ro_lo = c.ro_hi = 0;
+  if (fam == FAM_BLOCK && i < a.n) {
+    const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
+    c.ro_lo = ro[i / c.b];
+    c.ro_hi = ro[i / c.b + 1];
+  }
+  c.w = a.idx.tri_window[hh];
+  c.s = a.idx.tri_sinks[hh];
+  c.eye = fam != FAM_VS_NOEYE;
+  return c;
+}
+
+// Global words a tile's row mask needs, fetched one tile ahead so the load
+// latency hides under the previous tile's softmax.
+__device__ __forceinline__ void mask_fetch(const AttnArgs& a, const RowConst& c, int hh, int i,
+                                           uint32_t e, uint32_t (&raw)[9]) {
+  const uint32_t kind = tile_kind(e);
+  const int kt = (int)tile_ktile(e);
+  if (i >= a.n) return;
+  if (kind == TK_VS) {
+    const int j0 = kt * kTile;
+    const uint32_t* cb = a.idx.colbits + (size_t)hh * a.idx.vs_words + (j0 >> 5);
+    const uint32_t* dr = a.idx.diagrev + (size_t)hh * a.idx.vs_words + ((a.n + 127 - i + j0) >> 5);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) raw[k] = __ldg(cb + k);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) raw[4 + k] = __ldg(dr + k);
+  } else if (kind == TK_GATHER) {
+    const int k = c.ro_lo + kt;
+    raw[0] = k < c.ro_hi ? (uint32_t)__ldg(a.idx.blk_idx + k) : 0x7fffffffu;
+  }
+}
+
+// The 128-bit row mask of tile entry e for query row i (registers only,
+// except the rare union-mode Block tiles).
+__device__ __forceinline__ void mask_make(const AttnArgs& a, const RowConst& c, int i, int qt,
+                                          uint32_t e, const uint32_t (&raw)[9], uint32_t (&m)[4]) {
+  const uint32_t kind = tile_kind(e);
+  const int kt = (int)tile_ktile(e);
   if (i >= a.n) {  // padding rows past n: any non-empty mask (finite logits), never stored
     m[0] = m[1] = m[2] = m[3] = 0xffffffffu;
     return;
   }
   m[0] = m[1] = m[2] = m[3] = 0u;
+  const int j0 = kt * kTile;
   const int diag_c = i - j0;  // column (within tile) of the main diagonal
   if (kind == TK_CAUSAL) {
     mask_set_range(m, 0, diag_c + 1);
-    return;
-  }
-  if (kind == TK_GATHER) {
+  } else if (kind == TK_GATHER) {
     // kt is the rank g; the row's query block owns slot s = gq - qt * 128 / b,
     // filled iff the block row has a g-th off-diagonal entry (all causal)
-    const int b = a.idx.blk_b[hh];
-    const int gq = i / b;
-    const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
-    const int k = ro[gq] + kt;
-    if (k < ro[gq + 1] && a.idx.blk_idx[k] < gq) {
-      const int s = gq - qt * (kTile / b);
-      mask_set_range(m, s * b, s * b + b);
+    const int gq = i / c.b;
+    if ((int)raw[0] < gq) {
+      const int s = gq - qt * (kTile / c.b);
+      mask_set_range(m, s * c.b, s * c.b + c.b);
     }
-    return;
-  }
-  if (kind == TK_BLOCKDIAG) {
-    const int b = a.idx.blk_b[hh];
-    mask_set_range(m, (i / b) * b - j0, diag_c + 1);
-    return;
-  }
-  if (kind == TK_BAND) {
-    const int w = a.idx.tri_window[hh];
-    const int s = a.idx.tri_sinks[hh];
-    mask_set_range(m, diag_c - w + 1, diag_c + 1);
-    mask_set_range(m, 0, min(s - j0, diag_c + 1));
-    return;
-  }
-  if (kind == TK_VS) {
-    const uint32_t* cb = a.idx.colbits + (size_t)hh * a.idx.vs_words + (j0 >> 5);
-    const uint32_t* dr = a.idx.diagrev + (size_t)hh * a.idx.vs_words;
+  } else if (kind == TK_BLOCKDIAG) {
+    mask_set_range(m, (i / c.b) * c.b - j0, diag_c + 1);
+  } else if (kind == TK_BAND) {
+    mask_set_range(m, diag_c - c.w + 1, diag_c + 1);
+    mask_set_range(m, 0, min(c.s - j0, diag_c + 1));
+  } else if (kind == TK_VS) {
     // window bit c <=> diag[i - j0 - c] <=> diagrev bit (n + 127 - i + j0 + c)
-    const int p = a.n + 127 - i + j0;
-    const int w0 = p >> 5, sh = p & 31;
-    uint32_t d[5];
+    const int sh = (a.n + 127 - i + j0) & 31;
 #pragma unroll
-    for (int k = 0; k < 5; ++k) d[k] = __ldg(dr + w0 + k);
+    for (int k = 0; k < 4; ++k) m[k] = raw[k] | __funnelshift_r(raw[4 + k], raw[5 + k], sh);
+    if (diag_c >= 0 && diag_c < 128 && c.eye) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) m[k] = __ldg(cb + k) | __funnelshift_r(d[k], d[k + 1], sh);
-    if (diag_c >= 0 && diag_c < 128 && a.idx.family[hh] != FAM_VS_NOEYE)
-      m[diag_c >> 5] |= 1u << (diag_c & 31);  // forced diagonal (patterns.py:378)
+      for (int k = 0; k < 4; ++k) m[k] |= ((diag_c >> 5) == k) ? 1u << (diag_c & 31) : 0u;
+    }
     if (kt == qt) {  // causal cut on the diagonal tile
       uint32_t c4[4] = {0u, 0u, 0u, 0u};
       mask_set_range(c4, 0, diag_c + 1);
 #pragma unroll
       for (int k = 0; k < 4; ++k) m[k] &= c4[k];
     }
-    return;
-  }
-  if (kind == TK_BLOCK) {
-    const int b = a.idx.blk_b[hh];
-    const int gq = i / b;
-    const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
-    int lo = ro[gq], hi = ro[gq + 1];
-    // first listed key block whose end lies past j0
+  } else if (kind == TK_BLOCK) {
+    const int b = c.b;
     // rows are ascending key-block ids, possibly padded with INT32_MAX sentinels
     const int gfirst = j0 / b;                // first block ending after j0
     const int kend = (j0 + 128 + b - 1) / b;  // first block starting at/after j0 + 128
-    int L = lo, R = hi;
+    int L = c.ro_lo, R = c.ro_hi;
     while (L < R) {
       int mid = (L + R) >> 1;
       if (a.idx.blk_idx[mid] >= gfirst) R = mid; else L = mid + 1;
     }
-    for (int k = L; k < hi; ++k) {
+    for (int k = L; k < c.ro_hi; ++k) {
       const int gk = a.idx.blk_idx[k];
       if (gk >= kend) break;
       mask_set_range(m, gk * b - j0, (gk + 1) * b - j0);
@@ -162,12 +200,14 @@ __device__ __forceinline__ void build_row_mask(const AttnArgs& a, uint32_t kind,
     mask_set_range(c4, 0, diag_c + 1);
 #pragma unroll
     for (int k = 0; k < 4; ++k) m[k] &= c4[k];
-    return;
+  } else {
+    m[0] = m[1] = m[2] = m[3] = 0xffffffffu;
   }
-  // TK_FULL never reaches here
-  m[0] = m[1] = m[2] = m[3] = 0xffffffffu;
 }
 
+// POLY > 0: every POLY-th exp pair of a row chunk runs on the FMA pipe
+// (exp2_poly2) instead of MUFU, balancing the two pipes.
+template <int POLY>
 __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -177,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + B_NUM);
 
+  const long long t_entry = kProf ? clock64() : 0;
   const int warp = warp_id();
   int item;
   if (a.work != nullptr) {
@@ -232,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       tma_load_3d(sQ + 16384, &a.tmap_q, &bars[B_Q], 64, qt * kTile, hh);
     }
     const int bsz = a.idx.blk_b[hh];
+    PT_INIT
     int slot_gk = 0;  // gather tiles: key block of slot `lane` (0 = placeholder, masked)
     // ring sequence: K_0, V_0, K_1, V_1, ... (sub-tiles u = 2 j + half)
     for (int i = 0; i < 2 * nsub; ++i) {
@@ -252,7 +294,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         }
         slot_gk = gk;
       }
+      PT(0);
       if (i >= kRing) mbar_wait(&bars[B_EMPTY0 + slot], ((i / kRing) - 1) & 1);
+      PT(1);
       uint8_t* dst = sRing + slot * kSlotBytes;
       if (kind != TK_GATHER) {
         if (lane == 0) {
@@ -274,7 +318,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
           tma_load_3d(dst + dh * 8192 + bx * 1024, map, &bars[B_FULL0 + slot], dh * 64,
                       gk * bsz + key % bsz, hkv);
       }
+      PT(2);
+      if (kProf) pc[15] += 1;
     }
+    PT_FLUSH(32);
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
@@ -282,9 +329,12 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
       const uint32_t q_addr = smem_u32(sQ);
       const uint32_t ring_addr = smem_u32(sRing);
+      PT_INIT
       auto issue_qk = [&](int u) {
         const int i = 2 * u, slot = i % kRing;
+        PT(0);
         mbar_wait(&bars[B_FULL0 + slot], (i / kRing) & 1);
+        PT(1);
         tc_fence_after();
         const uint32_t k_addr = ring_addr + slot * kSlotBytes;
 #pragma unroll
@@ -296,15 +346,19 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         }
         mma_commit(&bars[B_EMPTY0 + slot]);
         mma_commit(&bars[B_SF0 + (u & 1)]);
+        PT(2);
       };
       mbar_wait(&bars[B_Q], 0);
       tc_fence_after();
       issue_qk(0);
       if (nsub > 1) issue_qk(1);
       for (int u = 0; u < nsub; ++u) {
+        PT(3);
         mbar_wait(&bars[B_PF0 + (u & 1)], (u >> 1) & 1);
+        PT(4);
         const int i = 2 * u + 1, slot = i % kRing;
         mbar_wait(&bars[B_FULL0 + slot], (i / kRing) & 1);
+        PT(5);
         tc_fence_after();
         const uint32_t v_addr = ring_addr + slot * kSlotBytes;
         const uint32_t p_addr = tbase + kColS + (u & 1) * kSub;
@@ -315,9 +369,12 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         }
         mma_commit(&bars[B_EMPTY0 + slot]);
         mma_commit(&bars[B_OD]);
+        PT(6);
+        if (kProf) pc[15] += 1;
         if (u + 2 < nsub) issue_qk(u + 2);
       }
       mma_commit(&bars[B_OF]);
+      PT_FLUSH(16);
     }
   } else {
     // ------------------------------------------------------------ softmax warps
@@ -329,23 +386,42 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     float l = 0.f;
     uint32_t msk[4] = {0u, 0u, 0u, 0u};
     uint32_t kind = TK_FULL;
+    const RowConst rc = row_const(a, hh, i);
+    uint32_t raw[9];
+    uint32_t e_cur = cnt > 0 ? tl[0] : 0u;
+    uint32_t e_nxt = cnt > 1 ? tl[1] : 0u;
+    mask_fetch(a, rc, hh, i, e_cur, raw);
+    PT_INIT
+    if (kProf) { pc[10] += pt_last - t_entry; pc[12] += 1; }
     for (int u = 0; u < nsub; ++u) {
       const int half = u & 1;
+      PT(0);
       if (half == 0) {
-        const uint32_t e = tl[u >> 1];
-        kind = tile_kind(e);
-        const int kt = (int)tile_ktile(e);
-        if (kind != TK_FULL) build_row_mask(a, kind, hh, i, kt * kTile, qt, kt, msk);
+        const int t = u >> 1;
+        kind = tile_kind(e_cur);
+#ifdef SA_NO_PREFETCH
+        mask_fetch(a, rc, hh, i, e_cur, raw);
+        if (kind != TK_FULL) mask_make(a, rc, i, qt, e_cur, raw, msk);
+#else
+        if (kind != TK_FULL) mask_make(a, rc, i, qt, e_cur, raw, msk);
+        // next tile's entry and mask words are loaded now, used one tile later
+        if (t + 1 < cnt) mask_fetch(a, rc, hh, i, e_nxt, raw);
+#endif
+        e_cur = e_nxt;
+        e_nxt = (t + 2 < cnt) ? tl[t + 2] : 0u;
       }
+      PT(1);
       mbar_wait(&bars[B_SF0 + half], (u >> 1) & 1);
+      PT(2);
       tc_fence_after();
       uint32_t s[2][32];
       const uint32_t s_col = tbase + lane_off + kColS + half * kSub;
       tmem_ld32(s_col, s[0]);
       tmem_ld32(s_col + 32, s[1]);
       tmem_ld_wait();
+      PT(3);
       if (kind != TK_FULL) {
-        const uint32_t m0 = msk[2 * half], m1 = msk[2 * half + 1];
+        const uint32_t m0 = half ? msk[2] : msk[0], m1 = half ? msk[3] : msk[1];
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           if (!((m0 >> t) & 1u)) s[0][t] = __float_as_uint(-INFINITY);
@@ -365,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
           }
         mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
       }
+      PT(4);
       const float mt = mx * sl2;
       // Lazy rescale: keep a stale max until the row max grows by > 2^8.  The
       // decision is per row but the TMEM round trip of O is warp-wide
@@ -395,6 +472,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         }
         if (need) m_used = mt;
       }
+      PT(5);
       const float moff = (m_used == -INFINITY) ? 0.f : m_used;
       // p = exp2(s * scale_log2 - m): FFMA2 + two MUFU.EX2; row sum in four FADD2 chains
       const float2 sc2 = make_float2(sl2, sl2);
@@ -407,8 +485,12 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 #pragma unroll
         for (int t = 0; t < 32; t += 2) {
           float2 x = ffma2(make_float2(__uint_as_float(s[c][t]), __uint_as_float(s[c][t + 1])), sc2, mo2);
-          x.x = fast_exp2(x.x);
-          x.y = fast_exp2(x.y);
+          if (POLY > 0 && ((t >> 1) % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY : 1) - 1) {
+            x = exp2_poly2(x);
+          } else {
+            x.x = fast_exp2(x.x);
+            x.y = fast_exp2(x.y);
+          }
           acc[(t >> 1) & 3] = fadd2(acc[(t >> 1) & 3], x);
           p[c * 16 + (t >> 1)] = pack_bf16(x.x, x.y);
         }
@@ -417,13 +499,17 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         const float2 t2 = fadd2(a01, a23);
         l += t2.x + t2.y;
       }
+      PT(6);
       tmem_st32(s_col, p);  // P (bf16 pairs) over the first 32 columns of this S buffer
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars[B_PF0 + half]);
+      PT(7);
+      if (kProf) pc[15] += 1;
     }
     // ------------------------------------------------------------ epilogue
     mbar_wait(&bars[B_OF], 0);
+    PT(8);
     tc_fence_after();
     const float inv = 1.0f / l;
     const bool valid = i < a.n && cnt > 0;  // cnt == 0: query tile not requested
@@ -447,6 +533,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     if (valid && a.lse != nullptr) {
       a.lse[(size_t)hh * a.n + i] = (m_used + log2f(l)) * 0.69314718055994531f;
     }
+    PT(9);
+    if (kProf) pc[11] += clock64() - t_entry;
+    PT_FLUSH(0);
   }
   tc_fence_before();
   __syncthreads();
@@ -457,17 +546,20 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 
 // ------------------------------------------------------------------ C ABI
 #include "api_common.h"
+#include "internal.h"
 
 static void* sa_attn_dbg_ptr = nullptr;
 
-extern "C" int sa_attn_debug_ptr(void* p) { sa_attn_dbg_ptr = p; return 0; }
+// Tool hook (not in the public header): in SA_ATTN_PROF builds the kernel adds
+// its per-role phase cycles into p[0..48) (softmax, MMA, TMA producer).
+extern "C" int sa_attn_profile_counters(void* p) { sa_attn_dbg_ptr = p; return 0; }
 
-extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float scale,
-                              const void* q, const void* k, const void* v, void* out,
-                              const sa_head_index* index, const int32_t* tile_off,
-                              const int32_t* tile_cnt, const uint32_t* tiles, float* lse,
-                              void* stream) {
-  using namespace sa;
+namespace sa {
+
+int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const void* q, const void* k,
+                const void* v, void* out, const sa_head_index* index, const int32_t* tile_off,
+                const int32_t* tile_cnt, const uint32_t* tiles, const int32_t* work, float* lse,
+                cudaStream_t cs, long long out_ld) {
   if (batch < 1 || heads < 1 || kv_heads < 1 || n < 1)
     return fail(SA_ERR_DIMENSION, "need batch, heads, kv_heads, n >= 1");
   if (heads % kv_heads != 0)
@@ -485,8 +577,8 @@ extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float s
   if ((st = make_tmap_3d_bf16(&a.tmap_k8, k, kHeadDim, n, batch * kv_heads, 8))) return st;
   if ((st = make_tmap_3d_bf16(&a.tmap_v8, v, kHeadDim, n, batch * kv_heads, 8))) return st;
   a.out = reinterpret_cast<__nv_bfloat16*>(out);
-  a.out_row_stride = (long long)heads * kHeadDim;
-  a.out_batch_stride = (long long)n * heads * kHeadDim;
+  a.out_row_stride = out_ld > 0 ? out_ld : (long long)heads * kHeadDim;
+  a.out_batch_stride = (long long)n * a.out_row_stride;
   a.n = n;
   a.heads = heads;
   a.kv_heads = kv_heads;
@@ -496,16 +588,44 @@ extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float s
   a.tile_off = tile_off;
   a.tile_cnt = tile_cnt;
   a.tiles = tiles;
-  a.work = nullptr;
+  a.work = work;
   a.idx = *index;
   a.lse = lse;
-  a.dbg = nullptr;
+  a.prof = reinterpret_cast<unsigned long long*>(sa_attn_dbg_ptr);
+  // exp split between MUFU and the FMA pipe (SA_ATTN_POLY overrides, for tuning)
+  static const int poly = [] {
+    const char* e = getenv("SA_ATTN_POLY");
+    const int v = e ? atoi(e) : kDefaultPoly;
+    return (v == 0 || v == 2 || v == 3 || v == 4 || v == 8) ? v : kDefaultPoly;
+  }();
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaFuncSetAttribute(attn_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaFuncSetAttribute(attn_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaFuncSetAttribute(attn_fwd_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaFuncSetAttribute(attn_fwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaFuncSetAttribute(attn_fwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     attr_set = true;
   }
   const int grid = a.hh_total * a.nqt;
-  attn_fwd_kernel<<<grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  // the need_weights path derives weights from lse: keep exact MUFU exps there
+  switch (lse != nullptr ? 0 : poly) {
+    case 2: attn_fwd_kernel<2><<<grid, kThreads, kSmemBytes, cs>>>(a); break;
+    case 3: attn_fwd_kernel<3><<<grid, kThreads, kSmemBytes, cs>>>(a); break;
+    case 4: attn_fwd_kernel<4><<<grid, kThreads, kSmemBytes, cs>>>(a); break;
+    case 8: attn_fwd_kernel<8><<<grid, kThreads, kSmemBytes, cs>>>(a); break;
+    default: attn_fwd_kernel<0><<<grid, kThreads, kSmemBytes, cs>>>(a); break;
+  }
   return check_launch("attn_fwd_kernel");
+}
+
+}  // namespace sa
+
+extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float scale,
+                              const void* q, const void* k, const void* v, void* out,
+                              const sa_head_index* index, const int32_t* tile_off,
+                              const int32_t* tile_cnt, const uint32_t* tiles, float* lse,
+                              void* stream) {
+  return sa::launch_attn(batch, heads, kv_heads, n, scale, q, k, v, out, index, tile_off, tile_cnt,
+                         tiles, nullptr, lse, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include "sparseattn_b200.h"
+
 namespace sa {
 
 struct TopkArgs {
@@ -57,5 +59,10 @@ int launch_select(int batch, int heads, int kv_heads, int n, int cal, float scal
                   const void* k, int ncand, const int32_t* cand_fam, const int32_t* cand_p1,
                   const int32_t* cand_p2, int32_t* choice_out, int32_t* family_out,
                   double* err_out, cudaStream_t stream);
+
+int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const void* q, const void* k,
+                const void* v, void* out, const sa_head_index* index, const int32_t* tile_off,
+                const int32_t* tile_cnt, const uint32_t* tiles, const int32_t* work, float* lse,
+                cudaStream_t st, long long out_ld = 0);
 
 }  // namespace sa

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 
 #include "api_common.h"
 #include "internal.h"
@@ -37,7 +38,7 @@ struct Layout {
 enum WsSlot {
   W_CHOICE = 0, W_FAMILY, W_ERR, W_TRIW, W_TRIS, W_COLBITS, W_DIAGREV, W_COLSC, W_DIAGSC,
   W_COLIDX, W_DIAGIDX, W_TAIL, W_BLKB, W_ROWOFF, W_BLKIDX, W_QP, W_KP, W_BLKWS,
-  W_TOFF, W_TCNT, W_TILES, W_NUM
+  W_TOFF, W_TCNT, W_TILES, W_WORK, W_NUM
 };
 
 struct Plan {
@@ -86,6 +87,8 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
     return fail(SA_ERR_DIMENSION, "heads=%d not a multiple of kv_heads=%d", d->heads, d->kv_heads);
   if (d->n > 262144) return fail(SA_ERR_DIMENSION, "n=%d exceeds 262144", d->n);
   if (!(d->scale > 0.f) || !std::isfinite(d->scale)) return fail(SA_ERR_DIMENSION, "bad scale");
+  if (d->out_ld != 0 && d->out_ld < (int64_t)d->heads * kHeadDim)
+    return fail(SA_ERR_DIMENSION, "out_ld=%lld is below heads * 128", (long long)d->out_ld);
   memset(p, 0, sizeof(*p));
   const int n = d->n;
   p->hh = d->batch * d->heads;
@@ -162,6 +165,7 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
   sz[W_TOFF] = hh * p->nqt * 4;
   sz[W_TCNT] = hh * p->nqt * 4;
   sz[W_TILES] = hh * (size_t)p->nqt * (p->nqt + 1) / 2 * 4;
+  sz[W_WORK] = hh * p->nqt * 4;
   size_t o = 0;
   for (int i = 0; i < W_NUM; ++i) {
     L->off[i] = o;
@@ -351,8 +355,18 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   // 4. executed tiles + attention
   if ((rc = sa_build_tiles(&V.index, p.hh, n, V.tile_off, V.tile_cnt, V.tiles, stream))) return rc;
   mark(3);
-  rc = sa_attn_sparse(B, H, HK, n, desc->scale, q, k, v, out, &V.index, V.tile_off, V.tile_cnt,
-                      V.tiles, nullptr, stream);
+  // longest-first CTA order (SA_ATTN_ORDER=0 keeps the kernel's kv-group-major default, for A/B)
+  static const bool lpt = [] {
+    const char* e = getenv("SA_ATTN_ORDER");
+    return !(e && e[0] == '0');
+  }();
+  int32_t* work = nullptr;
+  if (lpt) {
+    work = reinterpret_cast<int32_t*>(b + L.off[W_WORK]);
+    if ((rc = sa_order_work(V.tile_cnt, p.hh * p.nqt, p.nqt, work, stream))) return rc;
+  }
+  rc = launch_attn(B, H, HK, n, desc->scale, q, k, v, out, &V.index, V.tile_off, V.tile_cnt, V.tiles,
+                   work, nullptr, st, desc->out_ld);
   mark(4);
   return rc;
 }

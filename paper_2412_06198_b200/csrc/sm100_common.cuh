@@ -220,13 +220,40 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return r;
 }
 
+// 2^x for a pair on the FMA pipe (offloads MUFU.EX2): x = j + f with j = rint(x)
+// via the 1.5*2^23 magic add, 2^f by a degree-3 fit on [-0.5, 0.5] (max rel
+// error 7.5e-5, below the bf16 rounding of P), 2^j added into the exponent
+// field.  x is clamped at -125 (result ~2e-38 instead of 0 for masked logits).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
+  const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(j, make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(make_float2(0.0551716685f, 0.0551716685f), f, make_float2(0.242611155f, 0.242611155f));
+  p = ffma2(p, f, make_float2(0.693260968f, 0.693260968f));
+  p = ffma2(p, f, make_float2(0.999928057f, 0.999928057f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Bits [lo, hi) of one 32-bit word (lo/hi any ints; branch-free).
+__device__ __forceinline__ uint32_t word_range(int lo, int hi) {
+  lo = min(max(lo, 0), 32);
+  hi = min(max(hi, 0), 32);
+  const uint32_t up = static_cast<uint32_t>((1ull << hi) - 1ull);
+  const uint32_t dn = static_cast<uint32_t>((1ull << lo) - 1ull);
+  return hi > lo ? (up & ~dn) : 0u;
+}
+
 // Set bits [a, b) (clipped to [0,128)) in a 128-bit mask held as 4 words.
 __device__ __forceinline__ void mask_set_range(uint32_t (&m)[4], int a, int b) {
+#ifdef SA_BRANCHY_RANGE
   a = a < 0 ? 0 : a;
   b = b > 128 ? 128 : b;
 #pragma unroll
@@ -239,6 +266,10 @@ __device__ __forceinline__ void mask_set_range(uint32_t (&m)[4], int a, int b) {
       m[w] |= bits;
     }
   }
+#else
+#pragma unroll
+  for (int w = 0; w < 4; ++w) m[w] |= word_range(a - 32 * w, b - 32 * w);
+#endif
 }
 
 }  // namespace sa

@@ -154,6 +154,33 @@ __global__ void build_tiles_kernel(TileBuildArgs a) {
   }
 }
 
+// Longest-processing-time-first launch order: work[r] = the item (hh * nqt +
+// qt) with the r-th largest tile count (counting sort, one CTA).  The block
+// scheduler dispatches CTAs roughly in blockIdx order, so the heaviest query
+// tiles (full-width VS rows) start first and the light ones fill the tail.
+__global__ void order_work_kernel(const int32_t* __restrict__ cnt, int items, int max_cnt,
+                                  int32_t* __restrict__ work) {
+  extern __shared__ int32_t start[];  // [max_cnt + 2]
+  const int bins = max_cnt + 1;
+  for (int c = threadIdx.x; c <= bins; c += blockDim.x) start[c] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < items; i += blockDim.x) atomicAdd(&start[min(max(cnt[i], 0), max_cnt)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // bins <= 2049: exclusive scan from the heaviest bin down
+    int run = 0;
+    for (int c = max_cnt; c >= 0; --c) {
+      const int h = start[c];
+      start[c] = run;
+      run += h;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int pos = atomicAdd(&start[min(max(cnt[i], 0), max_cnt)], 1);
+    work[pos] = i;
+  }
+}
+
 }  // namespace sa
 
 // ------------------------------------------------------------------ C ABI
@@ -179,4 +206,14 @@ extern "C" int sa_build_tiles(const sa_head_index* index, int hh_total, int n, i
   const int grid = (int)((warps * 32 + threads - 1) / threads);
   build_tiles_kernel<<<grid, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
   return check_launch("build_tiles_kernel");
+}
+
+extern "C" int sa_order_work(const int32_t* tile_cnt, int items, int max_cnt, int32_t* work,
+                             void* stream) {
+  using namespace sa;
+  if (items < 1 || max_cnt < 0 || max_cnt > 65536) return fail(SA_ERR_DIMENSION, "bad work-order sizes");
+  if (!tile_cnt || !work) return fail(SA_ERR_DIMENSION, "null pointer");
+  order_work_kernel<<<1, 1024, (max_cnt + 2) * sizeof(int32_t), reinterpret_cast<cudaStream_t>(stream)>>>(
+      tile_cnt, items, max_cnt, work);
+  return check_launch("order_work_kernel");
 }

@@ -75,8 +75,9 @@ class KvCache:
         dev = D.require_cuda()
         tdt = dtype if isinstance(dtype, torch.dtype) else torch.from_numpy(np.zeros(0, dtype)).dtype
         h = n_heads if kv_heads is None else kv_heads
-        self._k = torch.zeros((batch, h, capacity, d_head), dtype=tdt, device=dev)
-        self._v = torch.zeros((batch, h, capacity, d_head), dtype=tdt, device=dev)
+        # rows past `length` are never read (keys()/values() slice), so no zero fill
+        self._k = torch.empty((batch, h, capacity, d_head), dtype=tdt, device=dev)
+        self._v = torch.empty((batch, h, capacity, d_head), dtype=tdt, device=dev)
         self._np = not isinstance(dtype, torch.dtype)
         self.length = 0
 
@@ -271,23 +272,28 @@ class PrefillPlan:
         """Per (batch, head) HeadPlan list from the device choice (one small D2H)."""
         v = self.views(ws)
         hh = self.hh
-        if self.mode == "dense":
-            return [[HeadPlan(head=h, pattern=None) for h in range(self.heads)] for _ in range(self.batch)]
-        if self.mode == "fixed":
-            return [[HeadPlan(head=h, pattern=self.fixed_pattern) for h in range(self.heads)]
-                    for _ in range(self.batch)]
+        if self.mode != "auto":
+            return self.plans_from(None, None, self.batch, self.heads, with_search)
         choice = _read_i32(v.choice, hh)
         errs = _read_f64(v.errors, hh * 3).reshape(hh, 3)
+        return self.plans_from(choice, errs, self.batch, self.heads, with_search)
+
+    def plans_from(self, choice, errs, batch: int, heads: int, with_search: bool = True):
+        """HeadPlan rows from host copies of the per-head choice and window errors."""
+        if self.mode == "dense":
+            return [[HeadPlan(head=h, pattern=None) for h in range(heads)] for _ in range(batch)]
+        if self.mode == "fixed":
+            return [[HeadPlan(head=h, pattern=self.fixed_pattern) for h in range(heads)] for _ in range(batch)]
         out = []
-        for b in range(self.batch):
+        for b in range(batch):
             row = []
-            for h in range(self.heads):
-                c = int(choice[b * self.heads + h])
+            for h in range(heads):
+                c = int(choice[b * heads + h])
                 rc, fp = self.refined[c], self.full[c]
                 res = None
                 if with_search:
                     res = SearchResult(chosen=fp, realized_flops=estimate_flops(fp, self.length, self.d_head, 0).total,
-                                       error=float(errs[b * self.heads + h, c]), iterations_used=rc.iterations,
+                                       error=float(errs[b * heads + h, c]), iterations_used=rc.iterations,
                                        converged=rc.converged)
                 row.append(HeadPlan(head=h, pattern=fp, search=res))
             out.append(row)
@@ -357,6 +363,10 @@ def prefill(q, k, v, cfg: ModelConfig, search: SearchSpace | None = None, mode: 
 
         raise SearchError(f"cal_window {cal_window} exceeds the dense evaluation cap {dense_cap}")
     dev = D.require_cuda()
+    if (D.is_torch(q) and D.is_torch(k) and D.is_torch(v) and not q.is_cuda and not k.is_cuda
+            and not v.is_cuda and cfg.d_head == D.HEAD_DIM):
+        return _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window, q_est,
+                                      batch, length, kv_heads)
     t0 = time.perf_counter()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     ev[0].record()
@@ -391,6 +401,97 @@ def prefill(q, k, v, cfg: ModelConfig, search: SearchSpace | None = None, mode: 
     select_s = ev[1].elapsed_time(ev[2]) / 1e3
     kernel_s = ev[2].elapsed_time(ev_end) / 1e3
     return PrefillResult(outputs=outputs, cache=cache, plans=plans, elapsed_s=elapsed,
+                         select_s=select_s, kernel_s=kernel_s)
+
+
+def _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window, q_est, batch, length,
+                           kv_heads) -> PrefillResult:
+    """prefill for host (CPU torch) inputs: the layer streams through the GPU one
+    kv-head group at a time so PCIe transfers overlap the kernels.
+
+    Per group (the g = H / HK query heads sharing one kv head): H2D of its
+    k, v, q on a copy stream; on the compute stream the finiteness check,
+    selection and sa_prefill (writing its column slice of the (B, L, H*d)
+    output through desc.out_ld) plus the KvCache fill; then a D2H of those
+    output columns on a third stream.  Group i's compute and D2H overlap
+    group i+1's H2D; the result is the same as the one-shot device path."""
+    dev = D.require_cuda()
+    t0 = time.perf_counter()
+    H, HK, n, d = cfg.n_heads, kv_heads, length, D.HEAD_DIM
+    g = H // HK
+    bf = torch.bfloat16
+    qs = q.reshape(batch * H, n, d)
+    ks = k.reshape(batch * HK, n, d)
+    vs = v.reshape(batch * HK, n, d)
+    if qs.dtype != bf:
+        qs, ks, vs = qs.to(bf), ks.to(bf), vs.to(bf)
+    qd = torch.empty((batch * H, n, d), dtype=bf, device=dev)
+    kd = torch.empty((batch * HK, n, d), dtype=bf, device=dev)
+    vd = torch.empty((batch * HK, n, d), dtype=bf, device=dev)
+    out = torch.empty((batch, n, H * d), dtype=bf, device=dev)
+    host_out = torch.empty((batch, n, H * d), dtype=bf, pin_memory=True)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    plan = PrefillPlan(1, g, 1, n, d, mode, search=search, fixed_pattern=fixed_pattern, cal_window=cal_window,
+                       q_est=q_est)
+    plan.desc.out_ld = H * d
+    ws = _workspace(plan.ws_bytes, dev)
+    view = plan.views(ws)
+    auto = mode == "auto"
+    choice_all = torch.zeros(batch * H, dtype=torch.int32, device=dev)
+    err_all = torch.zeros((batch * H, 3), dtype=torch.float64, device=dev)
+    cache = KvCache(batch, H, d, cfg.max_context, dtype=k.dtype, kv_heads=HK)
+    comp = torch.cuda.current_stream()
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    sel = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(batch * HK)]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(comp)
+    h2d.wait_stream(comp)
+    d2h.wait_stream(comp)
+    pitch = H * d * 2
+    for grp in range(batch * HK):
+        b, kh = divmod(grp, HK)
+        h0 = b * H + kh * g
+        with torch.cuda.stream(h2d):
+            kd[grp].copy_(ks[grp], non_blocking=True)
+            vd[grp].copy_(vs[grp], non_blocking=True)
+            qd[h0:h0 + g].copy_(qs[h0:h0 + g], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(h2d)
+        comp.wait_event(ready)
+        for x in (qd[h0:h0 + g], kd[grp], vd[grp]):
+            _lib.call("sa_check_finite_bf16", x.data_ptr(), x.numel(), flag.data_ptr(), comp.cuda_stream)
+        qg, kg, vg = qd[h0:h0 + g], kd[grp:grp + 1], vd[grp:grp + 1]
+        og = out[b, :, kh * g * d:]
+        sel[grp][0].record(comp)
+        if auto:
+            plan.select(qg, kg, ws)
+        sel[grp][1].record(comp)
+        plan.run(qg, kg, vg, og, ws)
+        if auto:
+            choice_all[h0:h0 + g].copy_(_wrap(view.choice, g, torch.int32))
+            err_all[h0:h0 + g].copy_(_wrap(view.errors, g * 3, torch.float64).view(g, 3))
+        cache._k[b, kh, :n].copy_(kd[grp])
+        cache._v[b, kh, :n].copy_(vd[grp])
+        done = torch.cuda.Event()
+        done.record(comp)
+        d2h.wait_event(done)
+        _lib.call("sa_memcpy2d_async", host_out.data_ptr() + (b * n * H + kh * g) * d * 2, pitch,
+                  og.data_ptr(), pitch, g * d * 2, n, d2h.cuda_stream)
+    e_end.record(comp)
+    comp.wait_stream(d2h)
+    torch.cuda.synchronize()
+    if int(flag.item()):
+        raise NonFiniteError("q, k or v contains NaN or Inf")
+    cache.length = n
+    cache._np = False
+    if auto:
+        plans = plan.plans_from(choice_all.cpu().numpy(), err_all.cpu().numpy(), batch, H)
+    else:
+        plans = plan.plans_from(None, None, batch, H)
+    select_s = sum(a.elapsed_time(z) for a, z in sel) / 1e3
+    kernel_s = e_start.elapsed_time(e_end) / 1e3 - select_s
+    outputs = host_out if q.dtype == bf else host_out.to(q.dtype)
+    return PrefillResult(outputs=outputs, cache=cache, plans=plans, elapsed_s=time.perf_counter() - t0,
                          select_s=select_s, kernel_s=kernel_s)
 
 

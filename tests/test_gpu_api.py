@@ -260,3 +260,40 @@ def test_golden_prefill(sa, cid):
     assert [conv(p) for p in got_plans] == [conv(p) for p in want]
     step = max(1, c["ctx"] // 64)
     close(res.outputs[0, ::step], arr[f"prefill_{cid}_rows"])
+
+
+@pytest.mark.parametrize("mode,n", [("auto", 1000), ("auto", 2048), ("dense", 300), ("fixed", 777)])
+def test_host_streamed_prefill_equals_device(sa, mode, n):
+    """CPU torch inputs stream through the GPU one kv group at a time; the
+    result (outputs, plans, cache) is identical to the device-input call."""
+    H, HK = 8, 2
+    q, k, v = O.synth_qkv_gqa(5, n, H, HK, 128)
+    q, k, v = (torch.from_numpy(O.bf16_round(x)).bfloat16() for x in (q, k, v))
+    cfg = sa.ModelConfig(n_heads=H, d_model=H * 128, d_head=128, max_context=n + 4)
+    kw = {"fixed_pattern": sa.VerticalSlash(40, 50)} if mode == "fixed" else {}
+    host = sa.prefill(q.pin_memory(), k.pin_memory(), v.pin_memory(), cfg, mode=mode, **kw)
+    dev = sa.prefill(q.cuda(), k.cuda(), v.cuda(), cfg, mode=mode, **kw)
+    assert not host.outputs.is_cuda and host.outputs.dtype == torch.bfloat16
+    assert torch.equal(host.outputs, dev.outputs.cpu())
+    assert [hp.pattern for hp in host.plans[0]] == [hp.pattern for hp in dev.plans[0]]
+    assert host.cache.length == n
+    assert torch.equal(host.cache.keys().cpu(), k.cuda().cpu())
+    assert torch.equal(host.cache.values().cpu(), v)
+    if mode == "auto":
+        e1 = [hp.search.error for hp in host.plans[0]]
+        e2 = [hp.search.error for hp in dev.plans[0]]
+        np.testing.assert_allclose(e1, e2, rtol=0, atol=0)
+
+
+def test_host_streamed_nonfinite(sa):
+    H, HK, n = 4, 2, 256
+    q, k, v = O.synth_qkv_gqa(6, n, H, HK, 128)
+    q, k, v = (torch.from_numpy(O.bf16_round(x)).bfloat16() for x in (q, k, v))
+    cfg = sa.ModelConfig(n_heads=H, d_model=H * 128, d_head=128, max_context=n)
+    v[0, 1, 17, 3] = float("nan")
+    with pytest.raises(sa.NonFiniteError):
+        sa.prefill(q, k, v, cfg, mode="auto")
+    v[0, 1, 17, 3] = 0.0
+    k[0, 0, n - 1, 127] = float("inf")
+    with pytest.raises(sa.NonFiniteError):
+        sa.prefill(q, k, v, cfg, mode="dense")
