@@ -10,7 +10,7 @@
 // weights in float64 (core.py:179-186), then takes the strict-< argmin in
 // candidate order (search.py:245-250: the earlier candidate wins ties).
 //
-// One CTA per head, everything in shared memory (cal <= 64, d <= 128).  The
+// One CTA per (head, candidate), everything in shared memory (cal <= 64, d <= 128).  The
 // family id written per head indexes the caller's candidate list; the host
 // has already refined the candidates and rescaled them to n (search.py:
 // 236-241, 261-273 — data-independent integer math).
@@ -58,20 +58,8 @@ struct SelectSmem {
   unsigned char colsel[kCalMax];
   unsigned char diagsel[kCalMax];
   unsigned char blksel[kCalMax][kCalMax];
-  double red[kSelThreads];
+  double red[kSelThreads / 32];
 };
-
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  red[threadIdx.x] = v;
-  __syncthreads();
-  for (int s = kSelThreads / 2; s > 0; s >>= 1) {
-    if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
-  const double r = red[0];
-  __syncthreads();
-  return r;
-}
 
 // stable top-k by rank: selected iff #{better} < k, better = larger score or
 // equal score at a lower index (patterns.py:231-234)
@@ -82,152 +70,233 @@ __device__ __forceinline__ bool rank_selected(const double* s, int len, int j, i
   return better < k;
 }
 
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One CTA per (head, candidate): blockIdx.x = head, blockIdx.y = candidate.
+// The dense part (logits, dense weights) is recomputed by each candidate's CTA
+// so the candidates run in parallel; rows are processed one warp per row with
+// shuffle reductions.  Writes err[hh, c]; select_argmin_kernel picks per head.
 __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
   extern __shared__ __align__(16) unsigned char sraw[];
   SelectSmem& S = *reinterpret_cast<SelectSmem*>(sraw);
   const int hh = blockIdx.x;
+  const int ci = blockIdx.y;
   const int bidx = hh / a.heads, h = hh % a.heads;
   const int hkv = bidx * a.kv_heads + h / (a.heads / a.kv_heads);
   const int cal = a.cal, n = a.n;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int kWarps = kSelThreads / 32;
   const __nv_bfloat16* qb = a.q + ((size_t)hh * n + (n - cal)) * kHeadDim;
   const __nv_bfloat16* kb = a.k + ((size_t)hkv * n + (n - cal)) * kHeadDim;
-  for (int e = tid; e < cal * kHeadDim; e += kSelThreads) {
-    const int r = e / kHeadDim, d = e % kHeadDim;
-    S.q[r][d] = __bfloat162float(qb[e]);
-    S.k[r][d] = __bfloat162float(kb[e]);
+  {
+    // 16-byte loads, all issued before any is consumed (one memory latency)
+    constexpr int kVec = kCalMax * kHeadDim / 8 / kSelThreads;  // uint4 per thread per matrix
+    uint4 qv[kVec], kv[kVec];
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) {
+      const int e = tid + u * kSelThreads;  // uint4 index: row e / 16, columns 8 (e % 16) ..
+      const bool ok = e < cal * (kHeadDim / 8);
+      qv[u] = ok ? __ldg(reinterpret_cast<const uint4*>(qb) + e) : make_uint4(0, 0, 0, 0);
+      kv[u] = ok ? __ldg(reinterpret_cast<const uint4*>(kb) + e) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) {
+      const int e = tid + u * kSelThreads;
+      if (e < cal * (kHeadDim / 8)) {
+        const int r = e / (kHeadDim / 8), d = 8 * (e % (kHeadDim / 8));
+        const uint32_t qw[4] = {qv[u].x, qv[u].y, qv[u].z, qv[u].w};
+        const uint32_t kw[4] = {kv[u].x, kv[u].y, kv[u].z, kv[u].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 a2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qw[t]));
+          const float2 b2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kw[t]));
+          S.q[r][d + 2 * t] = a2.x;
+          S.q[r][d + 2 * t + 1] = a2.y;
+          S.k[r][d + 2 * t] = b2.x;
+          S.k[r][d + 2 * t + 1] = b2.y;
+        }
+      }
+    }
   }
   __syncthreads();
-  // dense logits, causal
-  for (int e = tid; e < cal * cal; e += kSelThreads) {
-    const int r = e / cal, c = e % cal;
-    float acc = 0.f;
-    if (c <= r) {
-#pragma unroll 8
-      for (int d = 0; d < kHeadDim; ++d) acc = fmaf(S.q[r][d], S.k[c][d], acc);
+  // dense causal logits: each thread a 4x4 register tile of (row, column)
+  {
+    const int tr = tid / 16, tc = tid % 16;  // rows tr + 16 i, columns tc + 16 j
+    float acc[4][4] = {};
+    if (tr < cal) {
+#pragma unroll 4
+      for (int d = 0; d < kHeadDim; ++d) {
+        float qv[4], kv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          qv[i] = S.q[min(tr + 16 * i, kCalMax - 1)][d];
+          kv[i] = S.k[min(tc + 16 * i, kCalMax - 1)][d];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(qv[i], kv[j], acc[i][j]);
+      }
     }
-    S.L[r][c] = acc * a.scale;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = tr + 16 * i, c = tc + 16 * j;
+        if (r < cal && c < cal) S.L[r][c] = (c <= r) ? acc[i][j] * a.scale : 0.f;
+      }
   }
   __syncthreads();
-  // dense weights: one thread per row
-  for (int r = tid; r < cal; r += kSelThreads) {
-    float mx = -INFINITY;
-    for (int c = 0; c <= r; ++c) mx = fmaxf(mx, S.L[r][c]);
-    float sum = 0.f;
-    for (int c = 0; c <= r; ++c) {
-      const float e = expf(S.L[r][c] - mx);
-      S.Wd[r][c] = e;
-      sum += e;
-    }
-    for (int c = 0; c < cal; ++c) S.Wd[r][c] = (c <= r) ? S.Wd[r][c] / sum : 0.f;
+  // dense weights (core.py:138-154): one warp per row
+  for (int r = wid; r < cal; r += kWarps) {
+    const int c0 = lane, c1 = lane + 32;
+    const float l0 = (c0 <= r) ? S.L[r][c0] : -INFINITY;
+    const float l1 = (c1 <= r && c1 < cal) ? S.L[r][c1] : -INFINITY;
+    const float mx = warp_max(fmaxf(l0, l1));
+    const float e0 = (c0 <= r) ? expf(l0 - mx) : 0.f;
+    const float e1 = (c1 <= r && c1 < cal) ? expf(l1 - mx) : 0.f;
+    const float sum = warp_sum(e0 + e1);
+    if (c0 < cal) S.Wd[r][c0] = e0 / sum;
+    if (c1 < cal) S.Wd[r][c1] = e1 / sum;
   }
   __syncthreads();
 
-  double best = INFINITY;
-  int best_c = 0;
-  for (int ci = 0; ci < a.ncand; ++ci) {
-    const int fam = a.cand_fam[ci];
-    const int p1 = a.cand_p1[ci], p2 = a.cand_p2[ci];
-    if (fam == FAM_VS) {
-      // exact scoring over all cal rows (patterns.py:182-202), float64 sums
-      for (int j = tid; j < cal; j += kSelThreads) {
-        double cs = 0.0, ds = 0.0;
-        for (int r = 0; r < cal; ++r) cs += (double)S.Wd[r][j];
-        for (int r = j; r < cal; ++r) ds += (double)S.Wd[r][r - j];
-        S.colscore[j] = cs;
-        S.diagscore[j] = ds;
-      }
-      __syncthreads();
-      const int kv = min(p1, cal), ks = min(p2, cal);
-      for (int j = tid; j < cal; j += kSelThreads) {
-        S.colsel[j] = rank_selected(S.colscore, cal, j, kv);
-        S.diagsel[j] = rank_selected(S.diagscore, cal, j, ks);
-      }
-      __syncthreads();
-    } else if (fam == FAM_BLOCK) {
-      const int b = min(p1, cal);
-      const int nb = (cal + b - 1) / b;
-      const int kbk = min(p2, nb);
-      for (int e = tid; e < nb * kHeadDim; e += kSelThreads) {
-        const int g = e / kHeadDim, d = e % kHeadDim;
-        const int r0 = g * b, r1 = min(cal, r0 + b);
-        float sq = 0.f, sk = 0.f;
-        for (int r = r0; r < r1; ++r) {
-          sq += S.q[r][d];
-          sk += S.k[r][d];
-        }
-        S.pq[g][d] = sq / (float)(r1 - r0);
-        S.pk[g][d] = sk / (float)(r1 - r0);
-      }
-      __syncthreads();
-      for (int e = tid; e < nb * nb; e += kSelThreads) {
-        const int g = e / nb, c = e % nb;
-        float acc = 0.f;
-        for (int d = 0; d < kHeadDim; ++d) acc = fmaf(S.pq[g][d], S.pk[c][d], acc);
-        S.BL[g][c] = acc * a.scale;
-      }
-      __syncthreads();
-      for (int e = tid; e < nb * nb; e += kSelThreads) {
-        const int g = e / nb, c = e % nb;
-        bool sel = false;
-        if (c <= g) {
-          const int keff = min(kbk, g + 1);
-          int better = 0;
-          const float v = S.BL[g][c];
-          for (int i = 0; i <= g; ++i) better += (S.BL[g][i] > v) || (S.BL[g][i] == v && i < c);
-          sel = (better < keff) || (c == g);
-        }
-        S.blksel[g][c] = sel;
-      }
-      __syncthreads();
-    }
-    // candidate mask
-    for (int e = tid; e < cal * cal; e += kSelThreads) {
-      const int r = e / cal, c = e % cal;
-      bool m = false;
-      if (c <= r) {
-        if (fam == FAM_TRI) {
-          m = (r - c < p1) || (c < p2) || (r == c);
-        } else if (fam == FAM_VS) {
-          m = S.colsel[c] || S.diagsel[r - c] || (r == c);
-        } else {
-          const int b = min(p1, cal);
-          m = S.blksel[r / b][c / b];
-        }
-      }
-      S.M[r][c] = m;
+  // (selects, not a dynamic index, so the parameter arrays stay in constant space)
+  const int fam = ci == 0 ? a.cand_fam[0] : (ci == 1 ? a.cand_fam[1] : a.cand_fam[2]);
+  const int p1 = ci == 0 ? a.cand_p1[0] : (ci == 1 ? a.cand_p1[1] : a.cand_p1[2]);
+  const int p2 = ci == 0 ? a.cand_p2[0] : (ci == 1 ? a.cand_p2[1] : a.cand_p2[2]);
+  if (fam == FAM_VS) {
+    // exact scoring over all cal rows (patterns.py:182-202), float64 sums
+    for (int j = tid; j < cal; j += kSelThreads) {
+      double cs = 0.0, ds = 0.0;
+      for (int r = 0; r < cal; ++r) cs += (double)S.Wd[r][j];
+      for (int r = j; r < cal; ++r) ds += (double)S.Wd[r][r - j];
+      S.colscore[j] = cs;
+      S.diagscore[j] = ds;
     }
     __syncthreads();
-    // sparse weights per row vs dense, squared error in float64
-    double part = 0.0;
-    for (int r = tid; r < cal; r += kSelThreads) {
-      float mx = -INFINITY;
-      for (int c = 0; c <= r; ++c)
-        if (S.M[r][c]) mx = fmaxf(mx, S.L[r][c]);
-      float sum = 0.f;
-      for (int c = 0; c <= r; ++c)
-        if (S.M[r][c]) sum += expf(S.L[r][c] - mx);
-      for (int c = 0; c < cal; ++c) {
-        float w = 0.f;
-        if (c <= r && S.M[r][c]) w = expf(S.L[r][c] - mx) / sum;
+    const int kv = min(p1, cal), ks = min(p2, cal);
+    for (int j = tid; j < cal; j += kSelThreads) {
+      S.colsel[j] = rank_selected(S.colscore, cal, j, kv);
+      S.diagsel[j] = rank_selected(S.diagscore, cal, j, ks);
+    }
+    __syncthreads();
+  } else if (fam == FAM_BLOCK) {
+    const int b = min(p1, cal);
+    const int nb = (cal + b - 1) / b;
+    const int kbk = min(p2, nb);
+    for (int e = tid; e < nb * kHeadDim; e += kSelThreads) {
+      const int g = e / kHeadDim, d = e % kHeadDim;
+      const int r0 = g * b, r1 = min(cal, r0 + b);
+      float sq = 0.f, sk = 0.f;
+      for (int r = r0; r < r1; ++r) {
+        sq += S.q[r][d];
+        sk += S.k[r][d];
+      }
+      S.pq[g][d] = sq / (float)(r1 - r0);
+      S.pk[g][d] = sk / (float)(r1 - r0);
+    }
+    __syncthreads();
+    for (int e = tid; e < nb * nb; e += kSelThreads) {
+      const int g = e / nb, c = e % nb;
+      float acc = 0.f;
+      for (int d = 0; d < kHeadDim; ++d) acc = fmaf(S.pq[g][d], S.pk[c][d], acc);
+      S.BL[g][c] = acc * a.scale;
+    }
+    __syncthreads();
+    for (int e = tid; e < nb * nb; e += kSelThreads) {
+      const int g = e / nb, c = e % nb;
+      bool sel = false;
+      if (c <= g) {
+        const int keff = min(kbk, g + 1);
+        int better = 0;
+        const float v = S.BL[g][c];
+        for (int i = 0; i <= g; ++i) better += (S.BL[g][i] > v) || (S.BL[g][i] == v && i < c);
+        sel = (better < keff) || (c == g);
+      }
+      S.blksel[g][c] = sel;
+    }
+    __syncthreads();
+  }
+  // candidate mask
+  for (int e = tid; e < cal * cal; e += kSelThreads) {
+    const int r = e / cal, c = e % cal;
+    bool m = false;
+    if (c <= r) {
+      if (fam == FAM_TRI) {
+        m = (r - c < p1) || (c < p2) || (r == c);
+      } else if (fam == FAM_VS) {
+        m = S.colsel[c] || S.diagsel[r - c] || (r == c);
+      } else {
+        const int b = min(p1, cal);
+        m = S.blksel[r / b][c / b];
+      }
+    }
+    S.M[r][c] = m;
+  }
+  __syncthreads();
+  // sparse weights per row vs dense, squared error in float64 (core.py:179-186)
+  double part = 0.0;
+  for (int r = wid; r < cal; r += kWarps) {
+    float lv[2];
+    bool mv[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int c = lane + 32 * t;
+      mv[t] = c < cal && c <= r && S.M[r][c];
+      lv[t] = mv[t] ? S.L[r][c] : -INFINITY;
+    }
+    const float mx = warp_max(fmaxf(lv[0], lv[1]));
+    float ev[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) ev[t] = mv[t] ? expf(lv[t] - mx) : 0.f;
+    const float sum = warp_sum(ev[0] + ev[1]);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int c = lane + 32 * t;
+      if (c < cal) {
+        const float w = mv[t] ? ev[t] / sum : 0.f;
         const double dlt = (double)w - (double)S.Wd[r][c];
         part += dlt * dlt;
       }
     }
-    const double err = sqrt(block_sum(part, S.red));
-    if (tid == 0) {
-      if (a.err_out) a.err_out[(size_t)hh * 3 + ci] = err;
-    }
-    if (err < best) {
-      best = err;
-      best_c = ci;
-    }
-    __syncthreads();
   }
+  part = warp_sum(part);
+  if (lane == 0) S.red[wid] = part;
+  __syncthreads();
   if (tid == 0) {
-    a.choice_out[hh] = best_c;
-    if (a.family_out) a.family_out[hh] = a.cand_fam[best_c];
+    double tot = 0.0;
+    for (int w = 0; w < kWarps; ++w) tot += S.red[w];
+    a.err_out[(size_t)hh * 3 + ci] = sqrt(tot);
   }
+}
+
+// strict-< argmin in candidate order (search.py:245-250: earlier wins ties)
+__global__ void select_argmin_kernel(const double* err, int hh_total, int ncand, const int32_t* fam,
+                                     int32_t* choice_out, int32_t* family_out, int f0, int f1, int f2) {
+  const int hh = blockIdx.x * blockDim.x + threadIdx.x;
+  if (hh >= hh_total) return;
+  double best = INFINITY;
+  int best_c = 0;
+  for (int c = 0; c < ncand; ++c) {
+    const double e = err[(size_t)hh * 3 + c];
+    if (e < best) {
+      best = e;
+      best_c = c;
+    }
+  }
+  choice_out[hh] = best_c;
+  if (family_out) family_out[hh] = best_c == 0 ? f0 : (best_c == 1 ? f1 : f2);
 }
 
 }  // namespace sa
@@ -267,8 +336,24 @@ int launch_select(int batch, int heads, int kv_heads, int n, int cal, float scal
                          (int)sizeof(SelectSmem));
     attr = true;
   }
-  select_kernel<<<a.hh_total, kSelThreads, sizeof(SelectSmem), stream>>>(a);
-  return check_launch("select_kernel");
+  if (!a.err_out) {  // callers that do not want the errors still need a scratch row per head
+    static double* scratch = nullptr;
+    static int scratch_heads = 0;
+    if (scratch_heads < a.hh_total) {
+      if (scratch) cudaFree(scratch);
+      if (cudaMalloc(&scratch, (size_t)a.hh_total * 3 * sizeof(double)) != cudaSuccess)
+        return fail(SA_ERR_CUDA, "selector scratch allocation failed");
+      scratch_heads = a.hh_total;
+    }
+    a.err_out = scratch;
+  }
+  select_kernel<<<dim3(a.hh_total, ncand), kSelThreads, sizeof(SelectSmem), stream>>>(a);
+  int rc = check_launch("select_kernel");
+  if (rc) return rc;
+  select_argmin_kernel<<<(a.hh_total + 127) / 128, 128, 0, stream>>>(
+      a.err_out, a.hh_total, ncand, nullptr, choice_out, family_out, a.cand_fam[0],
+      ncand > 1 ? a.cand_fam[1] : 0, ncand > 2 ? a.cand_fam[2] : 0);
+  return check_launch("select_argmin_kernel");
 }
 }  // namespace sa
 

@@ -158,25 +158,43 @@ __global__ void build_tiles_kernel(TileBuildArgs a) {
 // qt) with the r-th largest tile count (counting sort, one CTA).  The block
 // scheduler dispatches CTAs roughly in blockIdx order, so the heaviest query
 // tiles (full-width VS rows) start first and the light ones fill the tail.
-__global__ void order_work_kernel(const int32_t* __restrict__ cnt, int items, int max_cnt,
-                                  int32_t* __restrict__ work) {
-  extern __shared__ int32_t start[];  // [max_cnt + 2]
-  const int bins = max_cnt + 1;
-  for (int c = threadIdx.x; c <= bins; c += blockDim.x) start[c] = 0;
+__global__ void __launch_bounds__(1024) order_work_kernel(const int32_t* __restrict__ cnt, int items,
+                                                          int max_cnt, int32_t* __restrict__ work) {
+  // bins: tile count >> shift, at most 1024 (one per thread), heaviest first
+  __shared__ int start[1024];
+  __shared__ int wsum[32];
+  int shift = 0;
+  while ((max_cnt >> shift) >= 1024) ++shift;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  start[t] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < items; i += blockDim.x) atomicAdd(&start[min(max(cnt[i], 0), max_cnt)], 1);
+  for (int i = t; i < items; i += blockDim.x) atomicAdd(&start[1023 - min(max(cnt[i], 0) >> shift, 1023)], 1);
   __syncthreads();
-  if (threadIdx.x == 0) {  // bins <= 2049: exclusive scan from the heaviest bin down
-    int run = 0;
-    for (int c = max_cnt; c >= 0; --c) {
-      const int h = start[c];
-      start[c] = run;
-      run += h;
+  // exclusive scan over position p = 1023 - bin (heaviest bin first)
+  const int v = start[t];
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    const int s0 = wsum[lane];
+    int sc = s0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, sc, o);
+      if (lane >= o) sc += y;
     }
+    wsum[lane] = sc - s0;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < items; i += blockDim.x) {
-    const int pos = atomicAdd(&start[min(max(cnt[i], 0), max_cnt)], 1);
+  start[t] = wsum[w] + x - v;
+  __syncthreads();
+  for (int i = t; i < items; i += blockDim.x) {
+    const int pos = atomicAdd(&start[1023 - min(max(cnt[i], 0) >> shift, 1023)], 1);
     work[pos] = i;
   }
 }
@@ -213,7 +231,7 @@ extern "C" int sa_order_work(const int32_t* tile_cnt, int items, int max_cnt, in
   using namespace sa;
   if (items < 1 || max_cnt < 0 || max_cnt > 65536) return fail(SA_ERR_DIMENSION, "bad work-order sizes");
   if (!tile_cnt || !work) return fail(SA_ERR_DIMENSION, "null pointer");
-  order_work_kernel<<<1, 1024, (max_cnt + 2) * sizeof(int32_t), reinterpret_cast<cudaStream_t>(stream)>>>(
+  order_work_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       tile_cnt, items, max_cnt, work);
   return check_launch("order_work_kernel");
 }

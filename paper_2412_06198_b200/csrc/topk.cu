@@ -44,9 +44,33 @@ __device__ __forceinline__ uint64_t composite(uint32_t key, int j) {
   return (static_cast<uint64_t>(key) << 32) | static_cast<uint32_t>(0xffffffffu - (uint32_t)j);
 }
 
-// bin of `key` in [lo, lo + span) split into kBins equal key intervals (monotone)
-__device__ __forceinline__ int key_bin(uint32_t key, uint32_t lo, uint64_t span) {
-  return (int)(((uint64_t)(key - lo) * kBins) / span);
+// Row access: CACHED rows were converted to preference keys in shared memory
+// by one coalesced pass; otherwise every pass re-reads the fp32 row (L2).
+template <bool CACHED>
+__device__ __forceinline__ uint32_t key_at(const float* s, const uint32_t* skey, int j) {
+  if (CACHED) return skey[j];
+  return pref_key(__ldg(s + j));
+}
+
+// bin of `key` in [lo, lo + span): floor((key - lo) * scale / 2^32) with
+// scale = floor(kBins * 2^32 / span) split as s_hi * 2^32 + s_lo, so the map
+// is two integer multiplies (monotone, < kBins) instead of a 64-bit division.
+struct BinMap {
+  uint32_t lo, s_hi, s_lo;
+};
+__host__ __device__ inline BinMap make_binmap(uint32_t lo, uint64_t span) {
+  const uint64_t scale = ((uint64_t)kBins << 32) / span;
+  return BinMap{lo, (uint32_t)(scale >> 32), (uint32_t)scale};
+}
+__device__ __forceinline__ int key_bin(uint32_t key, const BinMap& m) {
+  const uint32_t x = key - m.lo;
+  return (int)(x * m.s_hi + __umulhi(x, m.s_lo));
+}
+// first offset x (from lo) whose bin is >= b
+__device__ __forceinline__ uint64_t bin_start(int b, uint64_t span) {
+  const uint64_t scale = ((uint64_t)kBins << 32) / span;
+  const uint64_t x = (((uint64_t)b << 32) + scale - 1) / scale;
+  return x < span ? x : span;
 }
 
 // Exclusive block-wide scan of one int per thread (any warp count <= 32).
@@ -80,23 +104,25 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
 
 // Histogram of the keys inside [lo, lo + span) into kBins bins; returns the bin
 // holding the `want`-th largest of them and the count in higher bins.
-__device__ void hist_locate(const float* s, int len, uint32_t lo, uint64_t span, int want,
+template <bool CACHED>
+__device__ void hist_locate(const float* s, const uint32_t* skey, int len, uint32_t lo, uint64_t span, int want,
                             int* hist, int* warp_tot, int* sh_pair, int& bin_out, int& above_out) {
   const int tid = threadIdx.x;
   for (int t = tid; t < kBins; t += blockDim.x) hist[t] = 0;
   __syncthreads();
+  const BinMap bm = make_binmap(lo, span);
   for (int j0 = tid; j0 < len; j0 += 8 * blockDim.x) {
     uint32_t key[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int j = j0 + u * blockDim.x;
-      key[u] = j < len ? pref_key(__ldg(s + j)) : 0u;
+      key[u] = j < len ? key_at<CACHED>(s, skey, j) : 0u;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int j = j0 + u * blockDim.x;
       if (j < len && key[u] >= lo && (uint64_t)(key[u] - lo) < span)
-        atomicAdd(&hist[key_bin(key[u], lo, span)], 1);
+        atomicAdd(&hist[key_bin(key[u], bm)], 1);
     }
   }
   __syncthreads();
@@ -125,6 +151,7 @@ __device__ void hist_locate(const float* s, int len, uint32_t lo, uint64_t span,
   above_out = sh_pair[1];
 }
 
+template <bool CACHED>
 __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
   int r = blockIdx.x;
   const float* scores = a.scores;
@@ -152,6 +179,21 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
   extern __shared__ __align__(16) uint8_t tk_smem[];
   int* hist = reinterpret_cast<int*>(tk_smem);
   uint64_t* cand = reinterpret_cast<uint64_t*>(tk_smem + kBins * 4);
+  uint32_t* skey = reinterpret_cast<uint32_t*>(tk_smem + kTopkSmem);  // CACHED: [len]
+  if (CACHED) {
+    // one coalesced 16-byte pass: fp32 row -> preference keys in shared memory
+    const bool vec = ((reinterpret_cast<uintptr_t>(s) & 15) == 0);
+    const int n4 = vec ? len / 4 : 0;
+    for (int j4 = threadIdx.x; j4 < n4; j4 += blockDim.x) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(s) + j4);
+      skey[4 * j4] = pref_key(v.x);
+      skey[4 * j4 + 1] = pref_key(v.y);
+      skey[4 * j4 + 2] = pref_key(v.z);
+      skey[4 * j4 + 3] = pref_key(v.w);
+    }
+    for (int j = 4 * n4 + threadIdx.x; j < len; j += blockDim.x) skey[j] = pref_key(__ldg(s + j));
+    __syncthreads();
+  }
   __shared__ int warp_tot[33];
   __shared__ uint32_t sh_min, sh_max;
   __shared__ int sh_m;
@@ -167,18 +209,17 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
     // 1. key range
     uint32_t mn = 0xffffffffu, mx = 0u;
     for (int j0 = tid; j0 < len; j0 += 8 * blockDim.x) {
-      float v[8];
+      uint32_t v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int j = j0 + u * blockDim.x;
-        v[u] = j < len ? __ldg(s + j) : 0.f;
+        v[u] = j < len ? key_at<CACHED>(s, skey, j) : 0u;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         if (j0 + u * (int)blockDim.x < len) {
-          const uint32_t key = pref_key(v[u]);
-          mn = min(mn, key);
-          mx = max(mx, key);
+          mn = min(mn, v[u]);
+          mx = max(mx, v[u]);
         }
       }
     }
@@ -203,12 +244,12 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
     bool located = false;
     for (int level = 0; level < 2 && !located; ++level) {
       int bin, above;
-      hist_locate(s, len, lo, span, want, hist, warp_tot, sh_pair, bin, above);
+      hist_locate<CACHED>(s, skey, len, lo, span, want, hist, warp_tot, sh_pair, bin, above);
       const int m = sh_pair[2];
       want -= above;
       // narrow the key range to the bin: keys with key_bin == bin
-      const uint64_t b0 = ((uint64_t)bin * span + kBins - 1) / kBins;
-      const uint64_t b1 = ((uint64_t)(bin + 1) * span + kBins - 1) / kBins;
+      const uint64_t b0 = bin_start(bin, span);
+      const uint64_t b1 = bin_start(bin + 1, span);
       lo = lo + (uint32_t)b0;
       span = b1 - b0;
       if (m > kCand) continue;
@@ -216,16 +257,16 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
       if (tid == 0) sh_m = 0;
       __syncthreads();
       for (int j0 = tid; (j0 & ~31) < len; j0 += 8 * blockDim.x) {  // warp-uniform trip count
-        float v[8];
+        uint32_t v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int j = j0 + u * blockDim.x;
-          v[u] = j < len ? __ldg(s + j) : 0.f;
+          v[u] = j < len ? key_at<CACHED>(s, skey, j) : 0u;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int j = j0 + u * blockDim.x;
-          const uint32_t key = pref_key(v[u]);
+          const uint32_t key = v[u];
           const bool hit = j < len && key >= lo && (uint64_t)(key - lo) < span;
           const uint32_t bal = __ballot_sync(0xffffffffu, hit);
           if (bal) {
@@ -258,7 +299,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
         for (int t = tid; t < 256; t += blockDim.x) hist[t] = 0;
         __syncthreads();
         for (int j = tid; j < len; j += blockDim.x) {
-          const uint32_t key = pref_key(__ldg(s + j));
+          const uint32_t key = key_at<CACHED>(s, skey, j);
           if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
         }
         __syncthreads();
@@ -282,13 +323,13 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
       const int per = (len + blockDim.x - 1) / blockDim.x;
       const int b0 = min(len, tid * per), b1 = min(len, b0 + per);
       int eq = 0;
-      for (int j = b0; j < b1; ++j) eq += pref_key(__ldg(s + j)) == prefix;
+      for (int j = b0; j < b1; ++j) eq += key_at<CACHED>(s, skey, j) == prefix;
       int tot;
       const int before = block_excl_scan(eq, warp_tot, tot);
       if (before < remaining && before + eq >= remaining) {
         int seen = before;
         for (int j = b0; j < b1; ++j) {
-          if (pref_key(__ldg(s + j)) == prefix && ++seen == remaining) {
+          if (key_at<CACHED>(s, skey, j) == prefix && ++seen == remaining) {
             sh_T = composite(prefix, j);
             break;
           }
@@ -306,7 +347,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
   const int w0 = min(len, w * wlen), w1 = min(len, w0 + wlen);
   int mine = 0;
   for (int j = w0 + lane; (j - lane) < w1; j += 32) {
-    const bool keep = j < w1 && (take_all || (k > 0 && composite(pref_key(__ldg(s + j)), j) >= T));
+    const bool keep = j < w1 && (take_all || (k > 0 && composite(key_at<CACHED>(s, skey, j), j) >= T));
     mine += __popc(__ballot_sync(0xffffffffu, keep));
   }
   int total;
@@ -314,7 +355,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
   int pos = __shfl_sync(0xffffffffu, wbase, 0);
   if (mine > 0) {
     for (int j = w0 + lane; (j - lane) < w1; j += 32) {
-      const bool keep = j < w1 && (take_all || (k > 0 && composite(pref_key(__ldg(s + j)), j) >= T));
+      const bool keep = j < w1 && (take_all || (k > 0 && composite(key_at<CACHED>(s, skey, j), j) >= T));
       const uint32_t bal = __ballot_sync(0xffffffffu, keep);
       if (keep) {
         const int p = pos + __popc(bal & ((1u << lane) - 1u));
@@ -335,7 +376,19 @@ int launch_topk(const TopkArgs& a, cudaStream_t st) {
   if (rows <= 0) return SA_OK;
   // short segmented rows (block estimator) use 256 threads per row
   const int threads = (a.lens != nullptr && a.n <= 4096) ? 256 : kTopkThreads;
-  topk_rows_kernel<<<rows, threads, kTopkSmem, st>>>(a);
+  // rows up to kCacheMax keys are staged in shared memory once
+  constexpr int kCacheMax = 49152;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(topk_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kTopkSmem + kCacheMax * 4);
+    attr = true;
+  }
+  const int maxlen = a.lens ? a.n : a.n;  // a.n bounds every row length
+  if (maxlen <= kCacheMax && a.lens == nullptr)
+    topk_rows_kernel<true><<<rows, threads, kTopkSmem + maxlen * 4, st>>>(a);
+  else
+    topk_rows_kernel<false><<<rows, threads, kTopkSmem, st>>>(a);
   return check_launch("topk_rows_kernel");
 }
 

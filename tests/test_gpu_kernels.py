@@ -304,3 +304,23 @@ def test_selector_vs_oracle(sa):
         res = O.select(qh, kh, kh, ospace)
         assert refined[choice[h]].pattern.__class__.__name__[0] == {O.Tri: "T", O.VS: "V", O.Blk: "B"}[type(res[0])]
         np.testing.assert_allclose(errs[h], res[5], rtol=1e-4)
+
+
+@pytest.mark.parametrize("items,max_cnt", [(1, 0), (1000, 7), (8192, 256), (20000, 2048)])
+def test_order_work_is_heaviest_first_permutation(sa, items, max_cnt):
+    """sa_order_work: a permutation of the items, tile counts non-increasing
+    (exact below 1024 distinct counts, else within one count bucket)."""
+    from paper_2412_06198_b200 import _lib
+
+    rng = np.random.default_rng(items)
+    cnt = torch.from_numpy(rng.integers(0, max_cnt + 1, items).astype(np.int32)).cuda()
+    work = torch.empty(items, dtype=torch.int32, device="cuda")
+    _lib.call("sa_order_work", cnt.data_ptr(), items, max_cnt, work.data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    w = work.cpu().numpy()
+    np.testing.assert_array_equal(np.sort(w), np.arange(items))
+    c = cnt.cpu().numpy()[w]
+    shift = 0
+    while (max_cnt >> shift) >= 1024:
+        shift += 1
+    assert np.all(np.diff(c >> shift) <= 0)
