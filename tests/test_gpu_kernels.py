@@ -324,3 +324,24 @@ def test_order_work_is_heaviest_first_permutation(sa, items, max_cnt):
     while (max_cnt >> shift) >= 1024:
         shift += 1
     assert np.all(np.diff(c >> shift) <= 0)
+
+
+@pytest.mark.parametrize("case", ["zeros", "repeated_keys", "two_level"])
+def test_block_top1_ties_and_overflow(sa, case):
+    """k_b = 1 filter/refine path on degenerate inputs: exact ties everywhere
+    (every row overflows the candidate list and takes the exact scan) must
+    still pick the lowest block id, like the reference's stable top-k."""
+    n, b = 2048, 8
+    rng = np.random.default_rng(31)
+    q = rand_heads(40, 1, n)[0]
+    k = rand_heads(41, 1, n)[0]
+    if case == "zeros":
+        q = np.zeros_like(q)
+    elif case == "repeated_keys":
+        k = np.tile(k[:b], (n // b, 1))
+    else:  # many near-ties: two distinct key blocks repeated
+        k = np.tile(np.concatenate([k[:b], k[b:2 * b]]), (n // (2 * b), 1))
+    got = device_block_rows(q, k, b, 1)
+    want = O.block_index(q.astype(np.float64), k.astype(np.float64), b, 1).block_rows
+    for g, (r_got, r_want) in enumerate(zip(got, want)):
+        assert r_got == r_want.tolist(), (g, r_got, r_want.tolist())
