@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -57,6 +58,7 @@ struct AttnArgs {
   HeadIndexView idx;
   float* lse;  // optional [hh_total, n] natural-log row log-sum-exp
   unsigned long long* prof;  // SA_ATTN_PROF builds: per-role phase cycle counters [3 * 16]
+  int* counter;              // optional work-item counter (zeroed before launch): dynamic fetch
 };
 
 constexpr int kThreads = 192;
@@ -83,14 +85,18 @@ constexpr int kSmemBar = kSmemRing + kRing * kSlotBytes;           // 114688
 constexpr int kSmemBytes = kSmemBar + 256;  // + barriers; base is 1024-aligned (two CTAs per SM must fit)
 
 enum Bar {
-  B_Q = 0,
-  B_FULL0 = 1,                 // kRing
+  B_Q = 0,                     // Q tile landed
+  B_QE = 1,                    // every QK MMA of the item completed (Q buffer free)
+  B_FULL0 = 2,                 // kRing
   B_EMPTY0 = B_FULL0 + kRing,  // kRing
   B_SF0 = B_EMPTY0 + kRing,    // 2
   B_PF0 = B_SF0 + 2,           // 2
   B_OD = B_PF0 + 2,            // O updated by PV(u)
-  B_OF = B_OD + 1,             // final O
-  B_NUM = B_OF + 1
+  B_OF = B_OD + 1,             // final O of the item
+  B_OE = B_OF + 1,             // epilogue has read O
+  B_IF0 = B_OE + 1,            // 2: work-item slot published
+  B_IE0 = B_IF0 + 2,           // 2: work-item slot consumed
+  B_NUM = B_IE0 + 2
 };
 
 // Per-row constants of the mask builders, loaded once per CTA.
@@ -205,6 +211,24 @@ __device__ __forceinline__ void mask_make(const AttnArgs& a, const RowConst& c, 
   }
 }
 
+// Work item idx -> (hh * nqt + qt): the caller's order (LPT), else kv-group-major
+// (the group's K/V stays L2-resident), heaviest query tiles first in a group.
+__device__ __forceinline__ int item_at(const AttnArgs& a, int idx) {
+  if (a.work != nullptr) return a.work[idx];
+  const int gs = a.heads / a.kv_heads;
+  const int per_group = a.nqt * gs;
+  const int g = idx / per_group, r = idx % per_group;
+  const int qt = a.nqt - 1 - r / gs;
+  const int hh_ = (g / a.kv_heads) * a.heads + (g % a.kv_heads) * gs + r % gs;
+  return hh_ * a.nqt + qt;
+}
+
+// Persistent: each CTA (two per SM) walks work items (head, query tile).  The
+// producer fetches the next item (an atomic counter over the LPT list, or a
+// static stride) and publishes it through a two-slot shared-memory queue; the
+// barrier phases run on across items, so the next item's Q load and first
+// QK MMAs overlap the current item's last sub-tiles and epilogue.
+//
 // POLY > 0: every POLY-th exp pair of a row chunk runs on the FMA pipe
 // (exp2_poly2) instead of MUFU, balancing the two pipes.
 template <int POLY>
@@ -216,33 +240,15 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
   uint8_t* sRing = smem + kSmemRing;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + B_NUM);
+  volatile int* sItem = reinterpret_cast<volatile int*>(tmem_holder + 4);  // [2]
 
   const long long t_entry = kProf ? clock64() : 0;
   const int warp = warp_id();
-  int item;
-  if (a.work != nullptr) {
-    item = a.work[blockIdx.x];
-  } else {
-    // kv-group-major (the group's K/V stays L2-resident while its CTAs run),
-    // heaviest query tiles first inside a group, the group's q-heads adjacent
-    const int gs = a.heads / a.kv_heads;
-    const int per_group = a.nqt * gs;
-    const int g = blockIdx.x / per_group, r = blockIdx.x % per_group;
-    const int qt = a.nqt - 1 - r / gs;
-    const int hh_ = (g / a.kv_heads) * a.heads + (g % a.kv_heads) * gs + r % gs;
-    item = hh_ * a.nqt + qt;
-  }
-  const int hh = item / a.nqt;
-  const int qt = item % a.nqt;
-  const int bidx = hh / a.heads;
-  const int h = hh % a.heads;
-  const int hkv = bidx * a.kv_heads + h / (a.heads / a.kv_heads);
-  const int cnt = a.tile_cnt[item];
-  const int nsub = 2 * cnt;
-  const uint32_t* tl = a.tiles + a.tile_off[item];
+  const int n_items = a.hh_total * a.nqt;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[B_Q], 1);
+    mbar_init(&bars[B_QE], 1);
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&bars[B_FULL0 + i], 1);
       mbar_init(&bars[B_EMPTY0 + i], 1);
@@ -250,9 +256,12 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars[B_SF0 + i], 1);
       mbar_init(&bars[B_PF0 + i], 128);
+      mbar_init(&bars[B_IF0 + i], 1);
+      mbar_init(&bars[B_IE0 + i], 1 + 128);
     }
     mbar_init(&bars[B_OD], 1);
     mbar_init(&bars[B_OF], 1);
+    mbar_init(&bars[B_OE], 128);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc(tmem_holder, kTmemCols);
@@ -262,278 +271,332 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
   const uint32_t tbase = *tmem_holder;
 
   if (warp == 4) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ producer
     const int lane = lane_id();
     if (lane == 0) {
       tma_prefetch(&a.tmap_q);
       tma_prefetch(&a.tmap_k);
       tma_prefetch(&a.tmap_v);
-      mbar_arrive_expect_tx(&bars[B_Q], 32768);
-      tma_load_3d(sQ, &a.tmap_q, &bars[B_Q], 0, qt * kTile, hh);
-      tma_load_3d(sQ + 16384, &a.tmap_q, &bars[B_Q], 64, qt * kTile, hh);
     }
-    const int bsz = a.idx.blk_b[hh];
     PT_INIT
-    int slot_gk = 0;  // gather tiles: key block of slot `lane` (0 = placeholder, masked)
-    // ring sequence: K_0, V_0, K_1, V_1, ... (sub-tiles u = 2 j + half)
-    for (int i = 0; i < 2 * nsub; ++i) {
-      const int u = i >> 1;
-      const int slot = i % kRing;
-      const uint32_t e = tl[u >> 1];
-      const uint32_t kind = tile_kind(e);
-      if (kind == TK_GATHER && (i & 3) == 0) {
-        const int gq = qt * (kTile / bsz) + lane;
-        const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
-        int gk = 0;
-        if (lane < kTile / bsz && gq * bsz < a.n) {
-          const int k = ro[gq] + (int)tile_ktile(e);
-          if (k < ro[gq + 1]) {
-            const int x = a.idx.blk_idx[k];
-            if (x < gq) gk = x;
+    int rb = 0;  // ring items issued by this CTA so far
+    for (int J = 0;; ++J) {
+      // fetch and publish the next work item
+      int idx = 0;
+      if (lane == 0) idx = a.counter ? atomicAdd(a.counter, 1) : (int)blockIdx.x + J * (int)gridDim.x;
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      const int item = idx < n_items ? item_at(a, idx) : -1;
+      if (J >= 2) mbar_wait(&bars[B_IE0 + (J & 1)], ((J >> 1) - 1) & 1);
+      if (lane == 0) {
+        sItem[J & 1] = item;
+        mbar_arrive(&bars[B_IF0 + (J & 1)]);
+      }
+      if (item < 0) break;
+      const int hh = item / a.nqt, qt = item % a.nqt;
+      const int hkv = (hh / a.heads) * a.kv_heads + (hh % a.heads) / (a.heads / a.kv_heads);
+      const int cnt = a.tile_cnt[item];
+      const int nsub = 2 * cnt;
+      const uint32_t* tl = a.tiles + a.tile_off[item];
+      // Q: the buffer is free once every QK MMA of the previous item completed
+      if (J >= 1) mbar_wait(&bars[B_QE], (J - 1) & 1);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bars[B_Q], 32768);
+        tma_load_3d(sQ, &a.tmap_q, &bars[B_Q], 0, qt * kTile, hh);
+        tma_load_3d(sQ + 16384, &a.tmap_q, &bars[B_Q], 64, qt * kTile, hh);
+      }
+      const int bsz = a.idx.blk_b[hh];
+      int slot_gk = 0;  // gather tiles: key block of slot `lane` (0 = placeholder, masked)
+      // ring sequence: K_0, V_0, K_1, V_1, ... (sub-tiles u = 2 j + half)
+      for (int i = 0; i < 2 * nsub; ++i) {
+        const int u = i >> 1;
+        const int g = rb + i;
+        const int slot = g % kRing;
+        const uint32_t e = tl[u >> 1];
+        const uint32_t kind = tile_kind(e);
+        if (kind == TK_GATHER && (i & 3) == 0) {
+          const int gq = qt * (kTile / bsz) + lane;
+          const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
+          int gk = 0;
+          if (lane < kTile / bsz && gq * bsz < a.n) {
+            const int k = ro[gq] + (int)tile_ktile(e);
+            if (k < ro[gq + 1]) {
+              const int x = a.idx.blk_idx[k];
+              if (x < gq) gk = x;
+            }
           }
+          slot_gk = gk;
         }
-        slot_gk = gk;
-      }
-      PT(0);
-      if (i >= kRing) mbar_wait(&bars[B_EMPTY0 + slot], ((i / kRing) - 1) & 1);
-      PT(1);
-      uint8_t* dst = sRing + slot * kSlotBytes;
-      if (kind != TK_GATHER) {
-        if (lane == 0) {
-          const int row = (int)tile_ktile(e) * kTile + (u & 1) * kSub;
-          const CUtensorMap* map = (i & 1) ? &a.tmap_v : &a.tmap_k;
-          mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
-          tma_load_3d(dst, map, &bars[B_FULL0 + slot], 0, row, hkv);
-          tma_load_3d(dst + 8192, map, &bars[B_FULL0 + slot], 64, row, hkv);
+        PT(0);
+        if (g >= kRing) mbar_wait(&bars[B_EMPTY0 + slot], ((g / kRing) - 1) & 1);
+        PT(1);
+        uint8_t* dst = sRing + slot * kSlotBytes;
+        if (kind != TK_GATHER) {
+          if (lane == 0) {
+            const int row = (int)tile_ktile(e) * kTile + (u & 1) * kSub;
+            const CUtensorMap* map = (i & 1) ? &a.tmap_v : &a.tmap_k;
+            mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
+            tma_load_3d(dst, map, &bars[B_FULL0 + slot], 0, row, hkv);
+            tma_load_3d(dst + 8192, map, &bars[B_FULL0 + slot], 64, row, hkv);
+          }
+        } else {
+          // 64 gathered keys = 8 boxes of 8 rows x 2 d-halves; lane -> (box, half)
+          const int bx = lane & 7, dh = (lane >> 3) & 1;
+          const int key = (u & 1) * kSub + bx * 8;
+          const int gk = __shfl_sync(0xffffffffu, slot_gk, key / bsz);
+          const CUtensorMap* map = (i & 1) ? &a.tmap_v8 : &a.tmap_k8;
+          if (lane == 0) mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
+          __syncwarp();
+          if (lane < 16)
+            tma_load_3d(dst + dh * 8192 + bx * 1024, map, &bars[B_FULL0 + slot], dh * 64,
+                        gk * bsz + key % bsz, hkv);
         }
-      } else {
-        // 64 gathered keys = 8 boxes of 8 rows x 2 d-halves; lane -> (box, half)
-        const int bx = lane & 7, dh = (lane >> 3) & 1;
-        const int key = (u & 1) * kSub + bx * 8;
-        const int gk = __shfl_sync(0xffffffffu, slot_gk, key / bsz);
-        const CUtensorMap* map = (i & 1) ? &a.tmap_v8 : &a.tmap_k8;
-        if (lane == 0) mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
-        __syncwarp();
-        if (lane < 16)
-          tma_load_3d(dst + dh * 8192 + bx * 1024, map, &bars[B_FULL0 + slot], dh * 64,
-                      gk * bsz + key % bsz, hkv);
+        PT(2);
+        if (kProf) pc[15] += 1;
       }
-      PT(2);
-      if (kProf) pc[15] += 1;
+      rb += 2 * nsub;
     }
     PT_FLUSH(32);
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
-    if (elect_one()) {
-      constexpr uint32_t idesc_qk = idesc_bf16_f32(128, kSub, 0, 0);
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
-      const uint32_t q_addr = smem_u32(sQ);
-      const uint32_t ring_addr = smem_u32(sRing);
-      PT_INIT
-      auto issue_qk = [&](int u) {
-        const int i = 2 * u, slot = i % kRing;
-        PT(0);
-        mbar_wait(&bars[B_FULL0 + slot], (i / kRing) & 1);
-        PT(1);
-        tc_fence_after();
-        const uint32_t k_addr = ring_addr + slot * kSlotBytes;
+    const bool leader = elect_one();
+    constexpr uint32_t idesc_qk = idesc_bf16_f32(128, kSub, 0, 0);
+    constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
+    const uint32_t q_addr = smem_u32(sQ);
+    const uint32_t ring_addr = smem_u32(sRing);
+    PT_INIT
+    int rb = 0, sb = 0, pb = 0;  // ring items, S-buffer uses (per buffer), PV commits so far
+    for (int J = 0;; ++J) {
+      mbar_wait(&bars[B_IF0 + (J & 1)], (J >> 1) & 1);
+      const int item = sItem[J & 1];
+      __syncwarp();
+      if (leader) mbar_arrive(&bars[B_IE0 + (J & 1)]);
+      if (item < 0) break;
+      const int nsub = 2 * a.tile_cnt[item];
+      if (leader) {
+        auto issue_qk = [&](int u) {
+          const int g = rb + 2 * u, slot = g % kRing;
+          PT(0);
+          mbar_wait(&bars[B_FULL0 + slot], (g / kRing) & 1);
+          PT(1);
+          tc_fence_after();
+          const uint32_t k_addr = ring_addr + slot * kSlotBytes;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_ss(tbase + kColS + (u & 1) * kSub,
-                 sdesc_sw128(q_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                 sdesc_sw128(k_addr + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_qk,
-                 kk > 0 ? 1u : 0u);
-        }
-        mma_commit(&bars[B_EMPTY0 + slot]);
-        mma_commit(&bars[B_SF0 + (u & 1)]);
-        PT(2);
-      };
-      mbar_wait(&bars[B_Q], 0);
-      tc_fence_after();
-      issue_qk(0);
-      if (nsub > 1) issue_qk(1);
-      for (int u = 0; u < nsub; ++u) {
-        PT(3);
-        mbar_wait(&bars[B_PF0 + (u & 1)], (u >> 1) & 1);
-        PT(4);
-        const int i = 2 * u + 1, slot = i % kRing;
-        mbar_wait(&bars[B_FULL0 + slot], (i / kRing) & 1);
-        PT(5);
+          for (int kk = 0; kk < 8; ++kk) {
+            mma_ss(tbase + kColS + (u & 1) * kSub,
+                   sdesc_sw128(q_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                   sdesc_sw128(k_addr + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_qk,
+                   kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&bars[B_EMPTY0 + slot]);
+          mma_commit(&bars[B_SF0 + (u & 1)]);
+          if (u == nsub - 1) mma_commit(&bars[B_QE]);  // last reader of Q
+          PT(2);
+        };
+        mbar_wait(&bars[B_Q], J & 1);
         tc_fence_after();
-        const uint32_t v_addr = ring_addr + slot * kSlotBytes;
-        const uint32_t p_addr = tbase + kColS + (u & 1) * kSub;
+        if (nsub == 0) mma_commit(&bars[B_QE]);
+        if (nsub > 0) issue_qk(0);
+        if (nsub > 1) issue_qk(1);
+        for (int u = 0; u < nsub; ++u) {
+          PT(3);
+          mbar_wait(&bars[B_PF0 + (u & 1)], (sb + (u >> 1)) & 1);
+          PT(4);
+          const int g = rb + 2 * u + 1, slot = g % kRing;
+          mbar_wait(&bars[B_FULL0 + slot], (g / kRing) & 1);
+          // PV(0) overwrites O: the previous item's epilogue must have read it
+          if (u == 0 && J >= 1) mbar_wait(&bars[B_OE], (J - 1) & 1);
+          PT(5);
+          tc_fence_after();
+          const uint32_t v_addr = ring_addr + slot * kSlotBytes;
+          const uint32_t p_addr = tbase + kColS + (u & 1) * kSub;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          mma_ts(tbase + kColO, p_addr + kk * 8, sdesc_sw128(v_addr + kk * 2048, 8192, 1024),
-                 idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk) {
+            mma_ts(tbase + kColO, p_addr + kk * 8, sdesc_sw128(v_addr + kk * 2048, 8192, 1024),
+                   idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&bars[B_EMPTY0 + slot]);
+          mma_commit(&bars[B_OD]);
+          PT(6);
+          if (kProf) pc[15] += 1;
+          if (u + 2 < nsub) issue_qk(u + 2);
         }
-        mma_commit(&bars[B_EMPTY0 + slot]);
-        mma_commit(&bars[B_OD]);
-        PT(6);
-        if (kProf) pc[15] += 1;
-        if (u + 2 < nsub) issue_qk(u + 2);
+        mma_commit(&bars[B_OF]);
       }
-      mma_commit(&bars[B_OF]);
-      PT_FLUSH(16);
+      __syncwarp();
+      rb += 2 * nsub;
+      sb += nsub / 2;
+      pb += nsub;
     }
+    (void)pb;
+    PT_FLUSH(16);
   } else {
     // ------------------------------------------------------------ softmax warps
     const int r = threadIdx.x;  // 0..127
-    const int i = qt * kTile + r;
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     const float sl2 = a.scale_log2;
-    float m_used = -INFINITY;
-    float l = 0.f;
-    uint32_t msk[4] = {0u, 0u, 0u, 0u};
-    uint32_t kind = TK_FULL;
-    const RowConst rc = row_const(a, hh, i);
-    uint32_t raw[9];
-    uint32_t e_cur = cnt > 0 ? tl[0] : 0u;
-    uint32_t e_nxt = cnt > 1 ? tl[1] : 0u;
-    mask_fetch(a, rc, hh, i, e_cur, raw);
     PT_INIT
     if (kProf) { pc[10] += pt_last - t_entry; pc[12] += 1; }
-    for (int u = 0; u < nsub; ++u) {
-      const int half = u & 1;
-      PT(0);
-      if (half == 0) {
-        const int t = u >> 1;
-        kind = tile_kind(e_cur);
-#ifdef SA_NO_PREFETCH
-        mask_fetch(a, rc, hh, i, e_cur, raw);
-        if (kind != TK_FULL) mask_make(a, rc, i, qt, e_cur, raw, msk);
-#else
-        if (kind != TK_FULL) mask_make(a, rc, i, qt, e_cur, raw, msk);
-        // next tile's entry and mask words are loaded now, used one tile later
-        if (t + 1 < cnt) mask_fetch(a, rc, hh, i, e_nxt, raw);
-#endif
-        e_cur = e_nxt;
-        e_nxt = (t + 2 < cnt) ? tl[t + 2] : 0u;
-      }
-      PT(1);
-      mbar_wait(&bars[B_SF0 + half], (u >> 1) & 1);
-      PT(2);
-      tc_fence_after();
-      uint32_t s[2][32];
-      const uint32_t s_col = tbase + lane_off + kColS + half * kSub;
-      tmem_ld32(s_col, s[0]);
-      tmem_ld32(s_col + 32, s[1]);
-      tmem_ld_wait();
-      PT(3);
-      if (kind != TK_FULL) {
-        const uint32_t m0 = half ? msk[2] : msk[0], m1 = half ? msk[3] : msk[1];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          if (!((m0 >> t) & 1u)) s[0][t] = __float_as_uint(-INFINITY);
-          if (!((m1 >> t) & 1u)) s[1][t] = __float_as_uint(-INFINITY);
+    int sb = 0, pb = 0;
+    for (int J = 0;; ++J) {
+      mbar_wait(&bars[B_IF0 + (J & 1)], (J >> 1) & 1);
+      const int item = sItem[J & 1];
+      mbar_arrive(&bars[B_IE0 + (J & 1)]);
+      if (item < 0) break;
+      const int hh = item / a.nqt, qt = item % a.nqt;
+      const int bidx = hh / a.heads, h = hh % a.heads;
+      const int cnt = a.tile_cnt[item];
+      const int nsub = 2 * cnt;
+      const uint32_t* tl = a.tiles + a.tile_off[item];
+      const int i = qt * kTile + r;
+      float m_used = -INFINITY;
+      float l = 0.f;
+      uint32_t msk[4] = {0u, 0u, 0u, 0u};
+      uint32_t kind = TK_FULL;
+      const RowConst rc = row_const(a, hh, i);
+      uint32_t raw[9];
+      uint32_t e_cur = cnt > 0 ? tl[0] : 0u;
+      uint32_t e_nxt = cnt > 1 ? tl[1] : 0u;
+      mask_fetch(a, rc, hh, i, e_cur, raw);
+      for (int u = 0; u < nsub; ++u) {
+        const int half = u & 1;
+        PT(0);
+        if (half == 0) {
+          const int t = u >> 1;
+          kind = tile_kind(e_cur);
+          if (kind != TK_FULL) mask_make(a, rc, i, qt, e_cur, raw, msk);
+          // next tile's entry and mask words are loaded now, used one tile later
+          if (t + 1 < cnt) mask_fetch(a, rc, hh, i, e_nxt, raw);
+          e_cur = e_nxt;
+          e_nxt = (t + 2 < cnt) ? tl[t + 2] : 0u;
         }
-      }
-      // row max: four independent FMNMX3 chains
-      float mx;
-      {
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        PT(1);
+        mbar_wait(&bars[B_SF0 + half], (sb + (u >> 1)) & 1);
+        PT(2);
+        tc_fence_after();
+        uint32_t s[2][32];
+        const uint32_t s_col = tbase + lane_off + kColS + half * kSub;
+        tmem_ld32(s_col, s[0]);
+        tmem_ld32(s_col + 32, s[1]);
+        tmem_ld_wait();
+        PT(3);
+        if (kind != TK_FULL) {
+          const uint32_t m0 = half ? msk[2] : msk[0], m1 = half ? msk[3] : msk[1];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            if (!((m0 >> t) & 1u)) s[0][t] = __float_as_uint(-INFINITY);
+            if (!((m1 >> t) & 1u)) s[1][t] = __float_as_uint(-INFINITY);
+          }
+        }
+        // row max: four independent FMNMX3 chains
+        float mx;
+        {
+          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int t = 0; t < 32; t += 4) {
+              m4[2 * c] = fmax3(m4[2 * c], __uint_as_float(s[c][t]), __uint_as_float(s[c][t + 1]));
+              m4[2 * c + 1] = fmax3(m4[2 * c + 1], __uint_as_float(s[c][t + 2]), __uint_as_float(s[c][t + 3]));
+            }
+          mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+        }
+        PT(4);
+        const float mt = mx * sl2;
+        // Lazy rescale: keep a stale max until the row max grows by > 2^8.  The
+        // decision is per row but the TMEM round trip of O is warp-wide
+        // (tcgen05.ld/st are .sync.aligned), so rows that need none use 1.
+        const bool need = mt > m_used + 8.0f;
+        if (__any_sync(0xffffffffu, need)) {
+          const float alpha = need ? fast_exp2(m_used - mt) : 1.0f;  // 0 when m_used == -inf
+          l *= alpha;
+          if (u > 0) {
+            // PV(u-1) may still be accumulating into O (PV(u-2) completed before S_u)
+            mbar_wait(&bars[B_OD], (pb + u - 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o[32];
+              tmem_ld32(tbase + lane_off + kColO + 32 * c, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int t = 0; t < 32; t += 2) {
+                const float2 v = fmul2(make_float2(__uint_as_float(o[t]), __uint_as_float(o[t + 1])),
+                                       make_float2(alpha, alpha));
+                o[t] = __float_as_uint(v.x);
+                o[t + 1] = __float_as_uint(v.y);
+              }
+              tmem_st32(tbase + lane_off + kColO + 32 * c, o);
+            }
+            tmem_st_wait();
+          }
+          if (need) m_used = mt;
+        }
+        PT(5);
+        const float moff = (m_used == -INFINITY) ? 0.f : m_used;
+        // p = exp2(s * scale_log2 - m): FFMA2 + two MUFU.EX2; row sum in four FADD2 chains
+        const float2 sc2 = make_float2(sl2, sl2);
+        const float2 mo2 = make_float2(-moff, -moff);
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
+        uint32_t p[32];
 #pragma unroll
         for (int c = 0; c < 2; ++c)
 #pragma unroll
-          for (int t = 0; t < 32; t += 4) {
-            m4[2 * c] = fmax3(m4[2 * c], __uint_as_float(s[c][t]), __uint_as_float(s[c][t + 1]));
-            m4[2 * c + 1] = fmax3(m4[2 * c + 1], __uint_as_float(s[c][t + 2]), __uint_as_float(s[c][t + 3]));
-          }
-        mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
-      }
-      PT(4);
-      const float mt = mx * sl2;
-      // Lazy rescale: keep a stale max until the row max grows by > 2^8.  The
-      // decision is per row but the TMEM round trip of O is warp-wide
-      // (tcgen05.ld/st are .sync.aligned), so rows that need none use 1.
-      const bool need = mt > m_used + 8.0f;
-      if (__any_sync(0xffffffffu, need)) {
-        const float alpha = need ? fast_exp2(m_used - mt) : 1.0f;  // 0 when m_used == -inf
-        l *= alpha;
-        if (u > 0) {
-          // PV(u-1) may still be accumulating into O (PV(u-2) completed before S_u)
-          mbar_wait(&bars[B_OD], (u - 1) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tbase + lane_off + kColO + 32 * c, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int t = 0; t < 32; t += 2) {
-              const float2 v = fmul2(make_float2(__uint_as_float(o[t]), __uint_as_float(o[t + 1])),
-                                     make_float2(alpha, alpha));
-              o[t] = __float_as_uint(v.x);
-              o[t + 1] = __float_as_uint(v.y);
+          for (int t = 0; t < 32; t += 2) {
+            float2 x = ffma2(make_float2(__uint_as_float(s[c][t]), __uint_as_float(s[c][t + 1])), sc2, mo2);
+            if (POLY > 0 && ((t >> 1) % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY : 1) - 1) {
+              x = exp2_poly2(x);
+            } else {
+              x.x = fast_exp2(x.x);
+              x.y = fast_exp2(x.y);
             }
-            tmem_st32(tbase + lane_off + kColO + 32 * c, o);
+            acc[(t >> 1) & 3] = fadd2(acc[(t >> 1) & 3], x);
+            p[c * 16 + (t >> 1)] = pack_bf16(x.x, x.y);
           }
-          tmem_st_wait();
+        {
+          const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+          const float2 t2 = fadd2(a01, a23);
+          l += t2.x + t2.y;
         }
-        if (need) m_used = mt;
+        PT(6);
+        tmem_st32(s_col, p);  // P (bf16 pairs) over the first 32 columns of this S buffer
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars[B_PF0 + half]);
+        PT(7);
+        if (kProf) pc[15] += 1;
       }
-      PT(5);
-      const float moff = (m_used == -INFINITY) ? 0.f : m_used;
-      // p = exp2(s * scale_log2 - m): FFMA2 + two MUFU.EX2; row sum in four FADD2 chains
-      const float2 sc2 = make_float2(sl2, sl2);
-      const float2 mo2 = make_float2(-moff, -moff);
-      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                       make_float2(0.f, 0.f)};
-      uint32_t p[32];
+      // ---------------------------------------------------------- epilogue
+      mbar_wait(&bars[B_OF], J & 1);
+      PT(8);
+      tc_fence_after();
+      uint32_t o[4][32];
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int t = 0; t < 32; t += 2) {
-          float2 x = ffma2(make_float2(__uint_as_float(s[c][t]), __uint_as_float(s[c][t + 1])), sc2, mo2);
-          if (POLY > 0 && ((t >> 1) % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY : 1) - 1) {
-            x = exp2_poly2(x);
-          } else {
-            x.x = fast_exp2(x.x);
-            x.y = fast_exp2(x.y);
-          }
-          acc[(t >> 1) & 3] = fadd2(acc[(t >> 1) & 3], x);
-          p[c * 16 + (t >> 1)] = pack_bf16(x.x, x.y);
-        }
-      {
-        const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
-        const float2 t2 = fadd2(a01, a23);
-        l += t2.x + t2.y;
-      }
-      PT(6);
-      tmem_st32(s_col, p);  // P (bf16 pairs) over the first 32 columns of this S buffer
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(&bars[B_PF0 + half]);
-      PT(7);
-      if (kProf) pc[15] += 1;
-    }
-    // ------------------------------------------------------------ epilogue
-    mbar_wait(&bars[B_OF], 0);
-    PT(8);
-    tc_fence_after();
-    const float inv = 1.0f / l;
-    const bool valid = i < a.n && cnt > 0;  // cnt == 0: query tile not requested
-    __nv_bfloat16* orow = a.out + (long long)bidx * a.out_batch_stride +
-                          (long long)i * a.out_row_stride + (long long)h * kHeadDim;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      tmem_ld32(tbase + lane_off + kColO + 32 * c, o);
+      for (int c = 0; c < 4; ++c) tmem_ld32(tbase + lane_off + kColO + 32 * c, o[c]);
       tmem_ld_wait();
-      uint32_t pk[16];
-#pragma unroll
-      for (int t = 0; t < 16; ++t)
-        pk[t] = pack_bf16(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
+      tc_fence_before();
+      mbar_arrive(&bars[B_OE]);  // O may now be overwritten by the next item's PV(0)
+      const float inv = 1.0f / l;
+      const bool valid = i < a.n && cnt > 0;  // cnt == 0: query tile not requested
+      __nv_bfloat16* orow = a.out + (long long)bidx * a.out_batch_stride +
+                            (long long)i * a.out_row_stride + (long long)h * kHeadDim;
       if (valid) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            pk[t] = pack_bf16(__uint_as_float(o[c][2 * t]) * inv, __uint_as_float(o[c][2 * t + 1]) * inv);
+          uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+        }
+        if (a.lse != nullptr) a.lse[(size_t)hh * a.n + i] = (m_used + log2f(l)) * 0.69314718055994531f;
       }
+      PT(9);
+      sb += nsub / 2;
+      pb += nsub;
     }
-    if (valid && a.lse != nullptr) {
-      a.lse[(size_t)hh * a.n + i] = (m_used + log2f(l)) * 0.69314718055994531f;
-    }
-    PT(9);
     if (kProf) pc[11] += clock64() - t_entry;
     PT_FLUSH(0);
   }
@@ -559,7 +622,7 @@ namespace sa {
 int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const void* q, const void* k,
                 const void* v, void* out, const sa_head_index* index, const int32_t* tile_off,
                 const int32_t* tile_cnt, const uint32_t* tiles, const int32_t* work, float* lse,
-                cudaStream_t cs, long long out_ld) {
+                cudaStream_t cs, long long out_ld, int* counter) {
   if (batch < 1 || heads < 1 || kv_heads < 1 || n < 1)
     return fail(SA_ERR_DIMENSION, "need batch, heads, kv_heads, n >= 1");
   if (heads % kv_heads != 0)
@@ -589,6 +652,8 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   a.tile_cnt = tile_cnt;
   a.tiles = tiles;
   a.work = work;
+  a.counter = counter;
+  if (counter) cudaMemsetAsync(counter, 0, sizeof(int), cs);
   a.idx = *index;
   a.lse = lse;
   a.prof = reinterpret_cast<unsigned long long*>(sa_attn_dbg_ptr);
@@ -607,7 +672,14 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
     cudaFuncSetAttribute(attn_fwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     attr_set = true;
   }
-  const int grid = a.hh_total * a.nqt;
+  // persistent: two CTAs per SM (113 KB shared memory and 256 TMEM columns each)
+  static const int num_sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  const int grid = (int)std::min<long long>(2LL * num_sms, (long long)a.hh_total * a.nqt);
   // the need_weights path derives weights from lse: keep exact MUFU exps there
   switch (lse != nullptr ? 0 : poly) {
     case 2: attn_fwd_kernel<2><<<grid, kThreads, kSmemBytes, cs>>>(a); break;

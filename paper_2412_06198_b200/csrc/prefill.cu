@@ -165,7 +165,7 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
   sz[W_TOFF] = hh * p->nqt * 4;
   sz[W_TCNT] = hh * p->nqt * 4;
   sz[W_TILES] = hh * (size_t)p->nqt * (p->nqt + 1) / 2 * 4;
-  sz[W_WORK] = hh * p->nqt * 4;
+  sz[W_WORK] = hh * p->nqt * 4 + 16;  // + the persistent kernel's work counter
   size_t o = 0;
   for (int i = 0; i < W_NUM; ++i) {
     L->off[i] = o;
@@ -361,12 +361,13 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
     return !(e && e[0] == '0');
   }();
   int32_t* work = nullptr;
+  int* counter = reinterpret_cast<int*>(b + L.off[W_WORK]);
   if (lpt) {
-    work = reinterpret_cast<int32_t*>(b + L.off[W_WORK]);
+    work = counter + 4;
     if ((rc = sa_order_work(V.tile_cnt, p.hh * p.nqt, p.nqt, work, stream))) return rc;
   }
   rc = launch_attn(B, H, HK, n, desc->scale, q, k, v, out, &V.index, V.tile_off, V.tile_cnt, V.tiles,
-                   work, nullptr, st, desc->out_ld);
+                   work, nullptr, st, desc->out_ld, counter);
   mark(4);
   return rc;
 }
