@@ -72,48 +72,63 @@ def measured_peaks():
     return 1628.9, 1400.1, 6531.6, "measured (SURVEY.md §6 record of MEASURED_PEAKS.json)"
 
 
-class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+_SAMPLER = r"""
+import sys, time
+import pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+while True:
+    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    print(sm, mx, rs, flush=True)
+    time.sleep(0.002)
+"""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+class ClockSampler:
+    """SM clocks and throttle reasons sampled every ~2 ms by a separate NVML
+    process (not a thread: the launching thread holds the GIL) during the
+    timed region."""
 
     def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        self.idx = int(vis.split(",")[gpu_index]) if vis else gpu_index
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                parts = [x.strip() for x in out.stdout.strip().split(",")]
-                if len(parts) >= 6:
-                    self.samples.append(parts)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self._p = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.idx)], stdout=subprocess.PIPE,
+                                       stderr=subprocess.DEVNULL, text=True)
+            self._p.stdout.readline()  # sampler is up (one sample taken) before the region starts
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        self._p.terminate()
+        out, _ = self._p.communicate(timeout=10)
+        for line in out.splitlines():
+            try:
+                sm, mx, rs = line.split()
+                self.samples.append((float(sm), float(mx), int(rs)))
+            except ValueError:
+                pass
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        # NVML clocks-event reason bits (nvml.h): sw_power_cap 0x4, hw_slowdown 0x8,
+        # sw_thermal 0x20, hw_thermal 0x40, hw_power_brake 0x80
+        bits = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+        reasons = sorted({name for _, _, r in self.samples for b, name in bits.items() if r & b})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml, 2 ms"}
 
 
 # ----------------------------------------------------------------------------- CPU reference arm
@@ -228,6 +243,24 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- GPU arm
 
+def count_step_kernels(step):
+    """Kernel launches of one step, from a CUPTI trace (torch.profiler)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize()
+    names = {}
+    for ev in prof.events():
+        if ev.device_type is not None and "cuda" in str(ev.device_type).lower() and "memset" not in ev.name.lower() \
+                and "memcpy" not in ev.name.lower():
+            key = ev.name.split("(")[0].split("<")[0].replace("void ", "").replace("sa::", "")
+            names[key] = names.get(key, 0) + 1
+    return sum(names.values()), names
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -338,9 +371,8 @@ def run_ours(args):
     if world > 1:
         t = torch.tensor([exec_flops, attn_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    launches_per_step = 2 + (5 if "VerticalSlash" in fams else 0) + (4 if "BlockSparse" in fams else 0) + 2
-    if plan.mode != "auto":
-        launches_per_step -= 1
+    # kernels per step, counted by CUPTI (torch.profiler) on one extra untimed step
+    launches_per_step, kernel_names = count_step_kernels(step)
 
     e2e = None
     if not args.no_e2e:
@@ -405,6 +437,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps),
+            "kernels_per_step": kernel_names,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
