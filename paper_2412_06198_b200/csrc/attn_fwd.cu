@@ -437,26 +437,38 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     PT_INIT
     if (kProf) { pc[10] += pt_last - t_entry; pc[12] += 1; }
     int sb = 0, pb = 0;
-    for (int J = 0;; ++J) {
+    // The next item's descriptor, row constants and first tile entries are
+    // loaded before the current item's epilogue, hiding their latency.
+    int item, cnt;
+    const uint32_t* tl;
+    RowConst rc;
+    uint32_t raw[9];
+    uint32_t e_cur, e_nxt;
+    auto fetch_item = [&](int J) {
       mbar_wait(&bars[B_IF0 + (J & 1)], (J >> 1) & 1);
-      const int item = sItem[J & 1];
+      item = sItem[J & 1];
       mbar_arrive(&bars[B_IE0 + (J & 1)]);
+      if (item < 0) return;
+      cnt = a.tile_cnt[item];
+      tl = a.tiles + a.tile_off[item];
+      const int hh_ = item / a.nqt, i_ = (item % a.nqt) * kTile + r;
+      rc = row_const(a, hh_, i_);
+      e_cur = cnt > 0 ? tl[0] : 0u;
+      e_nxt = cnt > 1 ? tl[1] : 0u;
+      mask_fetch(a, rc, hh_, i_, e_cur, raw);
+    };
+    fetch_item(0);
+    for (int J = 0;; ++J) {
       if (item < 0) break;
       const int hh = item / a.nqt, qt = item % a.nqt;
       const int bidx = hh / a.heads, h = hh % a.heads;
-      const int cnt = a.tile_cnt[item];
       const int nsub = 2 * cnt;
-      const uint32_t* tl = a.tiles + a.tile_off[item];
       const int i = qt * kTile + r;
+      const int cur_cnt = cnt;
       float m_used = -INFINITY;
       float l = 0.f;
       uint32_t msk[4] = {0u, 0u, 0u, 0u};
       uint32_t kind = TK_FULL;
-      const RowConst rc = row_const(a, hh, i);
-      uint32_t raw[9];
-      uint32_t e_cur = cnt > 0 ? tl[0] : 0u;
-      uint32_t e_nxt = cnt > 1 ? tl[1] : 0u;
-      mask_fetch(a, rc, hh, i, e_cur, raw);
       for (int u = 0; u < nsub; ++u) {
         const int half = u & 1;
         PT(0);
@@ -567,32 +579,34 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         if (kProf) pc[15] += 1;
       }
       // ---------------------------------------------------------- epilogue
+      fetch_item(J + 1);  // next item's loads in flight during this epilogue
       mbar_wait(&bars[B_OF], J & 1);
       PT(8);
       tc_fence_after();
-      uint32_t o[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tbase + lane_off + kColO + 32 * c, o[c]);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&bars[B_OE]);  // O may now be overwritten by the next item's PV(0)
       const float inv = 1.0f / l;
-      const bool valid = i < a.n && cnt > 0;  // cnt == 0: query tile not requested
+      const bool valid = i < a.n && cur_cnt > 0;  // cnt == 0: query tile not requested
       __nv_bfloat16* orow = a.out + (long long)bidx * a.out_batch_stride +
                             (long long)i * a.out_row_stride + (long long)h * kHeadDim;
-      if (valid) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tbase + lane_off + kColO + 32 * c, o);
+        tmem_ld_wait();
+        if (c == 3) {
+          tc_fence_before();
+          mbar_arrive(&bars[B_OE]);  // O may now be overwritten by the next item's PV(0)
+        }
+        if (valid) {
           uint32_t pk[16];
 #pragma unroll
           for (int t = 0; t < 16; ++t)
-            pk[t] = pack_bf16(__uint_as_float(o[c][2 * t]) * inv, __uint_as_float(o[c][2 * t + 1]) * inv);
+            pk[t] = pack_bf16(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
           uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
 #pragma unroll
           for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
         }
-        if (a.lse != nullptr) a.lse[(size_t)hh * a.n + i] = (m_used + log2f(l)) * 0.69314718055994531f;
       }
+      if (valid && a.lse != nullptr) a.lse[(size_t)hh * a.n + i] = (m_used + log2f(l)) * 0.69314718055994531f;
       PT(9);
       sb += nsub / 2;
       pb += nsub;
