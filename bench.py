@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--ctx", type=int, default=32768)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--mode", default="auto", help="auto | dense | triangular | vertical-slash | block-sparse")
+    ap.add_argument("--pattern", default=None,
+                    help="fixed pattern for every head, e.g. block:8:1, vs:1536:1536, tri:3072:0 (overrides --mode)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -294,7 +296,11 @@ def run_ours(args):
 
     mode = args.mode
     fixed = None
-    if mode != "auto" and mode != "dense":
+    if args.pattern:
+        fam, p1, p2 = args.pattern.split(":")
+        fixed = {"tri": Triangular, "vs": VerticalSlash, "block": BlockSparse}[fam](int(p1), int(p2))
+        mode = "fixed"
+    elif mode != "auto" and mode != "dense":
         from oracle.sparse_oracle import fixed_pattern_for
 
         fp = fixed_pattern_for(mode, n)

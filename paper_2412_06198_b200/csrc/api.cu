@@ -70,6 +70,23 @@ int make_tmap_3d_bf16(CUtensorMap* map, const void* base, int d0, int d1, int d2
   return SA_OK;
 }
 
+// K/V viewed as [groups][n rows][2 d-halves][64] with the halves as the box's
+// outer dim: one box {64, 8, 2} = 8 rows x both halves = 2 KB, laid out in
+// shared memory as [half][8 rows][128 B] (two SWIZZLE_128B atoms).
+int make_tmap_kv_gather(CUtensorMap* map, const void* base, int n, int groups) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return fail(SA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {64, (cuuint64_t)n, 2, (cuuint64_t)groups};
+  cuuint64_t strides[3] = {256, 128, (cuuint64_t)n * 256};
+  cuuint32_t box[4] = {64, 8, 2, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SA_ERR_CUDA, "cuTensorMapEncodeTiled (gather map) failed (%d)", (int)r);
+  return SA_OK;
+}
+
 }  // namespace sa
 
 extern "C" {

@@ -17,6 +17,7 @@ int fail(int status, const char* fmt, ...);
 // Encode a 3-D bf16 tensor map over a [d2, d1, d0=128] row-major tensor,
 // box {64, box_rows, 1}, 128-byte swizzle.
 int make_tmap_3d_bf16(CUtensorMap* map, const void* base, int d0, int d1, int d2, int box_rows);
+int make_tmap_kv_gather(CUtensorMap* map, const void* base, int n, int groups);
 
 inline int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();

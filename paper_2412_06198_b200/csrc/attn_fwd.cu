@@ -40,7 +40,7 @@ struct AttnArgs {
   CUtensorMap tmap_q;  // [HH, n, 128] bf16, box {64, 128, 1}, SW128
   CUtensorMap tmap_k;  // [HK, n, 128], box {64, 64, 1}
   CUtensorMap tmap_v;  // [HK, n, 128], box {64, 64, 1}
-  CUtensorMap tmap_k8;  // same tensors, box {64, 8, 1}: one swizzle atom per gathered block row group
+  CUtensorMap tmap_k8;  // gather maps (make_tmap_kv_gather): box = 8 rows x both d-halves, 2 KB
   CUtensorMap tmap_v8;
   __nv_bfloat16* out;
   long long out_batch_stride;  // elements between batches
@@ -241,6 +241,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + B_NUM);
   volatile int* sItem = reinterpret_cast<volatile int*>(tmem_holder + 4);  // [2]
+  // per ring slot: 1 = gathered layout ([8-row block][half][8 rows][128 B]), 0 = [half][64 rows][128 B]
+  volatile int* sLay = sItem + 2;  // [kRing]
 
   const long long t_entry = kProf ? clock64() : 0;
   const int warp = warp_id();
@@ -334,21 +336,23 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
           if (lane == 0) {
             const int row = (int)tile_ktile(e) * kTile + (u & 1) * kSub;
             const CUtensorMap* map = (i & 1) ? &a.tmap_v : &a.tmap_k;
+            sLay[slot] = 0;
             mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
             tma_load_3d(dst, map, &bars[B_FULL0 + slot], 0, row, hkv);
             tma_load_3d(dst + 8192, map, &bars[B_FULL0 + slot], 64, row, hkv);
           }
         } else {
-          // 64 gathered keys = 8 boxes of 8 rows x 2 d-halves; lane -> (box, half)
-          const int bx = lane & 7, dh = (lane >> 3) & 1;
+          // 64 gathered keys = 8 boxes of 8 rows x both d-halves (2 KB each); lane -> box
+          const int bx = lane & 7;
           const int key = (u & 1) * kSub + bx * 8;
           const int gk = __shfl_sync(0xffffffffu, slot_gk, key / bsz);
           const CUtensorMap* map = (i & 1) ? &a.tmap_v8 : &a.tmap_k8;
-          if (lane == 0) mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
+          if (lane == 0) {
+            sLay[slot] = 1;
+            mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
+          }
           __syncwarp();
-          if (lane < 16)
-            tma_load_3d(dst + dh * 8192 + bx * 1024, map, &bars[B_FULL0 + slot], dh * 64,
-                        gk * bsz + key % bsz, hkv);
+          if (lane < 8) tma_load_4d(dst + bx * 2048, map, &bars[B_FULL0 + slot], 0, gk * bsz + key % bsz, 0, hkv);
         }
         PT(2);
         if (kProf) pc[15] += 1;
@@ -380,11 +384,14 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
           PT(1);
           tc_fence_after();
           const uint32_t k_addr = ring_addr + slot * kSlotBytes;
+          // gathered slots interleave the d-halves per 8-key block (half at +1 KB, blocks 2 KB apart)
+          const bool gl = sLay[slot] != 0;
+          const uint32_t k_half = gl ? 1024u : 8192u, k_sbo = gl ? 2048u : 1024u;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             mma_ss(tbase + kColS + (u & 1) * kSub,
                    sdesc_sw128(q_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                   sdesc_sw128(k_addr + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idesc_qk,
+                   sdesc_sw128(k_addr + (kk >> 2) * k_half + (kk & 3) * 32, 16, k_sbo), idesc_qk,
                    kk > 0 ? 1u : 0u);
           }
           mma_commit(&bars[B_EMPTY0 + slot]);
@@ -409,9 +416,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
           tc_fence_after();
           const uint32_t v_addr = ring_addr + slot * kSlotBytes;
           const uint32_t p_addr = tbase + kColS + (u & 1) * kSub;
+          const bool gl = sLay[slot] != 0;
+          const uint32_t v_step = gl ? 4096u : 2048u, v_lbo = gl ? 1024u : 8192u, v_sbo = gl ? 2048u : 1024u;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            mma_ts(tbase + kColO, p_addr + kk * 8, sdesc_sw128(v_addr + kk * 2048, 8192, 1024),
+            mma_ts(tbase + kColO, p_addr + kk * 8, sdesc_sw128(v_addr + kk * v_step, v_lbo, v_sbo),
                    idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&bars[B_EMPTY0 + slot]);
@@ -651,8 +660,8 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   if ((st = make_tmap_3d_bf16(&a.tmap_q, q, kHeadDim, n, batch * heads, kTile))) return st;
   if ((st = make_tmap_3d_bf16(&a.tmap_k, k, kHeadDim, n, batch * kv_heads, kSub))) return st;
   if ((st = make_tmap_3d_bf16(&a.tmap_v, v, kHeadDim, n, batch * kv_heads, kSub))) return st;
-  if ((st = make_tmap_3d_bf16(&a.tmap_k8, k, kHeadDim, n, batch * kv_heads, 8))) return st;
-  if ((st = make_tmap_3d_bf16(&a.tmap_v8, v, kHeadDim, n, batch * kv_heads, 8))) return st;
+  if ((st = make_tmap_kv_gather(&a.tmap_k8, k, n, batch * kv_heads))) return st;
+  if ((st = make_tmap_kv_gather(&a.tmap_v8, v, n, batch * kv_heads))) return st;
   a.out = reinterpret_cast<__nv_bfloat16*>(out);
   a.out_row_stride = out_ld > 0 ? out_ld : (long long)heads * kHeadDim;
   a.out_batch_stride = (long long)n * a.out_row_stride;

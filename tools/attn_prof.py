@@ -22,12 +22,21 @@ from paper_2412_06198_b200 import _lib, runtime as R  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--ctx", type=int, default=32768)
 ap.add_argument("--mode", default="auto")
+ap.add_argument("--pattern", default=None, help="fixed pattern for all heads, e.g. block:8:1")
 args = ap.parse_args()
 n = args.ctx
 q, k, v = bench.synth_inputs(0, n)
 dev = torch.device("cuda")
 qd, kd, vd = (torch.from_numpy(np.ascontiguousarray(x)).bfloat16().to(dev) for x in (q, k, v))
-plan = R.PrefillPlan(1, bench.H, bench.HK, n, bench.D, args.mode)
+fixed = None
+mode = args.mode
+if args.pattern:
+    from paper_2412_06198_b200.patterns import BlockSparse, Triangular, VerticalSlash
+
+    fam, p1, p2 = args.pattern.split(":")
+    fixed = {"tri": Triangular, "vs": VerticalSlash, "block": BlockSparse}[fam](int(p1), int(p2))
+    mode = "fixed"
+plan = R.PrefillPlan(1, bench.H, bench.HK, n, bench.D, mode, fixed_pattern=fixed)
 ws = R._workspace(plan.ws_bytes, dev)
 out = torch.empty((1, n, bench.H * bench.D), dtype=torch.bfloat16, device=dev)
 lib = _lib.load()
