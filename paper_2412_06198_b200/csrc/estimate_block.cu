@@ -128,8 +128,9 @@ enum BBar { BB_A = 0, BB_KF0, BB_KF1, BB_KF2, BB_KF3, BB_KE0, BB_KE1, BB_KE2, BB
 template <int K, bool FUSED>
 __global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid_constant__ BlockScoreArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-aligned offset into the dynamic shared array (pointer arithmetic on
+  // smem_raw keeps the shared address space, so accesses compile to LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int hh = a.hh_base + blockIdx.y;
   if (a.gate && a.gate[hh] != a.gate_val) return;
   const int qt = a.nqt - 1 - blockIdx.x;  // heavy tiles first

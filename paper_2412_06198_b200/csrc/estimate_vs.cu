@@ -33,7 +33,7 @@
 namespace sa {
 
 struct TailArgs {
-  CUtensorMap tmap_q;  // [HH, n, 128]
+  CUtensorMap tmap_q;  // [HH, n, 128], box rows 128 (single) or 64 (paired)
   CUtensorMap tmap_k;  // [HK, n, 128]
   int n, heads, kv_heads, hh_total;
   int r_lo, r_hi;      // scored rows (global indices), r_hi - r_lo <= 128
@@ -49,34 +49,50 @@ struct TailArgs {
   int accumulate;      // add into col_out (multi-group exact scoring)
   const int32_t* head_list;   // optional: the scored heads (ascending), else all heads
   const int32_t* head_count;  // device count of head_list
+  // work units: paired (R <= 64): two heads sharing a kv head stack their 64
+  // tail rows in one M=128 MMA box (rows 0-63 head A, 64-127 head B, B may be
+  // -1); single: one head, rows in the last R lanes of the 128-row box
+  int paired;
+  const int2* units;          // optional unit list (device), else unit u = head u
+  const int32_t* unit_count;  // device count of units
 };
 
 constexpr int kTailThreads = 192;
 constexpr int kWStride = 129;  // padded row stride of the W transpose buffer
 constexpr int kTailSmemQ = 0;
-constexpr int kTailSmemK = 32768;       // two 32 KB K slots
-constexpr int kTailSmemW = 98304;       // 128 x 129 floats
+constexpr int kTailKSlots = 4;          // 32 KB K tiles in flight (HBM latency in pass 2)
+constexpr int kTailSmemK = 32768;
+constexpr int kTailSmemW = kTailSmemK + kTailKSlots * 32768;  // 128 x 129 floats
 constexpr int kTailSmemBar = kTailSmemW + 128 * kWStride * 4;
 constexpr int kTailSmemBytes = kTailSmemBar + 256 + 1024;
 
-enum TBar { T_Q = 0, T_QE, T_KF0, T_KF1, T_KE0, T_KE1, T_SF0, T_SF1, T_SE0, T_SE1, T_NUM };
+enum TBar { T_Q = 0, T_QE, T_KF0, T_KE0 = T_KF0 + kTailKSlots, T_SF0 = T_KE0 + kTailKSlots, T_SF1,
+            T_SE0, T_SE1, T_NUM };
 
 __device__ __forceinline__ int tail_count(const TailArgs& a) {
   return a.head_count ? *a.head_count : a.hh_total;
+}
+__device__ __forceinline__ int unit_count(const TailArgs& a) {
+  return a.unit_count ? *a.unit_count : a.hh_total;
+}
+__device__ __forceinline__ int2 unit_at(const TailArgs& a, int u) {
+  return a.units ? a.units[u] : make_int2(u, -1);
 }
 __device__ __forceinline__ int tail_head(const TailArgs& a, int rank) {
   return a.head_list ? a.head_list[rank] : rank;
 }
 
-// Persistent: one CTA per SM walks the work items (scored head, chunk of
-// chunk_tiles key tiles) with a grid stride; barrier phases run on across
-// items (jg counts every key tile this CTA has processed).
+// Persistent: one CTA per SM walks the work items (unit, chunk of chunk_tiles
+// key tiles) with a grid stride; barrier phases run on across items (jg counts
+// every key tile this CTA has processed).  A paired unit reads each K tile once
+// for two heads of the same kv head and keeps all four softmax warps busy.
 template <int PASS>
 __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_constant__ TailArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  const int n_items = tail_count(a) * a.nchunks;
+  // 1024-aligned offset into the dynamic shared array (pointer arithmetic on
+  // smem_raw keeps the shared address space, so accesses compile to LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int n_items = unit_count(a) * a.nchunks;
   if ((int)blockIdx.x >= n_items) return;
 
   uint8_t* sQ = smem + kTailSmemQ;
@@ -89,9 +105,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
   if (threadIdx.x == 0) {
     mbar_init(&bars[T_Q], 1);
     mbar_init(&bars[T_QE], 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kTailKSlots; ++s) {
       mbar_init(&bars[T_KF0 + s], 1);
       mbar_init(&bars[T_KE0 + s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&bars[T_SF0 + s], 1);
       mbar_init(&bars[T_SE0 + s], 128);
     }
@@ -107,18 +125,27 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
     if (elect_one()) {
       int jg = 0, it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int hh = tail_head(a, item / a.nchunks);
+        const int2 un = unit_at(a, item / a.nchunks);
         const int chunk = item % a.nchunks;
         const int kt_lo = chunk * a.chunk_tiles;
         const int kt_hi = min(a.nkt, kt_lo + a.chunk_tiles);
+        const int hh = un.x;
         const int hkv = (hh / a.heads) * a.kv_heads + (hh % a.heads) / (a.heads / a.kv_heads);
         if (it > 0) mbar_wait(&bars[T_QE], (it - 1) & 1);  // previous item's MMAs have read Q
         mbar_arrive_expect_tx(&bars[T_Q], 32768);
-        tma_load_3d(sQ, &a.tmap_q, &bars[T_Q], 0, a.s0, hh);
-        tma_load_3d(sQ + 16384, &a.tmap_q, &bars[T_Q], 64, a.s0, hh);
+        if (a.paired) {
+          const int hb = un.y >= 0 ? un.y : un.x;  // a lone head fills the B half (rows inactive)
+          tma_load_3d(sQ, &a.tmap_q, &bars[T_Q], 0, a.r_hi - 64, hh);
+          tma_load_3d(sQ + 8192, &a.tmap_q, &bars[T_Q], 0, a.r_hi - 64, hb);
+          tma_load_3d(sQ + 16384, &a.tmap_q, &bars[T_Q], 64, a.r_hi - 64, hh);
+          tma_load_3d(sQ + 24576, &a.tmap_q, &bars[T_Q], 64, a.r_hi - 64, hb);
+        } else {
+          tma_load_3d(sQ, &a.tmap_q, &bars[T_Q], 0, a.s0, hh);
+          tma_load_3d(sQ + 16384, &a.tmap_q, &bars[T_Q], 64, a.s0, hh);
+        }
         for (int kt = kt_lo; kt < kt_hi; ++kt, ++jg) {
-          const int slot = jg & 1;
-          if (jg >= 2) mbar_wait(&bars[T_KE0 + slot], ((jg >> 1) - 1) & 1);
+          const int slot = jg % kTailKSlots;
+          if (jg >= kTailKSlots) mbar_wait(&bars[T_KE0 + slot], ((jg / kTailKSlots) - 1) & 1);
           uint8_t* dst = sK + slot * 32768;
           mbar_arrive_expect_tx(&bars[T_KF0 + slot], 32768);
           tma_load_3d(dst, &a.tmap_k, &bars[T_KF0 + slot], 0, kt * kTile, hkv);
@@ -138,38 +165,43 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
         mbar_wait(&bars[T_Q], it & 1);
         tc_fence_after();
         for (int kt = kt_lo; kt < kt_hi; ++kt, ++jg) {
-          const int slot = jg & 1;
-          mbar_wait(&bars[T_KF0 + slot], (jg >> 1) & 1);
-          if (jg >= 2) mbar_wait(&bars[T_SE0 + slot], ((jg >> 1) - 1) & 1);
+          const int slot = jg % kTailKSlots, sbuf = jg & 1;
+          mbar_wait(&bars[T_KF0 + slot], (jg / kTailKSlots) & 1);
+          if (jg >= 2) mbar_wait(&bars[T_SE0 + sbuf], ((jg >> 1) - 1) & 1);
           tc_fence_after();
           const uint32_t k_addr = smem_u32(sK + slot * 32768);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            mma_ss(tbase + slot * 128, sdesc_sw128(q_addr + off, 16, 1024),
+            mma_ss(tbase + sbuf * 128, sdesc_sw128(q_addr + off, 16, 1024),
                    sdesc_sw128(k_addr + off, 16, 1024), idesc, kk > 0 ? 1u : 0u);
           }
           mma_commit(&bars[T_KE0 + slot]);
-          mma_commit(&bars[T_SF0 + slot]);
+          mma_commit(&bars[T_SF0 + sbuf]);
         }
         mma_commit(&bars[T_QE]);
       }
     }
   } else {
-    const int t = threadIdx.x;  // lane / Q-box row
-    const int i = a.s0 + t;     // global query row
-    const bool active = (i >= a.r_lo) && (i < a.r_hi);
+    const int t = threadIdx.x;  // TMEM lane = row of the MMA box
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     const float sl2 = a.scale_log2;
-    const int t_lo = a.r_lo - a.s0, t_hi = a.r_hi - a.s0;
+    // rows of this thread: paired -> head half t >> 6, row r_hi - 64 + (t & 63),
+    // stats lane 64 + (t & 63); single -> row s0 + t, stats lane t
+    const int i = a.paired ? a.r_hi - 64 + (t & 63) : a.s0 + t;
+    const int slane = a.paired ? 64 + (t & 63) : t;
+    const int R = a.r_hi - a.r_lo;
+    // W rows [w_lo, w_hi) hold this half's scored rows
     int jg = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int hh = tail_head(a, item / a.nchunks);
+      const int2 un = unit_at(a, item / a.nchunks);
+      const int hh = (a.paired && t >= 64) ? un.y : un.x;
+      const bool active = hh >= 0 && i >= a.r_lo && i < a.r_hi;
       const int chunk = item % a.nchunks;
       const int kt_lo = chunk * a.chunk_tiles;
       const int kt_hi = min(a.nkt, kt_lo + a.chunk_tiles);
       float m = -INFINITY, ssum = 0.f, lse2 = 0.f;
-      if (PASS == 2 && active) lse2 = a.lse2[(size_t)hh * 128 + t];
+      if (PASS == 2 && active) lse2 = a.lse2[(size_t)hh * 128 + slane];
       for (int kt = kt_lo; kt < kt_hi; ++kt, ++jg) {
         const int slot = jg & 1;
         const int j0 = kt * kTile;
@@ -182,62 +214,92 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
         tc_fence_before();
         mbar_arrive(&bars[T_SE0 + slot]);
         const int lim = i - j0;  // keep columns c <= lim
-        if (PASS == 1) {
-          if (active) {
-            float mx = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-#pragma unroll
-              for (int u = 0; u < 32; ++u)
-                if (32 * c + u <= lim) mx = fmaxf(mx, __uint_as_float(s[c][u]));
-            if (mx > -INFINITY) {
-              const float mn = fmaxf(m, mx * sl2);
-              float acc = 0.f;
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-#pragma unroll
-                for (int u = 0; u < 32; ++u)
-                  if (32 * c + u <= lim) acc += fast_exp2(fmaf(__uint_as_float(s[c][u]), sl2, -mn));
-              ssum = ssum * fast_exp2(m - mn) + acc;
-              m = mn;
-            }
-          }
-        } else {
-          float* wrow = sW + t * kWStride;
+        if (active && lim < 127) {  // causal cut (the diagonal tile only)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
-            for (int u = 0; u < 32; ++u) {
-              const int cc = 32 * c + u;
-              float w = 0.f;
-              if (active && cc <= lim) w = fast_exp2(fmaf(__uint_as_float(s[c][u]), sl2, -lse2));
-              wrow[cc] = w;
+            for (int u = 0; u < 32; ++u)
+              if (32 * c + u > lim) s[c][u] = __float_as_uint(-INFINITY);
+        }
+        if (PASS == 1) {
+          if (active) {
+            float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int u = 0; u < 32; u += 2) m4[c] = fmax3(m4[c], __uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1]));
+            const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+            if (mx == -INFINITY) continue;  // no causal key of this row in the tile
+            const float mn = fmaxf(m, mx * sl2);
+            const float2 sc2 = make_float2(sl2, sl2), mo2 = make_float2(-mn, -mn);
+            float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int u = 0; u < 32; u += 2) {
+                // (MUFU only: the scores feed a bit-exact top-k, keep them at ex2.approx accuracy)
+                float2 x = ffma2(make_float2(__uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1])), sc2, mo2);
+                x.x = fast_exp2(x.x);
+                x.y = fast_exp2(x.y);
+                acc[(u >> 1) & 1] = fadd2(acc[(u >> 1) & 1], x);
+              }
+            ssum = ssum * fast_exp2(m - mn) + (acc[0].x + acc[0].y + acc[1].x + acc[1].y);
+            m = mn;
+          }
+        } else {
+          float* wrow = sW + t * kWStride;
+          const float2 sc2 = make_float2(sl2, sl2), mo2 = make_float2(-lse2, -lse2);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int u = 0; u < 32; u += 2) {
+              float2 x = ffma2(make_float2(__uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1])), sc2, mo2);
+              x.x = fast_exp2(x.x);
+              x.y = fast_exp2(x.y);
+              wrow[32 * c + u] = active ? x.x : 0.f;
+              wrow[32 * c + u + 1] = active ? x.y : 0.f;
             }
           named_bar_sync(1, 128);
-          // column sums: thread t owns column j0 + t
-          {
-            float acc = 0.f;
-            for (int r = t_lo; r < t_hi; ++r) acc += sW[r * kWStride + t];
-            float* dst = a.col_out + (size_t)hh * a.n + j0 + t;
-            if (j0 + t < a.n) *dst = a.accumulate ? (*dst + acc) : acc;
-          }
-          // diagonal partials: local offset op in [0, 256): c = (r - t_lo) + 127 - op
-          float* dp = a.dpart + ((size_t)hh * a.nkt + kt) * 256;
+          // per head half: column sums (thread t owns column j0 + t) and the
+          // diagonal partials, local offset op in [0, 256): c = (r - w_lo) + 127 - op
+#pragma unroll 1
+          for (int hf = 0; hf < (a.paired ? 2 : 1); ++hf) {
+            const int hx = hf ? un.y : un.x;
+            if (hx < 0) continue;
+            const int w_hi = a.paired ? 64 * hf + 64 : a.r_hi - a.s0;
+            const int w_lo = w_hi - R;
+            // independent partial sums (the loads of one sum are not serialised)
+            float c4[4] = {0.f, 0.f, 0.f, 0.f};
+            int r = w_lo;
+            for (; r + 4 <= w_hi; r += 4) {
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            const int op = t + 128 * half;
-            float acc = 0.f;
-            for (int r = t_lo; r < t_hi; ++r) {
-              const int c = (r - t_lo) + 127 - op;
-              if (c >= 0 && c < 128) acc += sW[r * kWStride + c];
+              for (int q = 0; q < 4; ++q) c4[q] += sW[(r + q) * kWStride + t];
             }
-            dp[op] = acc;
+            for (; r < w_hi; ++r) c4[0] += sW[r * kWStride + t];
+            const float acc = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+            float* dst = a.col_out + (size_t)hx * a.n + j0 + t;
+            if (j0 + t < a.n) *dst = a.accumulate ? (*dst + acc) : acc;
+            float* dp = a.dpart + ((size_t)hx * a.nkt + kt) * 256;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              const int op = t + 128 * half;
+              // rows r' = r - w_lo with column c = r' + 127 - op inside [0, 128)
+              const int r_a = w_lo + max(0, op - 127), r_b = w_lo + min(R, op + 1);
+              float d4[4] = {0.f, 0.f, 0.f, 0.f};
+              int rr = r_a;
+              for (; rr + 4 <= r_b; rr += 4) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) d4[q] += sW[(rr + q) * kWStride + (rr + q - w_lo) + 127 - op];
+              }
+              for (; rr < r_b; ++rr) d4[0] += sW[rr * kWStride + (rr - w_lo) + 127 - op];
+              dp[op] = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+            }
           }
           named_bar_sync(1, 128);
         }
       }
-      if (PASS == 1) {
-        a.stats[((size_t)hh * a.nchunks + chunk) * 128 + t] = make_float2(m, ssum);
+      if (PASS == 1 && hh >= 0) {
+        a.stats[((size_t)hh * a.nchunks + chunk) * 128 + slane] = make_float2(m, ssum);
       }
     }
   }
@@ -300,32 +362,48 @@ __global__ void diag_combine_kernel(const float* dpart, float* diag_out, int n, 
   *dst = accumulate ? (*dst + acc) : acc;
 }
 
-// Ascending list of the heads whose gate equals gate_val (one CTA, ballot compaction).
-__global__ void gate_list_kernel(const int32_t* gate, int gate_val, int hh_total, int32_t* list,
-                                 int32_t* count) {
-  __shared__ int base;
-  if (threadIdx.x == 0) base = 0;
+// Scored heads and work units from the device-selected families (one CTA, a
+// warp per kv group): head_list = every head whose gate equals gate_val (or
+// all heads), units = consecutive pairs of those heads inside a kv group (a
+// lone head pairs with -1), or one unit per head when pairing is off.
+__global__ void build_units_kernel(const int32_t* gate, int gate_val, int hh_total, int heads,
+                                   int kv_heads, int pair, int2* units, int32_t* unit_count,
+                                   int32_t* head_list, int32_t* head_count) {
+  __shared__ int n_units, n_heads;
+  if (threadIdx.x == 0) n_units = n_heads = 0;
   __syncthreads();
-  for (int h0 = 0; h0 < hh_total; h0 += blockDim.x) {
-    const int h = h0 + threadIdx.x;
-    const bool on = h < hh_total && gate[h] == gate_val;
-    const uint32_t bal = __ballot_sync(0xffffffffu, on);
-    __shared__ int wsum[32];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) wsum[w] = __popc(bal);
-    __syncthreads();
-    int before = base;
-    for (int x = 0; x < w; ++x) before += wsum[x];
-    if (on) list[before + __popc(bal & ((1u << lane) - 1u))] = h;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int tot = 0;
-      for (int x = 0; x < (int)(blockDim.x >> 5); ++x) tot += wsum[x];
-      base += tot;
+  const int g = heads / kv_heads;
+  const int groups = hh_total / g;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int grp = w; grp < groups; grp += nw) {
+    for (int base = 0; base < g; base += 32) {
+      const int h = grp * g + base + lane;
+      const bool on = base + lane < g && (gate == nullptr || gate[h] == gate_val);
+      const uint32_t bal = __ballot_sync(0xffffffffu, on);
+      const int cnt = __popc(bal);
+      const int rank = __popc(bal & ((1u << lane) - 1u));
+      int hb = 0, ub = 0;
+      const int nu = pair ? (cnt + 1) / 2 : cnt;
+      if (lane == 0) {
+        hb = atomicAdd(&n_heads, cnt);
+        ub = atomicAdd(&n_units, nu);
+      }
+      hb = __shfl_sync(0xffffffffu, hb, 0);
+      ub = __shfl_sync(0xffffffffu, ub, 0);
+      if (on) head_list[hb + rank] = h;
+      // the partner of selected rank 2p is the next selected lane
+      const uint32_t above = bal & ~((2u << lane) - 1u);
+      const int nxt = above ? __ffs(above) - 1 : -1;
+      const int hn = __shfl_sync(0xffffffffu, h, nxt >= 0 ? nxt : lane);
+      if (on && pair && (rank & 1) == 0) units[ub + rank / 2] = make_int2(h, nxt >= 0 ? hn : -1);
+      else if (on && !pair) units[ub + rank] = make_int2(h, -1);
     }
-    __syncthreads();
   }
-  if (threadIdx.x == 0) *count = base;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *unit_count = n_units;
+    *head_count = n_heads;
+  }
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -334,7 +412,7 @@ size_t tail_workspace_bytes(int hh_total, int n, int r_hi, int nchunks) {
   const int nkt = (r_hi + kTile - 1) / kTile;
   return align256((size_t)hh_total * nchunks * 128 * sizeof(float2)) +
          align256((size_t)hh_total * nkt * 256 * 4) + align256((size_t)hh_total * 128 * 4) +
-         align256((size_t)(hh_total + 1) * 4) + 256;
+         align256((size_t)(hh_total + 2) * 4) + align256((size_t)hh_total * 8) + 256;
 }
 
 // two key tiles per work item: enough items to fill every SM for one VS head
@@ -376,17 +454,21 @@ int launch_score_tail(int batch, int heads, int kv_heads, int n, float scale, co
   w += align256((size_t)a.hh_total * a.nkt * 256 * 4);
   a.lse2 = reinterpret_cast<float*>(w);
   w += align256((size_t)a.hh_total * 128 * 4);
-  int32_t* list = reinterpret_cast<int32_t*>(w);
+  int32_t* list = reinterpret_cast<int32_t*>(w);  // [0] head count, [1] unit count, [2..] heads
+  w += align256((size_t)(a.hh_total + 2) * 4);
+  int2* units = reinterpret_cast<int2*>(w);
   a.col_out = col_out;
   a.accumulate = accumulate;
-  a.head_list = nullptr;
-  a.head_count = nullptr;
-  if (gate) {
-    gate_list_kernel<<<1, 1024, 0, st>>>(gate, gate_val, a.hh_total, list + 1, list);
-    if ((rc = check_launch("gate_list_kernel"))) return rc;
-    a.head_list = list + 1;
-    a.head_count = list;
-  }
+  // two heads of one kv head share an M=128 box when the tail fits 64 rows
+  a.paired = (r_hi - r_lo <= 64 && heads / kv_heads >= 2) ? 1 : 0;
+  if (a.paired && (rc = make_tmap_3d_bf16(&a.tmap_q, q, kHeadDim, n, batch * heads, 64))) return rc;
+  build_units_kernel<<<1, 1024, 0, st>>>(gate, gate_val, a.hh_total, heads, kv_heads, a.paired, units, list + 1,
+                                          list + 2, list);
+  if ((rc = check_launch("build_units_kernel"))) return rc;
+  a.head_list = list + 2;
+  a.head_count = list;
+  a.units = units;
+  a.unit_count = list + 1;
   if (!accumulate) {
     // columns past the last scored row never receive mass
     cudaMemsetAsync(col_out, 0, (size_t)a.hh_total * n * sizeof(float), st);
