@@ -297,3 +297,78 @@ def test_host_streamed_nonfinite(sa):
     k[0, 0, n - 1, 127] = float("inf")
     with pytest.raises(sa.NonFiniteError):
         sa.prefill(q, k, v, cfg, mode="dense")
+
+
+# ---- runtime tests of the reference (test_runtime.py:74-148), device path ----
+
+def _inputs(seed, B, H, L, d):
+    rng = np.random.default_rng(seed)
+    return tuple(bf(rng.uniform(-1, 1, (B, H, L, d))) for _ in range(3))
+
+
+def test_auto_matches_manual_composition(sa):
+    """test_runtime.py:82-92: prefill(auto) == per-head build_index + sparse_attention."""
+    cfg = sa.ModelConfig(n_heads=2, d_model=8, d_head=4, max_context=64)
+    q, k, v = _inputs(62, 1, 2, 64, 4)
+    res = sa.prefill(q, k, v, cfg, mode="auto", cal_window=32, q_est=16)
+    for plan in res.plans[0]:
+        m = sa.AttnMatrices(q[0, plan.head], k[0, plan.head], v[0, plan.head])
+        idx = sa.build_index(m, plan.pattern, mode="estimated", q_est=16)
+        _, y = sa.sparse_attention(m, idx, need_weights=False)
+        h0 = plan.head * 4
+        close(res.outputs[0, :, h0:h0 + 4], y)
+
+
+def test_head_permutation_permutes_outputs_and_plans(sa):
+    """test_runtime.py:105-117 (exact equality: heads are independent on device too)."""
+    cfg = sa.ModelConfig(n_heads=3, d_model=6, d_head=2, max_context=16)
+    q, k, v = _inputs(64, 1, 3, 16, 2)
+    perm = [2, 0, 1]
+    base = sa.prefill(q, k, v, cfg, mode="auto", cal_window=8)
+    pres = sa.prefill(q[:, perm], k[:, perm], v[:, perm], cfg, mode="auto", cal_window=8)
+    for new_h, old_h in enumerate(perm):
+        np.testing.assert_array_equal(pres.outputs[0, :, new_h * 2:new_h * 2 + 2],
+                                      base.outputs[0, :, old_h * 2:old_h * 2 + 2])
+        assert pres.plans[0][new_h].pattern == base.plans[0][old_h].pattern
+
+
+@pytest.mark.parametrize("mode", ["dense", "auto"])
+def test_batched_sequences_independent(sa, mode):
+    """test_runtime.py:119-125, plus batch 3 x 4 heads x GQA against the oracle."""
+    cfg = sa.ModelConfig(n_heads=1, d_model=4, d_head=4, max_context=8)
+    q, k, v = _inputs(65, 2, 1, 8, 4)
+    both = sa.prefill(q, k, v, cfg, mode=mode)
+    solo = sa.prefill(q[1:], k[1:], v[1:], cfg, mode=mode)
+    np.testing.assert_array_equal(both.outputs[1], solo.outputs[0])
+    B, H, HK, n = 3, 4, 2, 700
+    q, k, v = (bf(x) for x in O.synth_qkv_gqa(66, n, H, HK, 128))
+    q, k, v = (np.concatenate([x, x[:, ::-1] * 0.5, -x], 0) for x in (q, k, v))
+    cfg = sa.ModelConfig(n_heads=H, d_model=H * 128, d_head=128, max_context=n)
+    res = sa.prefill(q, k, v, cfg, mode=mode)
+    want, plans = O.prefill(q, k, v, mode)
+    close(res.outputs, want)
+    if mode == "auto":
+        conv = lambda p: (type(p).__name__[0], *p.__dict__.values())  # noqa: E731
+        assert [[conv(hp.pattern) for hp in row] for row in res.plans] == [[conv(p) for p in row] for row in plans]
+
+
+def test_batched_host_streamed(sa):
+    """CPU torch inputs with batch 2 stream per (batch, kv group); same result as device inputs."""
+    B, H, HK, n = 2, 4, 2, 513
+    q, k, v = (torch.from_numpy(bf(x).astype(np.float32)).bfloat16() for x in O.synth_qkv_gqa(67, n, H, HK, 128))
+    q, k, v = (torch.cat([x, x.flip(2)], 0) for x in (q, k, v))
+    cfg = sa.ModelConfig(n_heads=H, d_model=H * 128, d_head=128, max_context=n)
+    host = sa.prefill(q, k, v, cfg, mode="auto")
+    dev = sa.prefill(q.cuda(), k.cuda(), v.cuda(), cfg, mode="auto")
+    assert torch.equal(host.outputs, dev.outputs.cpu())
+    assert [[hp.pattern for hp in r] for r in host.plans] == [[hp.pattern for hp in r] for r in dev.plans]
+
+
+def test_timing_decomposition(sa):
+    """test_runtime.py:139-147."""
+    cfg = sa.ModelConfig(n_heads=2, d_model=8, d_head=4, max_context=64)
+    q, k, v = _inputs(67, 1, 2, 64, 4)
+    res = sa.prefill(q, k, v, cfg, mode="auto", cal_window=32)
+    assert res.elapsed_s >= res.kernel_s >= 0.0
+    assert res.select_s >= 0.0
+    assert res.elapsed_s > 0.0
