@@ -63,6 +63,15 @@ struct AttnArgs {
 
 constexpr int kThreads = 192;
 constexpr int kDefaultPoly = 4;
+#ifndef SA_PRODUCER_SLEEP_NS
+#define SA_PRODUCER_SLEEP_NS 64
+#endif
+#ifndef SA_MMA_SLEEP_NS
+#define SA_MMA_SLEEP_NS 16
+#endif
+// polling back-off of the producer / MMA warps (they share sub-partitions with softmax warps)
+constexpr int kProducerSleepNs = SA_PRODUCER_SLEEP_NS;
+constexpr int kMmaSleepNs = SA_MMA_SLEEP_NS;
 #ifdef SA_ATTN_PROF
 constexpr bool kProf = true;
 #else
@@ -288,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       if (lane == 0) idx = a.counter ? atomicAdd(a.counter, 1) : (int)blockIdx.x + J * (int)gridDim.x;
       idx = __shfl_sync(0xffffffffu, idx, 0);
       const int item = idx < n_items ? item_at(a, idx) : -1;
-      if (J >= 2) mbar_wait(&bars[B_IE0 + (J & 1)], ((J >> 1) - 1) & 1);
+      if (J >= 2) mbar_wait_backoff<kProducerSleepNs>(&bars[B_IE0 + (J & 1)], ((J >> 1) - 1) & 1);
       if (lane == 0) {
         sItem[J & 1] = item;
         mbar_arrive(&bars[B_IF0 + (J & 1)]);
@@ -300,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       const int nsub = 2 * cnt;
       const uint32_t* tl = a.tiles + a.tile_off[item];
       // Q: the buffer is free once every QK MMA of the previous item completed
-      if (J >= 1) mbar_wait(&bars[B_QE], (J - 1) & 1);
+      if (J >= 1) mbar_wait_backoff<kProducerSleepNs>(&bars[B_QE], (J - 1) & 1);
       if (lane == 0) {
         mbar_arrive_expect_tx(&bars[B_Q], 32768);
         tma_load_3d(sQ, &a.tmap_q, &bars[B_Q], 0, qt * kTile, hh);
@@ -329,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
           slot_gk = gk;
         }
         PT(0);
-        if (g >= kRing) mbar_wait(&bars[B_EMPTY0 + slot], ((g / kRing) - 1) & 1);
+        if (g >= kRing) mbar_wait_backoff<kProducerSleepNs>(&bars[B_EMPTY0 + slot], ((g / kRing) - 1) & 1);
         PT(1);
         uint8_t* dst = sRing + slot * kSlotBytes;
         if (kind != TK_GATHER) {
@@ -370,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     PT_INIT
     int rb = 0, sb = 0, pb = 0;  // ring items, S-buffer uses (per buffer), PV commits so far
     for (int J = 0;; ++J) {
-      mbar_wait(&bars[B_IF0 + (J & 1)], (J >> 1) & 1);
+      mbar_wait_backoff<kMmaSleepNs>(&bars[B_IF0 + (J & 1)], (J >> 1) & 1);
       const int item = sItem[J & 1];
       __syncwarp();
       if (leader) mbar_arrive(&bars[B_IE0 + (J & 1)]);
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         auto issue_qk = [&](int u) {
           const int g = rb + 2 * u, slot = g % kRing;
           PT(0);
-          mbar_wait(&bars[B_FULL0 + slot], (g / kRing) & 1);
+          mbar_wait_backoff<kMmaSleepNs>(&bars[B_FULL0 + slot], (g / kRing) & 1);
           PT(1);
           tc_fence_after();
           const uint32_t k_addr = ring_addr + slot * kSlotBytes;
@@ -399,19 +408,19 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
           if (u == nsub - 1) mma_commit(&bars[B_QE]);  // last reader of Q
           PT(2);
         };
-        mbar_wait(&bars[B_Q], J & 1);
+        mbar_wait_backoff<kMmaSleepNs>(&bars[B_Q], J & 1);
         tc_fence_after();
         if (nsub == 0) mma_commit(&bars[B_QE]);
         if (nsub > 0) issue_qk(0);
         if (nsub > 1) issue_qk(1);
         for (int u = 0; u < nsub; ++u) {
           PT(3);
-          mbar_wait(&bars[B_PF0 + (u & 1)], (sb + (u >> 1)) & 1);
+          mbar_wait_backoff<kMmaSleepNs>(&bars[B_PF0 + (u & 1)], (sb + (u >> 1)) & 1);
           PT(4);
           const int g = rb + 2 * u + 1, slot = g % kRing;
-          mbar_wait(&bars[B_FULL0 + slot], (g / kRing) & 1);
+          mbar_wait_backoff<kMmaSleepNs>(&bars[B_FULL0 + slot], (g / kRing) & 1);
           // PV(0) overwrites O: the previous item's epilogue must have read it
-          if (u == 0 && J >= 1) mbar_wait(&bars[B_OE], (J - 1) & 1);
+          if (u == 0 && J >= 1) mbar_wait_backoff<kMmaSleepNs>(&bars[B_OE], (J - 1) & 1);
           PT(5);
           tc_fence_after();
           const uint32_t v_addr = ring_addr + slot * kSlotBytes;

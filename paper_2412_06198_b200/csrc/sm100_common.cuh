@@ -63,6 +63,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait that backs off with nanosleep between polls (for warps whose wake-up
+// latency is hidden by slack, e.g. a TMA producer running ahead of its ring),
+// so the polling loop leaves issue slots to the math warps of its sub-partition.
+template <int NS = 64>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+               "selp.b32 %0, 1, 0, P1;\n\t}" : "=r"(done) : "r"(addr), "r"(parity) : "memory");
+  while (!done) {
+    __nanosleep(NS);
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.b32 %0, 1, 0, P1;\n\t}" : "=r"(done) : "r"(addr), "r"(parity) : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
