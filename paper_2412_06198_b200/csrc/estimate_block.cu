@@ -131,9 +131,10 @@ __global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid
   // 1024-aligned offset into the dynamic shared array (pointer arithmetic on
   // smem_raw keeps the shared address space, so accesses compile to LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int hh = a.hh_base + blockIdx.y;
+  // grid (heads, query tiles): every head's heaviest tile is dispatched first
+  const int hh = a.hh_base + blockIdx.x;
   if (a.gate && a.gate[hh] != a.gate_val) return;
-  const int qt = a.nqt - 1 - blockIdx.x;  // heavy tiles first
+  const int qt = a.nqt - 1 - blockIdx.y;
   const int cnt = qt + 1;                  // causal key tiles
   uint8_t* sA = smem + kBsSmemA;
   uint8_t* sB = smem + kBsSmemB;
@@ -470,7 +471,7 @@ int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_
   if (k_b <= 8) {
     a.hh_base = 0;
     a.hh_count = hh_total;
-    dim3 grid(a.nqt, hh_total);
+    dim3 grid(hh_total, a.nqt);
     if (k_b == 1) block_score_kernel<1, true><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
     else if (k_b == 2) block_score_kernel<2, true><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
     else if (k_b <= 4) block_score_kernel<4, true><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
@@ -494,7 +495,7 @@ int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_
     const int cnt = std::min(G, hh_total - h0);
     a.hh_base = h0;
     a.hh_count = cnt;
-    dim3 grid(a.nqt, cnt);
+    dim3 grid(cnt, a.nqt);
     block_score_kernel<1, false><<<grid, kBsThreads, kBsSmemBytes, st>>>(a);
     if ((rc = check_launch("block_score_kernel<materialize>"))) return rc;
     TopkArgs t{};
