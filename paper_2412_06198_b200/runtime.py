@@ -268,6 +268,26 @@ class PrefillPlan:
         _lib.call("sa_prefill", self.desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                   ws.data_ptr(), ws.numel(), D.stream())
 
+    def graph(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor,
+              ws: torch.Tensor) -> torch.cuda.CUDAGraph:
+        """Capture selection + the whole layer into a CUDA graph bound to these
+        buffers; `replay()` recomputes `out` for whatever q/k/v then hold (same
+        shapes).  Saves the per-kernel launch gaps of the eager path."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            if self.mode == "auto":  # warm the lazy per-kernel attributes outside capture
+                self.select(q, k, ws)
+            self.run(q, k, v, out, ws)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=side):
+                if self.mode == "auto":
+                    self.select(q, k, ws)
+                self.run(q, k, v, out, ws)
+        torch.cuda.current_stream().wait_stream(side)
+        return g
+
     def plans(self, ws: torch.Tensor, with_search: bool = True):
         """Per (batch, head) HeadPlan list from the device choice (one small D2H)."""
         v = self.views(ws)

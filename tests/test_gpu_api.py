@@ -372,3 +372,30 @@ def test_timing_decomposition(sa):
     assert res.elapsed_s >= res.kernel_s >= 0.0
     assert res.select_s >= 0.0
     assert res.elapsed_s > 0.0
+
+
+def test_prefill_plan_graph_replay(sa):
+    """PrefillPlan.graph: a CUDA-graph replay equals the eager layer, and recomputes
+    for new contents of the same input buffers."""
+    from paper_2412_06198_b200 import runtime as R
+
+    H, HK, n = 8, 2, 1000
+    q, k, v = (torch.from_numpy(O.bf16_round(x)[0]).cuda().bfloat16() for x in O.synth_qkv_gqa(71, n, H, HK, 128))
+    plan = R.PrefillPlan(1, H, HK, n, 128, "auto")
+    ws = R._workspace(plan.ws_bytes, q.device)
+    out = torch.empty((1, n, H * 128), dtype=torch.bfloat16, device="cuda")
+    plan.select(q, k, ws)
+    plan.run(q, k, v, out, ws)
+    eager = out.clone()
+    g = plan.graph(q, k, v, out, ws)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+    q.mul_(-1)
+    g.replay()
+    plan.select(q, k, ws)
+    ref = torch.empty_like(out)
+    plan.run(q, k, v, ref, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
