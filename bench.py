@@ -58,10 +58,12 @@ def parse():
 
 def synth_inputs(seed: int, ctx: int):
     """bf16-rounded uniform q (H, n, d), k (HK, n, d), v (HK, n, d) as float32."""
-    from oracle.sparse_oracle import bf16_round, synth_qkv_gqa  # input generator only
+    import torch
+
+    from paper_2412_06198_b200.harness import synth_qkv_gqa
 
     q, k, v = synth_qkv_gqa(seed, ctx, H, HK, D)
-    return bf16_round(q[0]), bf16_round(k[0]), bf16_round(v[0])
+    return tuple(torch.from_numpy(x[0]).bfloat16().float().numpy() for x in (q, k, v))
 
 
 def measured_peaks():
@@ -301,10 +303,9 @@ def run_ours(args):
         fixed = {"tri": Triangular, "vs": VerticalSlash, "block": BlockSparse}[fam](int(p1), int(p2))
         mode = "fixed"
     elif mode != "auto" and mode != "dense":
-        from oracle.sparse_oracle import fixed_pattern_for
+        from paper_2412_06198_b200.harness import fixed_pattern_for
 
-        fp = fixed_pattern_for(mode, n)
-        fixed = {"Tri": Triangular, "VS": VerticalSlash, "Blk": BlockSparse}[type(fp).__name__](*fp.__dict__.values())
+        fixed = fixed_pattern_for(mode, n)
         mode = "fixed"
     plan = R.PrefillPlan(1, h_l, hk_l, n, D, mode, fixed_pattern=fixed)
     ws = R._workspace(plan.ws_bytes, dev)

@@ -60,6 +60,7 @@ struct AttnArgs {
   float* lse;  // optional [hh_total, n] natural-log row log-sum-exp
   unsigned long long* prof;  // SA_ATTN_PROF builds: per-role phase cycle counters [3 * 16]
   int* counter;              // optional work-item counter (zeroed before launch): dynamic fetch
+  const int32_t* n_work;     // optional device count of `work` entries (default hh_total * nqt)
 };
 
 constexpr int kThreads = 192;
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 
   const long long t_entry = kProf ? clock64() : 0;
   const int warp = warp_id();
-  const int n_items = a.hh_total * a.nqt;
+  const int n_items = a.n_work ? *a.n_work : a.hh_total * a.nqt;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[B_Q], 1);
@@ -399,12 +400,16 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         tmem_ld_wait();
         PT(3);
         if (kind != TK_FULL) {
+          // float selects on constant bit tests: ptxas emits R2P (7 mask bits
+          // to predicates at once) + FSEL, about one instruction per logit
           const uint32_t m0 = half ? msk[2] : msk[0], m1 = half ? msk[3] : msk[1];
+          // (one loop per mask word: interleaving the two words defeats the R2P match)
 #pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            if (!((m0 >> t) & 1u)) s[0][t] = __float_as_uint(-INFINITY);
-            if (!((m1 >> t) & 1u)) s[1][t] = __float_as_uint(-INFINITY);
-          }
+          for (int t = 0; t < 32; ++t)
+            if (!(m0 & (1u << t))) s[0][t] = __float_as_uint(-INFINITY);
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (!(m1 & (1u << t))) s[1][t] = __float_as_uint(-INFINITY);
         }
         // row max: four independent FMNMX3 chains
         float mx;
@@ -543,7 +548,7 @@ namespace sa {
 int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const void* q, const void* k,
                 const void* v, void* out, const sa_head_index* index, const int32_t* tile_off,
                 const int32_t* tile_cnt, const uint32_t* tiles, const int32_t* work, float* lse,
-                cudaStream_t cs, long long out_ld, int* counter) {
+                cudaStream_t cs, long long out_ld, int* counter, const int32_t* n_work) {
   if (batch < 1 || heads < 1 || kv_heads < 1 || n < 1)
     return fail(SA_ERR_DIMENSION, "need batch, heads, kv_heads, n >= 1");
   if (heads % kv_heads != 0)
@@ -574,6 +579,7 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   a.tiles = tiles;
   a.work = work;
   a.counter = counter;
+  a.n_work = n_work;
   if (counter) cudaMemsetAsync(counter, 0, sizeof(int), cs);
   a.idx = *index;
   a.lse = lse;

@@ -165,7 +165,7 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
   sz[W_TOFF] = hh * p->nqt * 4;
   sz[W_TCNT] = hh * p->nqt * 4;
   sz[W_TILES] = hh * (size_t)p->nqt * (p->nqt + 1) / 2 * 4;
-  sz[W_WORK] = hh * p->nqt * 4 + 16;  // + the persistent kernel's work counter
+  sz[W_WORK] = (64 + hh * p->nqt) * 4;  // [counter, item count], then the work order
   size_t o = 0;
   for (int i = 0; i < W_NUM; ++i) {
     L->off[i] = o;
@@ -355,19 +355,19 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   // 4. executed tiles + attention
   if ((rc = sa_build_tiles(&V.index, p.hh, n, V.tile_off, V.tile_cnt, V.tiles, stream))) return rc;
   mark(3);
-  // longest-first CTA order (SA_ATTN_ORDER=0 keeps the kernel's kv-group-major default, for A/B)
+  // longest-first CTA order over the non-empty items (SA_ATTN_ORDER=0 keeps
+  // the kernel's kv-group-major default, for A/B)
   static const bool lpt = [] {
     const char* e = getenv("SA_ATTN_ORDER");
     return !(e && e[0] == '0');
   }();
-  int32_t* work = nullptr;
-  int* counter = reinterpret_cast<int*>(b + L.off[W_WORK]);
-  if (lpt) {
-    work = counter + 4;
-    if ((rc = sa_order_work(V.tile_cnt, p.hh * p.nqt, p.nqt, work, stream))) return rc;
-  }
+  int32_t* wbase = reinterpret_cast<int32_t*>(b + L.off[W_WORK]);
+  int* counter = wbase;
+  int32_t* n_work = wbase + 1;
+  int32_t* work = wbase + 64;
+  if (lpt && (rc = launch_order_work(V.tile_cnt, p.hh * p.nqt, p.nqt, work, n_work, st))) return rc;
   rc = launch_attn(B, H, HK, n, desc->scale, q, k, v, out, &V.index, V.tile_off, V.tile_cnt, V.tiles,
-                   work, nullptr, st, desc->out_ld, counter);
+                   lpt ? work : nullptr, nullptr, st, desc->out_ld, counter, lpt ? n_work : nullptr);
   mark(4);
   return rc;
 }

@@ -158,17 +158,23 @@ __global__ void build_tiles_kernel(TileBuildArgs a) {
 // qt) with the r-th largest tile count (counting sort, one CTA).  The block
 // scheduler dispatches CTAs roughly in blockIdx order, so the heaviest query
 // tiles (full-width VS rows) start first and the light ones fill the tail.
+// Items of count 0 (nothing to compute) go last; n_work, when given, receives
+// the number of nonzero items.
+__device__ __forceinline__ int order_bin(int c, int shift) {
+  return c > 0 ? 1022 - min(c >> shift, 1022) : 1023;
+}
 __global__ void __launch_bounds__(1024) order_work_kernel(const int32_t* __restrict__ cnt, int items,
-                                                          int max_cnt, int32_t* __restrict__ work) {
-  // bins: tile count >> shift, at most 1024 (one per thread), heaviest first
+                                                          int max_cnt, int32_t* __restrict__ work,
+                                                          int32_t* __restrict__ n_work) {
+  // bins: tile count >> shift, at most 1023 (one per thread) plus the empty bin, heaviest first
   __shared__ int start[1024];
   __shared__ int wsum[32];
   int shift = 0;
-  while ((max_cnt >> shift) >= 1024) ++shift;
+  while ((max_cnt >> shift) >= 1023) ++shift;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   start[t] = 0;
   __syncthreads();
-  for (int i = t; i < items; i += blockDim.x) atomicAdd(&start[1023 - min(max(cnt[i], 0) >> shift, 1023)], 1);
+  for (int i = t; i < items; i += blockDim.x) atomicAdd(&start[order_bin(cnt[i], shift)], 1);
   __syncthreads();
   // exclusive scan over position p = 1023 - bin (heaviest bin first)
   const int v = start[t];
@@ -192,9 +198,10 @@ __global__ void __launch_bounds__(1024) order_work_kernel(const int32_t* __restr
   }
   __syncthreads();
   start[t] = wsum[w] + x - v;
+  if (t == 1023 && n_work) *n_work = start[t];
   __syncthreads();
   for (int i = t; i < items; i += blockDim.x) {
-    const int pos = atomicAdd(&start[1023 - min(max(cnt[i], 0) >> shift, 1023)], 1);
+    const int pos = atomicAdd(&start[order_bin(cnt[i], shift)], 1);
     work[pos] = i;
   }
 }
@@ -203,6 +210,7 @@ __global__ void __launch_bounds__(1024) order_work_kernel(const int32_t* __restr
 
 // ------------------------------------------------------------------ C ABI
 #include "api_common.h"
+#include "internal.h"
 
 extern "C" int sa_build_tiles(const sa_head_index* index, int hh_total, int n, int32_t* tile_off,
                               int32_t* tile_cnt, uint32_t* tiles, void* stream) {
@@ -232,6 +240,14 @@ extern "C" int sa_order_work(const int32_t* tile_cnt, int items, int max_cnt, in
   if (items < 1 || max_cnt < 0 || max_cnt > 65536) return fail(SA_ERR_DIMENSION, "bad work-order sizes");
   if (!tile_cnt || !work) return fail(SA_ERR_DIMENSION, "null pointer");
   order_work_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      tile_cnt, items, max_cnt, work);
+      tile_cnt, items, max_cnt, work, nullptr);
   return check_launch("order_work_kernel");
 }
+
+namespace sa {
+int launch_order_work(const int32_t* cost, int items, int max_cost, int32_t* work, int32_t* n_work,
+                      cudaStream_t st) {
+  order_work_kernel<<<1, 1024, 0, st>>>(cost, items, max_cost, work, n_work);
+  return check_launch("order_work_kernel");
+}
+}  // namespace sa
