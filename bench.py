@@ -66,6 +66,12 @@ def synth_inputs(seed: int, ctx: int):
     return tuple(torch.from_numpy(x[0]).bfloat16().float().numpy() for x in (q, k, v))
 
 
+def l2_note(n: int) -> str:
+    q_mb, kv_mb = H * n * D * 2 / 1e6, 2 * HK * n * D * 2 / 1e6
+    fits = "exceed" if q_mb + kv_mb > 126 else "fit in"
+    return f"inputs (Q {q_mb:.0f} MB + K/V {kv_mb:.0f} MB) {fits} the 126 MB L2; no flush"
+
+
 def measured_peaks():
     p = os.path.join(HERE, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -447,7 +453,7 @@ def run_ours(args):
             "config": {"workload": f"llama3-8b-attn-layer-{n // 1024}k-{args.mode}", "heads": H, "kv_heads": HK,
                        "head_dim": D, "seq_len": n, "batch": 1, "mode": args.mode,
                        "parallelism": f"head-parallel x{world} + NCCL all-gather" if world > 1 else "single GPU",
-                       "l2": "inputs (Q 268 MB + K/V 134 MB at 32K) exceed the 126 MB L2; no flush",
+                       "l2": l2_note(n),
                        "launch": "timed steps replay a CUDA graph of selection + layer (PrefillPlan.graph); "
                                  "stage_ms from eager steps with stage events",
                        "families_rank0": fam_counts},

@@ -18,6 +18,13 @@
 // Rows whose candidates stay above 1024 after two levels (massive exact ties)
 // use an exact 4 x 8-bit radix select.  Output: every j with composite >= T,
 // in index order, by a warp-ballot ordered compaction.
+//
+// Long rows (n >= kClusterMin, the VS score rows at 16K+ tokens) run on a cluster of
+// kClusterC CTAs per row: each CTA stages 1/kClusterC of the row as keys in its
+// shared memory, the per-CTA histograms and candidates meet in the leader CTA
+// through distributed shared memory, and the ordered compaction offsets each
+// CTA by the kept counts of the lower-ranked ones.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -371,20 +378,297 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
   if (tid == 0 && a.count_out) a.count_out[blockIdx.x] = total;
 }
 
+namespace cg = cooperative_groups;
+constexpr int kClusterC = 8;
+constexpr int kClusterMin = 16384;  // plain rows at least this long use a cluster per row
+
+// Radix fallback (massive exact ties) over the fp32 row in global memory; the
+// result lands in *T_out (block-wide; every thread of the CTA calls it).
+__device__ void radix_threshold(const float* s, int len, int k, int* hist, int* warp_tot, uint32_t* sh_digit,
+                                int* sh_rem, uint64_t* T_out) {
+  const int tid = threadIdx.x;
+  uint32_t prefix = 0u, mask = 0u;
+  int remaining = k;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int t = tid; t < 256; t += blockDim.x) hist[t] = 0;
+    __syncthreads();
+    for (int j = tid; j < len; j += blockDim.x) {
+      const uint32_t key = pref_key(__ldg(s + j));
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int d = 255; d >= 0; --d) {
+        if (run + hist[d] >= remaining) {
+          *sh_digit = (uint32_t)d;
+          *sh_rem = remaining - run;
+          break;
+        }
+        run += hist[d];
+      }
+    }
+    __syncthreads();
+    prefix |= *sh_digit << shift;
+    mask |= 255u << shift;
+    remaining = *sh_rem;
+    __syncthreads();
+  }
+  const int per = (len + blockDim.x - 1) / blockDim.x;
+  const int b0 = min(len, tid * per), b1 = min(len, b0 + per);
+  int eq = 0;
+  for (int j = b0; j < b1; ++j) eq += pref_key(__ldg(s + j)) == prefix;
+  int tot;
+  const int before = block_excl_scan(eq, warp_tot, tot);
+  if (before < remaining && before + eq >= remaining) {
+    int seen = before;
+    for (int j = b0; j < b1; ++j) {
+      if (pref_key(__ldg(s + j)) == prefix && ++seen == remaining) {
+        *T_out = composite(prefix, j);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads)
+    topk_cluster_kernel(TopkArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int cr = (int)cl.block_rank();
+  int r = blockIdx.x / kClusterC;
+  const float* scores = a.scores;
+  int kk = a.k;
+  int32_t* idx_out = a.idx_out;
+  long long out_ld = a.out_ld;
+  uint32_t* bits = a.bits;
+  int bit_base = a.bit_base, bit_neg = a.bit_neg;
+  if (a.split > 0 && r >= a.split) {
+    r -= a.split;
+    scores = a.scores2;
+    kk = a.k2;
+    idx_out = a.idx_out2;
+    out_ld = a.out_ld2;
+    bits = a.bits2;
+    bit_base = a.bit_base2;
+    bit_neg = a.bit_neg2;
+  }
+  if (a.gate && a.gate[r / a.gate_div] != a.gate_val) return;  // uniform over the cluster
+  const int len = a.n;
+  const int k = kk < len ? kk : len;
+  const float* s = scores + (long long)r * a.ld;
+  // this CTA's slice [j_lo, j_hi), a multiple of 4 keys long
+  const int per = (((len + kClusterC - 1) / kClusterC) + 3) & ~3;
+  const int j_lo = min(len, cr * per), j_hi = min(len, j_lo + per), sl = j_hi - j_lo;
+
+  extern __shared__ __align__(16) uint8_t tk_smem[];
+  int* hist = reinterpret_cast<int*>(tk_smem);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(tk_smem + kBins * 4);
+  uint32_t* skey = reinterpret_cast<uint32_t*>(tk_smem + kTopkSmem);  // [per]
+  __shared__ int warp_tot[33];
+  __shared__ uint32_t sh_min, sh_max;
+  __shared__ int sh_m, sh_tot, sh_base;
+  __shared__ int sh_pair[3];
+  __shared__ uint64_t sh_T;
+  __shared__ uint32_t sh_digit;
+  __shared__ int sh_rem;
+  const int tid = threadIdx.x, lane = tid & 31;
+
+  // stage the slice as preference keys (16-byte loads when aligned)
+  {
+    const float* sp = s + j_lo;
+    const bool vec = ((reinterpret_cast<uintptr_t>(sp) & 15) == 0);
+    const int n4 = vec ? sl / 4 : 0;
+    for (int j4 = tid; j4 < n4; j4 += blockDim.x) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(sp) + j4);
+      skey[4 * j4] = pref_key(v.x);
+      skey[4 * j4 + 1] = pref_key(v.y);
+      skey[4 * j4 + 2] = pref_key(v.z);
+      skey[4 * j4 + 3] = pref_key(v.w);
+    }
+    for (int j = 4 * n4 + tid; j < sl; j += blockDim.x) skey[j] = pref_key(__ldg(sp + j));
+  }
+  const bool take_all = k >= len;
+  uint64_t T = 0;
+  if (!take_all && k > 0) {
+    // 1. key range: CTA min/max, then the leader's
+    if (tid == 0) {
+      sh_min = 0xffffffffu;
+      sh_max = 0u;
+    }
+    __syncthreads();
+    uint32_t mn = 0xffffffffu, mx = 0u;
+    for (int j = tid; j < sl; j += blockDim.x) {
+      mn = min(mn, skey[j]);
+      mx = max(mx, skey[j]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+      atomicMin(&sh_min, mn);
+      atomicMax(&sh_max, mx);
+    }
+    cl.sync();
+    if (tid == 0 && cr != 0) {
+      atomicMin(cl.map_shared_rank(&sh_min, 0), sh_min);
+      atomicMax(cl.map_shared_rank(&sh_max, 0), sh_max);
+    }
+    cl.sync();
+    uint32_t lo = *cl.map_shared_rank(&sh_min, 0);
+    uint64_t span = (uint64_t)(*cl.map_shared_rank(&sh_max, 0) - lo) + 1;
+    int want = k;
+    bool located = false;
+    for (int level = 0; level < 2 && !located; ++level) {
+      // 2. per-CTA histograms of the slice; the leader sums them and locates
+      for (int t = tid; t < kBins; t += blockDim.x) hist[t] = 0;
+      __syncthreads();
+      const BinMap bm = make_binmap(lo, span);
+      for (int j = tid; j < sl; j += blockDim.x) {
+        const uint32_t key = skey[j];
+        if (key >= lo && (uint64_t)(key - lo) < span) atomicAdd(&hist[key_bin(key, bm)], 1);
+      }
+      cl.sync();
+      if (cr == 0) {
+        for (int q = 1; q < kClusterC; ++q) {
+          const int* rh = cl.map_shared_rank(hist, q);
+          for (int t = tid; t < kBins; t += blockDim.x) hist[t] += rh[t];
+        }
+        __syncthreads();
+        const int pb = kBins / blockDim.x;
+        const int b_hi = kBins - tid * pb;
+        int mine = 0;
+        for (int q = 1; q <= pb; ++q) mine += hist[b_hi - q];
+        int tot;
+        const int before = block_excl_scan(mine, warp_tot, tot);
+        if (before < want && before + mine >= want) {
+          int run = before;
+          for (int q = 1; q <= pb; ++q) {
+            const int b = b_hi - q;
+            if (run + hist[b] >= want) {
+              sh_pair[0] = b;
+              sh_pair[1] = run;
+              sh_pair[2] = hist[b];
+              break;
+            }
+            run += hist[b];
+          }
+        }
+        if (tid == 0) sh_m = 0;
+      }
+      cl.sync();
+      const int* lp = cl.map_shared_rank(sh_pair, 0);
+      const int bin = lp[0], above = lp[1], m = lp[2];
+      want -= above;
+      const uint64_t b0 = bin_start(bin, span);
+      const uint64_t b1 = bin_start(bin + 1, span);
+      lo = lo + (uint32_t)b0;
+      span = b1 - b0;
+      if (m > kCand) continue;  // uniform: every CTA read the same m
+      // 3. the bin's composites gather in the leader
+      int* lm = cl.map_shared_rank(&sh_m, 0);
+      uint64_t* lc = cl.map_shared_rank(cand, 0);
+      for (int j0 = tid; (j0 & ~31) < sl; j0 += blockDim.x) {  // warp-uniform trip count
+        const uint32_t key = j0 < sl ? skey[j0] : 0u;
+        const bool hit = j0 < sl && key >= lo && (uint64_t)(key - lo) < span;
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (bal) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(lm, __popc(bal));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (hit) lc[base + __popc(bal & ((1u << lane) - 1u))] = composite(key, j_lo + j0);
+        }
+      }
+      cl.sync();
+      // 4. exact ranks in the leader
+      if (cr == 0) {
+        for (int c = tid; c < m; c += blockDim.x) {
+          const uint64_t me = cand[c];
+          int rank = 0;
+          for (int o = 0; o < m; ++o) rank += cand[o] > me;
+          if (rank == want - 1) sh_T = me;
+        }
+      }
+      cl.sync();
+      T = *cl.map_shared_rank(&sh_T, 0);
+      located = true;
+    }
+    if (!located) {
+      if (cr == 0) radix_threshold(s, len, k, hist, warp_tot, &sh_digit, &sh_rem, &sh_T);
+      cl.sync();
+      T = *cl.map_shared_rank(&sh_T, 0);
+    }
+  }
+
+  // ordered compaction of the slice, offset by the kept counts of lower ranks
+  const int nw = blockDim.x >> 5, w = tid >> 5;
+  const int wlen = (((sl + nw - 1) / nw) + 31) & ~31;
+  const int w0 = min(sl, w * wlen), w1 = min(sl, w0 + wlen);
+  int mine = 0;
+  for (int j = w0 + lane; (j - lane) < w1; j += 32) {
+    const bool keep = j < w1 && (take_all || (k > 0 && composite(skey[j], j_lo + j) >= T));
+    mine += __popc(__ballot_sync(0xffffffffu, keep));
+  }
+  int total;
+  const int wbase = block_excl_scan(lane == 0 ? mine : 0, warp_tot, total);
+  if (tid == 0) sh_tot = total;
+  cl.sync();
+  if (tid == 0) {
+    int b = 0, all = 0;
+    for (int q = 0; q < kClusterC; ++q) {
+      const int c = *cl.map_shared_rank(&sh_tot, q);
+      if (q < cr) b += c;
+      all += c;
+    }
+    sh_base = b;
+    if (cr == 0 && a.count_out) a.count_out[blockIdx.x / kClusterC] = all;
+  }
+  __syncthreads();
+  int pos = sh_base + __shfl_sync(0xffffffffu, wbase, 0);
+  if (mine > 0) {
+    for (int j = w0 + lane; (j - lane) < w1; j += 32) {
+      const bool keep = j < w1 && (take_all || (k > 0 && composite(skey[j], j_lo + j) >= T));
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int p = pos + __popc(bal & ((1u << lane) - 1u));
+        const int jj = j_lo + j;
+        if (idx_out) idx_out[(long long)r * out_ld + p] = jj;
+        if (bits) {
+          const int bp = bit_neg ? bit_base - jj : bit_base + jj;
+          atomicOr(bits + (long long)r * a.bits_ld + (bp >> 5), 1u << (bp & 31));
+        }
+      }
+      pos += __popc(bal);
+    }
+  }
+  cl.sync();  // no CTA leaves while its shared memory may still be read
+}
+
 int launch_topk(const TopkArgs& a, cudaStream_t st) {
   const int rows = a.split > 0 ? 2 * a.split : a.rows;
   if (rows <= 0) return SA_OK;
   // short segmented rows (block estimator) use 256 threads per row
   const int threads = (a.lens != nullptr && a.n <= 4096) ? 256 : kTopkThreads;
-  // rows up to kCacheMax keys are staged in shared memory once
+  // rows up to kCacheMax keys are staged in shared memory once by one CTA;
+  // longer plain rows by a cluster of kClusterC CTAs
   constexpr int kCacheMax = 49152;
+  const int cl_per = (((a.n + kClusterC - 1) / kClusterC) + 3) & ~3;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(topk_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kTopkSmem + kCacheMax * 4);
+    cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kTopkSmem + ((262144 / kClusterC) + 4) * 4);
     attr = true;
   }
-  const int maxlen = a.lens ? a.n : a.n;  // a.n bounds every row length
+  if (a.lens == nullptr && a.ks == nullptr && a.n >= kClusterMin && a.n <= 262144 && threads == kTopkThreads) {
+    topk_cluster_kernel<<<rows * kClusterC, kTopkThreads, kTopkSmem + cl_per * 4, st>>>(a);
+    return check_launch("topk_cluster_kernel");
+  }
+  const int maxlen = a.n;  // a.n bounds every row length
   if (maxlen <= kCacheMax && a.lens == nullptr)
     topk_rows_kernel<true><<<rows, threads, kTopkSmem + maxlen * 4, st>>>(a);
   else

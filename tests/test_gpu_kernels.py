@@ -173,7 +173,8 @@ def device_topk(scores32: np.ndarray, k: int) -> np.ndarray:
     return out.cpu().numpy()
 
 
-@pytest.mark.parametrize("n,k", [(1, 1), (7, 3), (300, 300), (4096, 205), (131072, 6144), (131072, 1)])
+@pytest.mark.parametrize("n,k", [(1, 1), (7, 3), (300, 300), (4096, 205), (49153, 2000), (131072, 6144),
+                                 (131072, 1), (131075, 131074), (262144, 9000)])
 def test_topk_bit_exact(sa, n, k):
     rng = np.random.default_rng(n + k)
     rows = np.stack([
