@@ -57,7 +57,10 @@ struct TailArgs {
   const int32_t* unit_count;  // device count of units
 };
 
-constexpr int kTailThreads = 192;
+// warps 0-7: two per TMEM lane quarter, each row's 128 keys split in halves
+// (cpart = warp / 4); warp 8: TMA producer; warp 9: MMA issuer
+constexpr int kTailThreads = 320;
+constexpr int kTailSoft = 256;
 constexpr int kWStride = 129;  // padded row stride of the W transpose buffer
 constexpr int kTailSmemQ = 0;
 constexpr int kTailKSlots = 4;          // 32 KB K tiles in flight (HBM latency in pass 2)
@@ -111,17 +114,17 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bars[T_SF0 + s], 1);
-      mbar_init(&bars[T_SE0 + s], 128);
+      mbar_init(&bars[T_SE0 + s], kTailSoft);
     }
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc(tmem_holder, 256);
+  if (warp == 9) tmem_alloc(tmem_holder, 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (elect_one()) {
       int jg = 0, it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, 128, 0, 0);
       const uint32_t q_addr = smem_u32(sQ);
@@ -183,15 +186,15 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
       }
     }
   } else {
-    const int t = threadIdx.x;  // TMEM lane = row of the MMA box
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const int t = threadIdx.x & 127;  // TMEM lane = row of the MMA box
+    const int cpart = warp >> 2;      // this thread's half of the row's 128 keys
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const float sl2 = a.scale_log2;
     // rows of this thread: paired -> head half t >> 6, row r_hi - 64 + (t & 63),
     // stats lane 64 + (t & 63); single -> row s0 + t, stats lane t
     const int i = a.paired ? a.r_hi - 64 + (t & 63) : a.s0 + t;
     const int slane = a.paired ? 64 + (t & 63) : t;
     const int R = a.r_hi - a.r_lo;
-    // W rows [w_lo, w_hi) hold this half's scored rows
     int jg = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int2 un = unit_at(a, item / a.nchunks);
@@ -204,19 +207,19 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
       if (PASS == 2 && active) lse2 = a.lse2[(size_t)hh * 128 + slane];
       for (int kt = kt_lo; kt < kt_hi; ++kt, ++jg) {
         const int slot = jg & 1;
-        const int j0 = kt * kTile;
+        const int j0 = kt * kTile + 64 * cpart;  // first key of this thread's half
         mbar_wait(&bars[T_SF0 + slot], (jg >> 1) & 1);
         tc_fence_after();
-        uint32_t s[4][32];
+        uint32_t s[2][32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(tbase + lane_off + slot * 128 + 32 * c, s[c]);
+        for (int c = 0; c < 2; ++c) tmem_ld32(tbase + lane_off + slot * 128 + 64 * cpart + 32 * c, s[c]);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars[T_SE0 + slot]);
         const int lim = i - j0;  // keep columns c <= lim
-        if (active && lim < 127) {  // causal cut (the diagonal tile only)
+        if (active && lim < 63) {  // causal cut (the diagonal tile only)
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
             for (int u = 0; u < 32; ++u)
               if (32 * c + u > lim) s[c][u] = __float_as_uint(-INFINITY);
@@ -225,16 +228,19 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
           if (active) {
             float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < 2; ++c)
 #pragma unroll
-              for (int u = 0; u < 32; u += 2) m4[c] = fmax3(m4[c], __uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1]));
+              for (int u = 0; u < 32; u += 4) {
+                m4[2 * c] = fmax3(m4[2 * c], __uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1]));
+                m4[2 * c + 1] = fmax3(m4[2 * c + 1], __uint_as_float(s[c][u + 2]), __uint_as_float(s[c][u + 3]));
+              }
             const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-            if (mx == -INFINITY) continue;  // no causal key of this row in the tile
+            if (mx == -INFINITY) continue;  // no causal key of this row in the half tile
             const float mn = fmaxf(m, mx * sl2);
             const float2 sc2 = make_float2(sl2, sl2), mo2 = make_float2(-mn, -mn);
             float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < 2; ++c)
 #pragma unroll
               for (int u = 0; u < 32; u += 2) {
                 // (MUFU only: the scores feed a bit-exact top-k, keep them at ex2.approx accuracy)
@@ -247,10 +253,10 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
             m = mn;
           }
         } else {
-          float* wrow = sW + t * kWStride;
+          float* wrow = sW + t * kWStride + 64 * cpart;
           const float2 sc2 = make_float2(sl2, sl2), mo2 = make_float2(-lse2, -lse2);
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
             for (int u = 0; u < 32; u += 2) {
               float2 x = ffma2(make_float2(__uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1])), sc2, mo2);
@@ -259,53 +265,70 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
               wrow[32 * c + u] = active ? x.x : 0.f;
               wrow[32 * c + u + 1] = active ? x.y : 0.f;
             }
-          named_bar_sync(1, 128);
-          // per head half: column sums (thread t owns column j0 + t) and the
-          // diagonal partials, local offset op in [0, 256): c = (r - w_lo) + 127 - op
+          named_bar_sync(1, kTailSoft);
+          // reduction tasks per head half: 128 column sums (task c -> column
+          // j0 + c) and 256 diagonal partials (local offset op, elements at
+          // column c = (r - w_lo) + 127 - op); 256 threads stride over them
+          const int kt0 = kt * kTile;
+          const int nh = a.paired ? 2 : 1;
 #pragma unroll 1
-          for (int hf = 0; hf < (a.paired ? 2 : 1); ++hf) {
+          for (int task = threadIdx.x; task < nh * 384; task += kTailSoft) {
+            const int hf = task / 384, rem = task % 384;
             const int hx = hf ? un.y : un.x;
             if (hx < 0) continue;
             const int w_hi = a.paired ? 64 * hf + 64 : a.r_hi - a.s0;
             const int w_lo = w_hi - R;
-            // independent partial sums (the loads of one sum are not serialised)
-            float c4[4] = {0.f, 0.f, 0.f, 0.f};
-            int r = w_lo;
-            for (; r + 4 <= w_hi; r += 4) {
+            // every W row of the half is written (inactive rows as 0), so the
+            // sums run over all of them unconditionally, 32 independent loads
+            // per block (latency, not bandwidth, bounds this phase)
+            const int rows0 = a.paired ? 64 * hf : 0, nrows = a.paired ? 64 : 128;
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (rem < 128) {
+              for (int rb = 0; rb < nrows; rb += 32) {
 #pragma unroll
-              for (int q = 0; q < 4; ++q) c4[q] += sW[(r + q) * kWStride + t];
-            }
-            for (; r < w_hi; ++r) c4[0] += sW[r * kWStride + t];
-            const float acc = (c4[0] + c4[1]) + (c4[2] + c4[3]);
-            float* dst = a.col_out + (size_t)hx * a.n + j0 + t;
-            if (j0 + t < a.n) *dst = a.accumulate ? (*dst + acc) : acc;
-            float* dp = a.dpart + ((size_t)hx * a.nkt + kt) * 256;
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-              const int op = t + 128 * half;
-              // rows r' = r - w_lo with column c = r' + 127 - op inside [0, 128)
-              const int r_a = w_lo + max(0, op - 127), r_b = w_lo + min(R, op + 1);
-              float d4[4] = {0.f, 0.f, 0.f, 0.f};
-              int rr = r_a;
-              for (; rr + 4 <= r_b; rr += 4) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) d4[q] += sW[(rr + q) * kWStride + (rr + q - w_lo) + 127 - op];
+                for (int u = 0; u < 32; ++u) acc[u & 7] += sW[(rows0 + rb + u) * kWStride + rem];
               }
-              for (; rr < r_b; ++rr) d4[0] += sW[rr * kWStride + (rr - w_lo) + 127 - op];
-              dp[op] = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+              const float sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+              float* dst = a.col_out + (size_t)hx * a.n + kt0 + rem;
+              if (kt0 + rem < a.n) *dst = a.accumulate ? (*dst + sum) : sum;
+            } else {
+              const int op = rem - 128;
+              // row r holds this diagonal at column c = (r - w_lo) + 127 - op
+              for (int rb = 0; rb < nrows; rb += 32) {
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                  const int r = rows0 + rb + u;
+                  const int c = (r - w_lo) + 127 - op;
+                  if ((unsigned)c < 128u) acc[u & 7] += sW[r * kWStride + c];
+                }
+              }
+              const float sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+              a.dpart[((size_t)hx * a.nkt + kt) * 256 + op] = sum;
             }
           }
-          named_bar_sync(1, 128);
+          named_bar_sync(1, kTailSoft);
         }
       }
-      if (PASS == 1 && hh >= 0) {
-        a.stats[((size_t)hh * a.nchunks + chunk) * 128 + slane] = make_float2(m, ssum);
+      // pass-1 statistics per (row, chunk): the key half 1 thread hands its
+      // (max, sum) to the half 0 thread through the (idle) W buffer
+      if (PASS == 1) {
+        float2* xch = reinterpret_cast<float2*>(sW);
+        if (cpart) xch[t] = make_float2(m, ssum);
+        named_bar_sync(1, kTailSoft);
+        if (!cpart && hh >= 0) {
+          const float2 o = xch[t];
+          const float mn = fmaxf(m, o.x);
+          float sum = 0.f;
+          if (mn > -INFINITY) sum = ssum * fast_exp2(m - mn) + o.y * fast_exp2(o.x - mn);
+          a.stats[((size_t)hh * a.nchunks + chunk) * 128 + slane] = make_float2(mn, sum);
+        }
+        named_bar_sync(1, kTailSoft);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc(tbase, 256);
+  if (warp == 9) tmem_dealloc(tbase, 256);
 }
 
 // Merge the per-chunk (max2, sum) row statistics into log2-sum-exp: one warp per
@@ -315,6 +338,8 @@ __global__ void tail_merge_kernel(TailArgs a) {
   const int lane = threadIdx.x & 31;
   if (gw >= tail_count(a) * 128) return;
   const int hh = tail_head(a, gw / 128), t = gw % 128;
+  // only the lanes holding scored rows carry statistics
+  if (t < (a.paired ? 128 - (a.r_hi - a.r_lo) : a.r_lo - a.s0)) return;
   const float2* st = a.stats + (size_t)hh * a.nchunks * 128 + t;
   float m = -INFINITY, s = 0.f;
   for (int c = lane; c < a.nchunks; c += 32) {
