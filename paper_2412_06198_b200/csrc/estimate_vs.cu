@@ -10,9 +10,10 @@
 // Row statistics need every key before any weight is final, so the estimator
 // is two streaming passes over K (the second mostly L2-resident):
 //   pass 1: S = Q_tail K_tile^T in TMEM -> per-(row, chunk) online (max, sum)
-//   pass 2: merge the chunk stats, recompute S, w = exp2(s*c - lse2), then a
-//           skewed shared-memory transpose turns rows into column sums and
-//           per-tile diagonal partials; a final deterministic pass adds the
+//   pass 2: merge the chunk stats, recompute S^T (keys on TMEM lanes),
+//           w = exp2(s*c - lse2); each key's column sum is a register sum,
+//           the weights go to a skewed shared-memory buffer whose columns
+//           are the tile's diagonals; a final deterministic pass adds the
 //           (<= 3) per-tile partials of each diagonal in key order.
 // Work is split over (key-tile chunk, head); heads whose family != gate_val
 // exit at once, so one launch serves the device-selected VS heads of a layer.
@@ -61,13 +62,19 @@ struct TailArgs {
 // (cpart = warp / 4); warp 8: TMA producer; warp 9: MMA issuer
 constexpr int kTailThreads = 320;
 constexpr int kTailSoft = 256;
-constexpr int kWStride = 129;  // padded row stride of the W transpose buffer
 constexpr int kTailSmemQ = 0;
-constexpr int kTailKSlots = 4;          // 32 KB K tiles in flight (HBM latency in pass 2)
+constexpr int kTailKSlots = 4;  // barrier slots; pass 1 streams K through 4 x 32 KB, pass 2 through 2
 constexpr int kTailSmemK = 32768;
-constexpr int kTailSmemW = kTailSmemK + kTailKSlots * 32768;  // 128 x 129 floats
-constexpr int kTailSmemBar = kTailSmemW + 128 * kWStride * 4;
-constexpr int kTailSmemBytes = kTailSmemBar + 256 + 1024;
+// pass 1: K ring (4 slots) + a 1 KB statistics exchange; pass 2: K ring
+// (2 slots) + the skewed diagonal buffer D[128 rows][256 offsets] fp32 +
+// a 512 B column-sum exchange
+__host__ __device__ constexpr int tail_slots(int pass) { return pass == 1 ? 4 : 2; }
+__host__ __device__ constexpr int tail_smem_x(int pass) { return kTailSmemK + tail_slots(pass) * 32768; }
+constexpr int kDStride = 256;
+__host__ __device__ constexpr int tail_smem_bar(int pass) {
+  return tail_smem_x(pass) + (pass == 1 ? 1024 : 128 * kDStride * 4 + 512);
+}
+__host__ __device__ constexpr int tail_smem_bytes(int pass) { return tail_smem_bar(pass) + 256 + 1024; }
 
 enum TBar { T_Q = 0, T_QE, T_KF0, T_KE0 = T_KF0 + kTailKSlots, T_SF0 = T_KE0 + kTailKSlots, T_SF1,
             T_SE0, T_SE1, T_NUM };
@@ -100,8 +107,9 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
 
   uint8_t* sQ = smem + kTailSmemQ;
   uint8_t* sK = smem + kTailSmemK;
-  float* sW = reinterpret_cast<float*>(smem + kTailSmemW);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTailSmemBar);
+  constexpr int kSlots = tail_slots(PASS);
+  float* sX = reinterpret_cast<float*>(smem + tail_smem_x(PASS));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tail_smem_bar(PASS));
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + T_NUM);
   const int warp = warp_id();
 
@@ -124,31 +132,39 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
+  // Consecutive items of a CTA usually belong to the same unit (head pair):
+  // its Q box is loaded once and reused (qn counts Q loads; the MMA warp
+  // releases Q after the last item of the unit).
   if (warp == 8) {
     if (elect_one()) {
-      int jg = 0, it = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int2 un = unit_at(a, item / a.nchunks);
+      int jg = 0, qn = 0, prev_unit = -1;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int unit = item / a.nchunks;
+        const int2 un = unit_at(a, unit);
         const int chunk = item % a.nchunks;
         const int kt_lo = chunk * a.chunk_tiles;
         const int kt_hi = min(a.nkt, kt_lo + a.chunk_tiles);
         const int hh = un.x;
         const int hkv = (hh / a.heads) * a.kv_heads + (hh % a.heads) / (a.heads / a.kv_heads);
-        if (it > 0) mbar_wait(&bars[T_QE], (it - 1) & 1);  // previous item's MMAs have read Q
-        mbar_arrive_expect_tx(&bars[T_Q], 32768);
-        if (a.paired) {
-          const int hb = un.y >= 0 ? un.y : un.x;  // a lone head fills the B half (rows inactive)
-          tma_load_3d(sQ, &a.tmap_q, &bars[T_Q], 0, a.r_hi - 64, hh);
-          tma_load_3d(sQ + 8192, &a.tmap_q, &bars[T_Q], 0, a.r_hi - 64, hb);
-          tma_load_3d(sQ + 16384, &a.tmap_q, &bars[T_Q], 64, a.r_hi - 64, hh);
-          tma_load_3d(sQ + 24576, &a.tmap_q, &bars[T_Q], 64, a.r_hi - 64, hb);
-        } else {
-          tma_load_3d(sQ, &a.tmap_q, &bars[T_Q], 0, a.s0, hh);
-          tma_load_3d(sQ + 16384, &a.tmap_q, &bars[T_Q], 64, a.s0, hh);
+        if (unit != prev_unit) {
+          if (qn > 0) mbar_wait_backoff<64>(&bars[T_QE], (qn - 1) & 1);  // MMAs of the last unit have read Q
+          mbar_arrive_expect_tx(&bars[T_Q], 32768);
+          if (a.paired) {
+            const int hb = un.y >= 0 ? un.y : un.x;  // a lone head fills the B half (rows inactive)
+            tma_load_3d(sQ, &a.tmap_q, &bars[T_Q], 0, a.r_hi - 64, hh);
+            tma_load_3d(sQ + 8192, &a.tmap_q, &bars[T_Q], 0, a.r_hi - 64, hb);
+            tma_load_3d(sQ + 16384, &a.tmap_q, &bars[T_Q], 64, a.r_hi - 64, hh);
+            tma_load_3d(sQ + 24576, &a.tmap_q, &bars[T_Q], 64, a.r_hi - 64, hb);
+          } else {
+            tma_load_3d(sQ, &a.tmap_q, &bars[T_Q], 0, a.s0, hh);
+            tma_load_3d(sQ + 16384, &a.tmap_q, &bars[T_Q], 64, a.s0, hh);
+          }
+          ++qn;
+          prev_unit = unit;
         }
         for (int kt = kt_lo; kt < kt_hi; ++kt, ++jg) {
-          const int slot = jg % kTailKSlots;
-          if (jg >= kTailKSlots) mbar_wait(&bars[T_KE0 + slot], ((jg / kTailKSlots) - 1) & 1);
+          const int slot = jg % kSlots;
+          if (jg >= kSlots) mbar_wait_backoff<64>(&bars[T_KE0 + slot], ((jg / kSlots) - 1) & 1);
           uint8_t* dst = sK + slot * 32768;
           mbar_arrive_expect_tx(&bars[T_KF0 + slot], 32768);
           tma_load_3d(dst, &a.tmap_k, &bars[T_KF0 + slot], 0, kt * kTile, hkv);
@@ -160,32 +176,41 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, 128, 0, 0);
       const uint32_t q_addr = smem_u32(sQ);
-      int jg = 0, it = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      int jg = 0, qn = 0, prev_unit = -1;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int unit = item / a.nchunks;
         const int chunk = item % a.nchunks;
         const int kt_lo = chunk * a.chunk_tiles;
         const int kt_hi = min(a.nkt, kt_lo + a.chunk_tiles);
-        mbar_wait(&bars[T_Q], it & 1);
+        if (unit != prev_unit) {
+          mbar_wait_backoff<16>(&bars[T_Q], qn & 1);
+          ++qn;
+          prev_unit = unit;
+        }
         tc_fence_after();
         for (int kt = kt_lo; kt < kt_hi; ++kt, ++jg) {
-          const int slot = jg % kTailKSlots, sbuf = jg & 1;
-          mbar_wait(&bars[T_KF0 + slot], (jg / kTailKSlots) & 1);
-          if (jg >= 2) mbar_wait(&bars[T_SE0 + sbuf], ((jg >> 1) - 1) & 1);
+          const int slot = jg % kSlots, sbuf = jg & 1;
+          mbar_wait_backoff<16>(&bars[T_KF0 + slot], (jg / kSlots) & 1);
+          if (jg >= 2) mbar_wait_backoff<16>(&bars[T_SE0 + sbuf], ((jg >> 1) - 1) & 1);
           tc_fence_after();
           const uint32_t k_addr = smem_u32(sK + slot * 32768);
+          // pass 1: S (rows on TMEM lanes); pass 2: S^T (keys on lanes, rows on columns)
+          const uint32_t a_addr = PASS == 1 ? q_addr : k_addr, b_addr = PASS == 1 ? k_addr : q_addr;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            mma_ss(tbase + sbuf * 128, sdesc_sw128(q_addr + off, 16, 1024),
-                   sdesc_sw128(k_addr + off, 16, 1024), idesc, kk > 0 ? 1u : 0u);
+            mma_ss(tbase + sbuf * 128, sdesc_sw128(a_addr + off, 16, 1024),
+                   sdesc_sw128(b_addr + off, 16, 1024), idesc, kk > 0 ? 1u : 0u);
           }
           mma_commit(&bars[T_KE0 + slot]);
           mma_commit(&bars[T_SF0 + sbuf]);
         }
-        mma_commit(&bars[T_QE]);
+        const int nxt = item + (int)gridDim.x;
+        if (nxt >= n_items || nxt / a.nchunks != unit) mma_commit(&bars[T_QE]);  // last item of the unit
       }
     }
-  } else {
+  } else if (PASS == 1) {
+    // ---------------------------------------------------------- pass 1
     const int t = threadIdx.x & 127;  // TMEM lane = row of the MMA box
     const int cpart = warp >> 2;      // this thread's half of the row's 128 keys
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -194,7 +219,6 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
     // stats lane 64 + (t & 63); single -> row s0 + t, stats lane t
     const int i = a.paired ? a.r_hi - 64 + (t & 63) : a.s0 + t;
     const int slane = a.paired ? 64 + (t & 63) : t;
-    const int R = a.r_hi - a.r_lo;
     int jg = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int2 un = unit_at(a, item / a.nchunks);
@@ -203,8 +227,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
       const int chunk = item % a.nchunks;
       const int kt_lo = chunk * a.chunk_tiles;
       const int kt_hi = min(a.nkt, kt_lo + a.chunk_tiles);
-      float m = -INFINITY, ssum = 0.f, lse2 = 0.f;
-      if (PASS == 2 && active) lse2 = a.lse2[(size_t)hh * 128 + slane];
+      float m = -INFINITY, ssum = 0.f;
       for (int kt = kt_lo; kt < kt_hi; ++kt, ++jg) {
         const int slot = jg & 1;
         const int j0 = kt * kTile + 64 * cpart;  // first key of this thread's half
@@ -216,113 +239,174 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars[T_SE0 + slot]);
+        if (!active) continue;
         const int lim = i - j0;  // keep columns c <= lim
-        if (active && lim < 63) {  // causal cut (the diagonal tile only)
+        if (lim < 63) {  // causal cut (the diagonal tile only)
 #pragma unroll
           for (int c = 0; c < 2; ++c)
 #pragma unroll
             for (int u = 0; u < 32; ++u)
               if (32 * c + u > lim) s[c][u] = __float_as_uint(-INFINITY);
         }
-        if (PASS == 1) {
-          if (active) {
-            float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-            for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-              for (int u = 0; u < 32; u += 4) {
-                m4[2 * c] = fmax3(m4[2 * c], __uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1]));
-                m4[2 * c + 1] = fmax3(m4[2 * c + 1], __uint_as_float(s[c][u + 2]), __uint_as_float(s[c][u + 3]));
-              }
-            const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-            if (mx == -INFINITY) continue;  // no causal key of this row in the half tile
-            const float mn = fmaxf(m, mx * sl2);
-            const float2 sc2 = make_float2(sl2, sl2), mo2 = make_float2(-mn, -mn);
-            float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-              for (int u = 0; u < 32; u += 2) {
-                // (MUFU only: the scores feed a bit-exact top-k, keep them at ex2.approx accuracy)
-                float2 x = ffma2(make_float2(__uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1])), sc2, mo2);
-                x.x = fast_exp2(x.x);
-                x.y = fast_exp2(x.y);
-                acc[(u >> 1) & 1] = fadd2(acc[(u >> 1) & 1], x);
-              }
-            ssum = ssum * fast_exp2(m - mn) + (acc[0].x + acc[0].y + acc[1].x + acc[1].y);
-            m = mn;
+          for (int u = 0; u < 32; u += 4) {
+            m4[2 * c] = fmax3(m4[2 * c], __uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1]));
+            m4[2 * c + 1] = fmax3(m4[2 * c + 1], __uint_as_float(s[c][u + 2]), __uint_as_float(s[c][u + 3]));
           }
-        } else {
-          float* wrow = sW + t * kWStride + 64 * cpart;
-          const float2 sc2 = make_float2(sl2, sl2), mo2 = make_float2(-lse2, -lse2);
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        if (mx == -INFINITY) continue;  // no causal key of this row in the half tile
+        const float mn = fmaxf(m, mx * sl2);
+        const float2 sc2 = make_float2(sl2, sl2), mo2 = make_float2(-mn, -mn);
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int u = 0; u < 32; u += 2) {
-              float2 x = ffma2(make_float2(__uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1])), sc2, mo2);
-              x.x = fast_exp2(x.x);
-              x.y = fast_exp2(x.y);
-              wrow[32 * c + u] = active ? x.x : 0.f;
-              wrow[32 * c + u + 1] = active ? x.y : 0.f;
-            }
-          named_bar_sync(1, kTailSoft);
-          // reduction tasks per head half: 128 column sums (task c -> column
-          // j0 + c) and 256 diagonal partials (local offset op, elements at
-          // column c = (r - w_lo) + 127 - op); 256 threads stride over them
-          const int kt0 = kt * kTile;
-          const int nh = a.paired ? 2 : 1;
-#pragma unroll 1
-          for (int task = threadIdx.x; task < nh * 384; task += kTailSoft) {
-            const int hf = task / 384, rem = task % 384;
-            const int hx = hf ? un.y : un.x;
-            if (hx < 0) continue;
-            const int w_hi = a.paired ? 64 * hf + 64 : a.r_hi - a.s0;
-            const int w_lo = w_hi - R;
-            // every W row of the half is written (inactive rows as 0), so the
-            // sums run over all of them unconditionally, 32 independent loads
-            // per block (latency, not bandwidth, bounds this phase)
-            const int rows0 = a.paired ? 64 * hf : 0, nrows = a.paired ? 64 : 128;
-            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            if (rem < 128) {
-              for (int rb = 0; rb < nrows; rb += 32) {
-#pragma unroll
-                for (int u = 0; u < 32; ++u) acc[u & 7] += sW[(rows0 + rb + u) * kWStride + rem];
-              }
-              const float sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-              float* dst = a.col_out + (size_t)hx * a.n + kt0 + rem;
-              if (kt0 + rem < a.n) *dst = a.accumulate ? (*dst + sum) : sum;
-            } else {
-              const int op = rem - 128;
-              // row r holds this diagonal at column c = (r - w_lo) + 127 - op
-              for (int rb = 0; rb < nrows; rb += 32) {
-#pragma unroll
-                for (int u = 0; u < 32; ++u) {
-                  const int r = rows0 + rb + u;
-                  const int c = (r - w_lo) + 127 - op;
-                  if ((unsigned)c < 128u) acc[u & 7] += sW[r * kWStride + c];
-                }
-              }
-              const float sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-              a.dpart[((size_t)hx * a.nkt + kt) * 256 + op] = sum;
-            }
+          for (int u = 0; u < 32; u += 2) {
+            // (MUFU only: the scores feed a bit-exact top-k, keep them at ex2.approx accuracy)
+            float2 x = ffma2(make_float2(__uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1])), sc2, mo2);
+            x.x = fast_exp2(x.x);
+            x.y = fast_exp2(x.y);
+            acc[(u >> 1) & 1] = fadd2(acc[(u >> 1) & 1], x);
           }
-          named_bar_sync(1, kTailSoft);
+        ssum = ssum * fast_exp2(m - mn) + (acc[0].x + acc[0].y + acc[1].x + acc[1].y);
+        m = mn;
+      }
+      // statistics per (row, chunk): the key half 1 thread hands its (max, sum)
+      // to the half 0 thread
+      float2* xch = reinterpret_cast<float2*>(sX);
+      if (cpart) xch[t] = make_float2(m, ssum);
+      named_bar_sync(1, kTailSoft);
+      if (!cpart && hh >= 0) {
+        const float2 o = xch[t];
+        const float mn = fmaxf(m, o.x);
+        float sum = 0.f;
+        if (mn > -INFINITY) sum = ssum * fast_exp2(m - mn) + o.y * fast_exp2(o.x - mn);
+        a.stats[((size_t)hh * a.nchunks + chunk) * 128 + slane] = make_float2(mn, sum);
+      }
+      named_bar_sync(1, kTailSoft);
+    }
+  } else {
+    // ---------------------------------------------------------- pass 2
+    // S^T in TMEM: lane = key j0 + t of the tile, column = row of the Q box.
+    // Thread (t, half hf = warp / 4) owns key t against the box rows
+    // [64 hf, 64 hf + 64).  w = exp2(s * c - lse2[row]) with lse2 = +inf on rows
+    // that are not scored (w = 0); the column sum of key t is a register sum;
+    // the diagonal partials go through D[row][op] (skewed so a diagonal is a
+    // column of D, op = (row - w_lo) + 127 - t) and are summed per column.
+    const int t = threadIdx.x & 127;
+    const int hf = warp >> 2;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const float sl2 = a.scale_log2;
+    const int R = a.r_hi - a.r_lo;
+    // the box rows of this half: row r = 64 hf + rl (rl < 64), global row i(r)
+    const int ibase = a.paired ? a.r_hi - 64 : a.s0 + 64 * hf;  // global row of rl = 0
+    const int w_hi = a.paired ? 64 * hf + 64 : a.r_hi - a.s0;  // box rows of the scored window
+    const int w_lo = w_hi - R;
+    const int rl_lo = max(0, w_lo - 64 * hf);  // scored rl of this half: [rl_lo, rl_hi)
+    const int rl_hi = min(64, w_hi - 64 * hf);
+    float* sD = sX;
+    float* sC = sX + 128 * kDStride;  // [128] column-sum exchange (single-head units)
+    int jg = 0, cur_unit = -1;
+    float nl[64];
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int2 un = unit_at(a, item / a.nchunks);
+      const int hx = a.paired ? (hf ? un.y : un.x) : un.x;
+      const int chunk = item % a.nchunks;
+      const int kt_lo = chunk * a.chunk_tiles;
+      const int kt_hi = min(a.nkt, kt_lo + a.chunk_tiles);
+      // -lse2 per row of this half (registers, reloaded when the unit
+      // changes), -inf -> w = 0 for unscored rows
+      if (item / a.nchunks != cur_unit) {
+        cur_unit = item / a.nchunks;
+        const int sl0 = a.paired ? 64 : 64 * hf;  // stats lane of rl = 0
+        const float* src = a.lse2 + (size_t)max(hx, 0) * 128 + sl0;
+#pragma unroll
+        for (int rl = 0; rl < 64; rl += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(src + rl);
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            nl[rl + q] = (hx >= 0 && rl + q >= rl_lo && rl + q < rl_hi) ? -vv[q] : -INFINITY;
         }
       }
-      // pass-1 statistics per (row, chunk): the key half 1 thread hands its
-      // (max, sum) to the half 0 thread through the (idle) W buffer
-      if (PASS == 1) {
-        float2* xch = reinterpret_cast<float2*>(sW);
-        if (cpart) xch[t] = make_float2(m, ssum);
-        named_bar_sync(1, kTailSoft);
-        if (!cpart && hh >= 0) {
-          const float2 o = xch[t];
-          const float mn = fmaxf(m, o.x);
-          float sum = 0.f;
-          if (mn > -INFINITY) sum = ssum * fast_exp2(m - mn) + o.y * fast_exp2(o.x - mn);
-          a.stats[((size_t)hh * a.nchunks + chunk) * 128 + slane] = make_float2(mn, sum);
+      for (int kt = kt_lo; kt < kt_hi; ++kt, ++jg) {
+        const int slot = jg & 1;
+        const int j = kt * kTile + t;  // this thread's key
+        mbar_wait(&bars[T_SF0 + slot], (jg >> 1) & 1);
+        tc_fence_after();
+        uint32_t s[2][32];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) tmem_ld32(tbase + lane_off + slot * 128 + 64 * hf + 32 * c, s[c]);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&bars[T_SE0 + slot]);
+        // causal: row rl sees key j iff ibase + rl >= j, i.e. rl >= j - ibase
+        const int rl_causal = j - ibase;
+        const float2 sc2 = make_float2(sl2, sl2);
+        float2 cs = make_float2(0.f, 0.f);
+        float w[64];
+        const bool cut = __any_sync(0xffffffffu, rl_causal > 0);  // only tiles at the scored rows
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int u = 0; u < 32; u += 2) {
+            const int rl = 32 * c + u;
+            float2 x = ffma2(make_float2(__uint_as_float(s[c][u]), __uint_as_float(s[c][u + 1])), sc2,
+                             make_float2(nl[rl], nl[rl + 1]));
+            x.x = fast_exp2(x.x);
+            x.y = fast_exp2(x.y);
+            if (cut) {
+              x.x = rl >= rl_causal ? x.x : 0.f;
+              x.y = rl + 1 >= rl_causal ? x.y : 0.f;
+            }
+            cs = fadd2(cs, x);
+            w[rl] = x.x;
+            w[rl + 1] = x.y;
+          }
+        named_bar_sync(1, kTailSoft);  // the previous tile's D readers are done
+        // D[r][op], op = (r - w_lo) + 127 - t for the scored rows r of this half
+#pragma unroll
+        for (int rl = 0; rl < 64; ++rl) {
+          const int r = 64 * hf + rl;
+          if (rl >= rl_lo && rl < rl_hi) sD[r * kDStride + (r - w_lo) + 127 - t] = w[rl];
         }
+        const float csum = cs.x + cs.y;
+        if (!a.paired && hf) sC[t] = csum;
         named_bar_sync(1, kTailSoft);
+        const int kt0 = kt * kTile;
+        if (a.paired) {
+          if (hx >= 0 && j < a.n) {
+            float* dst = a.col_out + (size_t)hx * a.n + j;
+            *dst = a.accumulate ? (*dst + csum) : csum;
+          }
+        } else if (!hf && hx >= 0 && j < a.n) {
+          const float tot = csum + sC[t];
+          float* dst = a.col_out + (size_t)hx * a.n + j;
+          *dst = a.accumulate ? (*dst + tot) : tot;
+        }
+        // diagonal partials: (unit half, op) tasks, op < R + 127, over the D rows
+        // [r_a, r_b) holding them; 32 independent predicated loads per block
+        const int nh = a.paired ? 2 : 1;
+        const int nop = R + 127;
+#pragma unroll 1
+        for (int task = threadIdx.x; task < nh * nop; task += kTailSoft) {
+          const int uh = task / nop, op = task % nop;
+          const int ux = a.paired ? (uh ? un.y : un.x) : un.x;
+          if (ux < 0) continue;
+          const int wl = a.paired ? 64 * uh + 64 - R : w_lo;  // w_lo of that half's frame
+          const int r_a = wl + max(0, op - 127), r_b = wl + min(R, op + 1);
+          float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          for (int rb = r_a; rb < r_b; rb += 32) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+              if (rb + u < r_b) acc[u & 7] += sD[(rb + u) * kDStride + op];
+          }
+          a.dpart[((size_t)ux * a.nkt + kt) * 256 + op] =
+              ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        }
       }
     }
   }
@@ -500,8 +584,8 @@ int launch_score_tail(int batch, int heads, int kv_heads, int n, float scale, co
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tail_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemBytes);
-    cudaFuncSetAttribute(tail_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemBytes);
+    cudaFuncSetAttribute(tail_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem_bytes(1));
+    cudaFuncSetAttribute(tail_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem_bytes(2));
     attr = true;
   }
   static int num_sms = [] {
@@ -511,11 +595,11 @@ int launch_score_tail(int batch, int heads, int kv_heads, int n, float scale, co
     return v;
   }();
   const int grid = std::min(num_sms, a.hh_total * a.nchunks);
-  tail_kernel<1><<<grid, kTailThreads, kTailSmemBytes, st>>>(a);
+  tail_kernel<1><<<grid, kTailThreads, tail_smem_bytes(1), st>>>(a);
   if ((rc = check_launch("tail_kernel<1>"))) return rc;
   tail_merge_kernel<<<(a.hh_total * 128 * 32 + 255) / 256, 256, 0, st>>>(a);
   if ((rc = check_launch("tail_merge_kernel"))) return rc;
-  tail_kernel<2><<<grid, kTailThreads, kTailSmemBytes, st>>>(a);
+  tail_kernel<2><<<grid, kTailThreads, tail_smem_bytes(2), st>>>(a);
   if ((rc = check_launch("tail_kernel<2>"))) return rc;
   dim3 g2((n + 255) / 256, a.hh_total);
   diag_combine_kernel<<<g2, 256, 0, st>>>(a.dpart, diag_out, n, a.nkt, r_lo, r_hi - r_lo,
