@@ -86,7 +86,8 @@ typedef struct {
                             estimator, [3] tile lists, [4] attention, [5] unused */
   int64_t out_ld;        /* elements between output rows; 0 = heads * 128 (the
                             (B, L, H*d) layout of runtime.py:194).  A larger
-                            value writes a head group into a wider layer output. */
+                            value writes a head group into a wider layer output;
+                            must be a multiple of 8 (16-byte output rows). */
 } sa_prefill_desc;
 
 /* Device views into a prefill workspace (valid after sa_prefill). */

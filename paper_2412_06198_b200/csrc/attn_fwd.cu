@@ -61,6 +61,7 @@ struct AttnArgs {
   unsigned long long* prof;  // SA_ATTN_PROF builds: per-role phase cycle counters [3 * 16]
   int* counter;              // optional work-item counter (zeroed before launch): dynamic fetch
   const int32_t* n_work;     // optional device count of `work` entries (default hh_total * nqt)
+  int st256;                 // output rows 32-byte aligned: 256-bit stores
 };
 
 constexpr int kThreads = 192;
@@ -513,9 +514,14 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 #pragma unroll
           for (int t = 0; t < 16; ++t)
             pk[t] = pack_bf16(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
-          uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
+          if (a.st256) {  // 32-byte stores: whole L2 sectors per lane
 #pragma unroll
-          for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+            for (int t = 0; t < 2; ++t) st_global_v8(orow + 32 * c + 16 * t, pk + 8 * t);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+          }
         }
       }
       if (valid && a.lse != nullptr) a.lse[(size_t)hh * a.n + i] = (m_used + log2f(l)) * 0.69314718055994531f;
@@ -568,6 +574,9 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   a.out = reinterpret_cast<__nv_bfloat16*>(out);
   a.out_row_stride = out_ld > 0 ? out_ld : (long long)heads * kHeadDim;
   a.out_batch_stride = (long long)n * a.out_row_stride;
+  if (a.out_row_stride % 8 != 0 || (reinterpret_cast<uintptr_t>(out) & 15) != 0)
+    return fail(SA_ERR_DIMENSION, "output rows must be 16-byte aligned (out_ld %% 8 == 0)");
+  a.st256 = (a.out_row_stride % 16 == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0) ? 1 : 0;
   a.n = n;
   a.heads = heads;
   a.kv_heads = kv_heads;

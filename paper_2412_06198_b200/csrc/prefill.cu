@@ -89,6 +89,8 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
   if (!(d->scale > 0.f) || !std::isfinite(d->scale)) return fail(SA_ERR_DIMENSION, "bad scale");
   if (d->out_ld != 0 && d->out_ld < (int64_t)d->heads * kHeadDim)
     return fail(SA_ERR_DIMENSION, "out_ld=%lld is below heads * 128", (long long)d->out_ld);
+  if (d->out_ld % 8 != 0)
+    return fail(SA_ERR_DIMENSION, "out_ld=%lld must be a multiple of 8 (16-byte rows)", (long long)d->out_ld);
   memset(p, 0, sizeof(*p));
   const int n = d->n;
   p->hh = d->batch * d->heads;
