@@ -54,12 +54,13 @@ __global__ void block_pool_kernel(const __nv_bfloat16* __restrict__ x, int G, in
   const uint2* src = reinterpret_cast<const uint2*>(x + ((long long)g * n + r0) * kHeadDim) + lane;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
   int r = r0;
-  for (; r + 4 <= r1; r += 4) {
-    uint2 v[4];
+  // 8 row loads in flight per lane (a whole b = 8 block: 2 KB per warp)
+  for (; r + 8 <= r1; r += 8) {
+    uint2 v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = __ldg(src + (size_t)(r - r0 + u) * (kHeadDim / 4));
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (size_t)(r - r0 + u) * (kHeadDim / 4));
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const __nv_bfloat162 lo2 = *reinterpret_cast<const __nv_bfloat162*>(&v[u].x);
       const __nv_bfloat162 hi2 = *reinterpret_cast<const __nv_bfloat162*>(&v[u].y);
       acc[0] += __low2float(lo2);
