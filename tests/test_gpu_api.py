@@ -399,3 +399,32 @@ def test_prefill_plan_graph_replay(sa):
     plan.run(q, k, v, ref, ws)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("extra", [8, 16])
+def test_out_ld_row_layouts(sa, extra):
+    """desc.out_ld wider than heads * 128: rows 16-byte aligned only (extra = 8,
+    16-byte stores) or 32-byte aligned (extra = 16, 256-bit stores) give the
+    same columns as the packed layout; out_ld % 8 != 0 is rejected."""
+    from paper_2412_06198_b200 import runtime as R
+
+    H, HK, n = 4, 2, 700
+    q, k, v = O.synth_qkv_gqa(9, n, H, HK, 128)
+    q, k, v = (torch.from_numpy(O.bf16_round(x[0])).bfloat16().cuda() for x in (q, k, v))
+    plan = R.PrefillPlan(1, H, HK, n, 128, "fixed", fixed_pattern=sa.VerticalSlash(40, 50))
+    ws = R._workspace(plan.ws_bytes, q.device)
+    ref = torch.empty((1, n, H * 128), dtype=torch.bfloat16, device="cuda")
+    plan.run(q, k, v, ref, ws)
+    ld = H * 128 + extra
+    wide = torch.zeros((1, n, ld), dtype=torch.bfloat16, device="cuda")
+    plan.desc.out_ld = ld
+    try:
+        plan.run(q, k, v, wide, ws)
+        torch.cuda.synchronize()
+        assert torch.equal(wide[..., : H * 128], ref)
+        assert not wide[..., H * 128:].any()
+        plan.desc.out_ld = ld + 4
+        with pytest.raises(sa.SparseAttnError):
+            plan.run(q, k, v, wide, ws)
+    finally:
+        plan.desc.out_ld = 0
