@@ -187,6 +187,16 @@ int sa_build_tiles(const sa_head_index* index, int hh_total, int n, int32_t* til
  * the item with the r-th largest tile count (longest-processing-time first).
  * No reference counterpart: the reference runs heads serially (runtime.py:174). */
 int sa_order_work(const int32_t* tile_cnt, int items, int max_cnt, int32_t* work, void* stream);
+/* One decode step (reference runtime.py:209-242 decode_step): the new token's
+ * queries q [batch * heads, d] fp32 attend densely over the first n rows of a
+ * KV cache laid out [batch, kv_heads, capacity, d] (kv_dtype 0 = fp32,
+ * 1 = bf16), out [batch * heads, d] fp32.  Split-K over 256-key chunks, K/V
+ * read in place once per kv head; ws >= sa_decode_workspace(...). */
+size_t sa_decode_workspace(int batch, int heads, int kv_heads, int n, int d);
+int sa_decode_attn(int batch, int heads, int kv_heads, int n, int d, int capacity, float scale, const float* q,
+                   const void* k_cache, const void* v_cache, int kv_dtype, float* out, void* ws, size_t ws_bytes,
+                   void* stream);
+
 int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float scale, const void* q,
                    const void* k, const void* v, void* out, const sa_head_index* index,
                    const int32_t* tile_off, const int32_t* tile_cnt, const uint32_t* tiles,

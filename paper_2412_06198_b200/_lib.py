@@ -113,6 +113,8 @@ _SIGNATURES = {
     "sa_build_tiles": (ctypes.c_int, [_IDX, _I, _I, _P, _P, _P, _P]),
     "sa_check_finite_bf16": (ctypes.c_int, [_P, _LL, _P, _P]),
     "sa_memcpy2d_async": (ctypes.c_int, [_P, _SZ, _P, _SZ, _SZ, _SZ, _P]),
+    "sa_decode_workspace": (_SZ, [_I, _I, _I, _I, _I]),
+    "sa_decode_attn": (ctypes.c_int, [_I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _I, _P, _P, _SZ, _P]),
     "sa_order_work": (ctypes.c_int, [_P, _I, _I, _P, _P]),
     "sa_attn_sparse": (ctypes.c_int, [_I, _I, _I, _I, _F, _P, _P, _P, _P, _IDX, _P, _P, _P, _P,
                                       _P]),

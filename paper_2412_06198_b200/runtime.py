@@ -543,11 +543,8 @@ def _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window
 def decode_step(q_new, k_new, v_new, cache: KvCache, cfg: ModelConfig) -> DecodeResult:
     """Append one token's k/v and attend its query over the whole cache (runtime.py:209-242).
 
-    Decode is outside the prefill hot path.  It reuses the tcgen05
-    attention kernel with a dense causal index whose tile list holds only the
-    last query tile of each head; the new query sits at row n - 1."""
-    from . import device_index as DI
-
+    Decode is outside the prefill hot path: a split-K CUDA-core
+    kernel (csrc/decode.cu) reads the cache's K/V in place once per kv head."""
     batch, length, kv_heads = _check_qkv(q_new, k_new, v_new, cfg)
     if length != 1:
         raise DimensionError(f"decode consumes exactly one token, got length {length}")
@@ -557,28 +554,19 @@ def decode_step(q_new, k_new, v_new, cache: KvCache, cfg: ModelConfig) -> Decode
     cache.append(k_new, v_new)
     n = cache.length
     H, d = cfg.n_heads, cfg.d_head
-    hh = batch * H
-    qd = D.stage_heads(_flat(q_new, hh, 1, d), "q")
-    dev = qd.device
-    qfull = torch.zeros((hh, n, D.HEAD_DIM), dtype=torch.bfloat16, device=dev)
-    qfull[:, n - 1] = qd[:, 0]
-    kd = D.stage_heads(cache._k[:, :, :n].reshape(batch * kv_heads, n, d), "k")
-    vd = D.stage_heads(cache._v[:, :, :n].reshape(batch * kv_heads, n, d), "v")
-    b = DI.HostIndexBuilder(n, hh)
-    idx = b.upload(dev)  # every head dense
-    nqt = DI.num_qtiles(n)
-    cnt = torch.zeros((hh, nqt), dtype=torch.int32)
-    cnt[:, nqt - 1] = nqt
-    off = torch.zeros((hh, nqt), dtype=torch.int32)
-    off[:, nqt - 1] = torch.arange(hh, dtype=torch.int32) * nqt
-    tiles = torch.arange(nqt, dtype=torch.int32).repeat(hh)
-    tiles.view(hh, nqt)[:, nqt - 1] |= 1 << 28  # diagonal tile: causal mask
-    cnt, off, tiles = cnt.to(dev), off.to(dev), tiles.to(dev)
-    out = torch.empty((batch, n, H * D.HEAD_DIM), dtype=torch.bfloat16, device=dev)
-    _lib.call("sa_attn_sparse", batch, H, kv_heads, n, 1.0 / math.sqrt(d), qfull.data_ptr(), kd.data_ptr(),
-              vd.data_ptr(), out.data_ptr(), idx.view(), off.data_ptr(), cnt.data_ptr(), tiles.data_ptr(),
-              None, D.stream())
-    y = out[:, n - 1:n].reshape(batch, 1, H, D.HEAD_DIM)[..., :d].reshape(batch, 1, H * d)
+    dev = cache._k.device
+    qt = torch.as_tensor(q_new) if not D.is_torch(q_new) else q_new
+    q32 = qt.to(device=dev, dtype=torch.float32).reshape(batch * H, d).contiguous()
+    kc, vc, cap = cache._k, cache._v, cache.capacity
+    if kc.dtype not in (torch.float32, torch.bfloat16):  # other cache dtypes: a converted copy
+        kc, vc, cap = kc[:, :, :n].float().contiguous(), vc[:, :, :n].float().contiguous(), n
+    out = torch.empty((batch * H, d), dtype=torch.float32, device=dev)
+    nbytes = int(_lib.load().sa_decode_workspace(batch, H, kv_heads, n, d))
+    ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+    _lib.call("sa_decode_attn", batch, H, kv_heads, n, d, cap, 1.0 / math.sqrt(d), q32.data_ptr(),
+              kc.data_ptr(), vc.data_ptr(), 0 if kc.dtype == torch.float32 else 1, out.data_ptr(),
+              ws.data_ptr(), ws.numel(), D.stream())
+    y = out.reshape(batch, 1, H * d)
     output = D.to_host_or_keep(y, q_new)
     torch.cuda.synchronize()
     return DecodeResult(output=output, cache=cache, elapsed_s=time.perf_counter() - t0)

@@ -3,6 +3,8 @@
 with the bf16 tolerances of the north star, plus the reference-generated
 golden prefill cases (tests/golden/)."""
 
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -428,3 +430,27 @@ def test_out_ld_row_layouts(sa, extra):
             plan.run(q, k, v, wide, ws)
     finally:
         plan.desc.out_ld = 0
+
+
+@pytest.mark.parametrize("H,HK,d,n,dt", [(8, 2, 128, 3000, "bf16"), (4, 4, 5, 300, "f32"), (32, 8, 128, 9000, "bf16"),
+                                         (16, 1, 64, 700, "f32")])
+def test_decode_step_split_k(sa, H, HK, d, n, dt):
+    """decode_step (split-K kernel over the cache, in place) equals dense
+    attention of the last row: both GQA and MHA, bf16 and fp32 caches, odd
+    head_dim, query heads per kv head above one pass (16)."""
+    rng = np.random.default_rng(n + d)
+    q, k, v = (rng.uniform(-1, 1, (1, h, n, d)).astype(np.float32) for h in (H, HK, HK))
+    if dt == "bf16":
+        q, k, v = (torch.from_numpy(x).bfloat16().cuda() for x in (q, k, v))
+    else:
+        q, k, v = (torch.from_numpy(x).cuda() for x in (q, k, v))
+    cfg = sa.ModelConfig(n_heads=H, d_model=H * d, d_head=d, max_context=n + 8)
+    part = sa.prefill(q[:, :, : n - 1], k[:, :, : n - 1], v[:, :, : n - 1], cfg, mode="dense")
+    dec = sa.decode_step(q[:, :, n - 1:], k[:, :, n - 1:], v[:, :, n - 1:], part.cache, cfg)
+    assert dec.cache.length == n
+    g = H // HK
+    kf, vf = k[0].float().repeat_interleave(g, 0), v[0].float().repeat_interleave(g, 0)
+    s = torch.einsum("hd,hjd->hj", q[0, :, n - 1].float(), kf) / math.sqrt(d)
+    want = torch.einsum("hj,hjd->hd", torch.softmax(s.double(), 1).float(), vf).reshape(1, 1, H * d)
+    err = (dec.output.float() - want).abs()
+    assert err.max().item() <= MAX_ABS and err.mean().item() <= MEAN_ABS, (err.max().item(), err.mean().item())
