@@ -279,8 +279,13 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # SA_DIST_BACKEND=gloo lets ranks share one GPU (a dry run of the N > 1 path)
+        backend = os.environ.get("SA_DIST_BACKEND", "nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", torch.cuda.current_device())
     if HK % world != 0:
         raise SystemExit(f"--gpus {world} must divide the {HK} kv heads")
@@ -317,6 +322,15 @@ def run_ours(args):
     ws = R._workspace(plan.ws_bytes, dev)
     out = torch.empty((1, n, h_l * D), dtype=torch.bfloat16, device=dev)
     final = torch.empty((n, H * D), dtype=torch.bfloat16, device=dev) if world > 1 else None
+    # N > 1: the load-balanced layer (multigpu.BalancedLayer) is the timed step;
+    # SA_MG_BALANCED=0 times the plain GQA-group sharding + output all-gather
+    balanced = world > 1 and os.environ.get("SA_MG_BALANCED", "1") != "0"
+    layer = None
+    if balanced:
+        from paper_2412_06198_b200.multigpu import BalancedLayer
+
+        qf, kf, vf = (torch.from_numpy(np.ascontiguousarray(x)).bfloat16().to(dev) for x in (q, k, v))
+        layer = BalancedLayer(rank, world, H, HK, n, D, mode, fixed_pattern=fixed, device=dev)
 
     def step(events=None):
         if events is not None:
@@ -330,7 +344,7 @@ def run_ours(args):
         if events is not None:
             for i in range(5):
                 plan.desc.stage_events[i] = None
-        if world > 1:
+        if world > 1 and not balanced:
             gather_heads(out[0], world, out=final)
         if events is not None:
             events[6].record()
@@ -338,13 +352,17 @@ def run_ours(args):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    # the timed steps replay a CUDA graph of selection + layer (PrefillPlan.graph)
-    graph = plan.graph(qd, kd, vd, out, ws)
+    if balanced:
+        def gstep():
+            layer.step(qf, kf, vf)
+    else:
+        # the timed steps replay a CUDA graph of selection + layer (PrefillPlan.graph)
+        graph = plan.graph(qd, kd, vd, out, ws)
 
-    def gstep():
-        graph.replay()
-        if world > 1:
-            gather_heads(out[0], world, out=final)
+        def gstep():
+            graph.replay()
+            if world > 1:
+                gather_heads(out[0], world, out=final)
 
     for _ in range(2):
         gstep()
@@ -390,10 +408,25 @@ def run_ours(args):
     nqt = view.nqt
     cnt = R._wrap(view.tile_cnt, plan.hh * nqt, torch.int32).cpu().numpy()
     exec_tiles = int(cnt.sum())
+    if balanced:  # this rank's attention launch covers its dealt items of every head
+        from paper_2412_06198_b200.multigpu import _view
+
+        cf = _view(layer.ws_full, layer.vf.tile_cnt, layer.items, torch.int32)
+        exec_tiles = int(cf[layer.mine.long()].sum().item())
     exec_flops = exec_tiles * 4.0 * 128 ** 3
     plans = plan.plans(ws, with_search=False)
     fams = [type(hp.pattern).__name__ if hp.pattern is not None else "dense" for hp in plans[0]]
     attn_ms = float(stage_ms[4])
+    if balanced:  # the attention launch of this rank's dealt items, CUDA events on its stream
+        ts = []
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            layer.attend(qf, kf, vf)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        attn_ms = float(np.mean(ts))
     peak, peak_sus, hbm, peak_kind = measured_peaks()
     achieved = exec_flops / (attn_ms * 1e-3) / 1e12
     if world > 1:
@@ -452,10 +485,14 @@ def run_ours(args):
             "data": "synthetic (uniform [-1,1], rng([seed, ctx]) GQA draw, bf16)",
             "config": {"workload": f"llama3-8b-attn-layer-{n // 1024}k-{args.mode}", "heads": H, "kv_heads": HK,
                        "head_dim": D, "seq_len": n, "batch": 1, "mode": args.mode,
-                       "parallelism": f"head-parallel x{world} + NCCL all-gather" if world > 1 else "single GPU",
+                       "parallelism": (f"balanced head-parallel x{world}: per-group estimation, index all-gather, "
+                                       f"heaviest-first (head, q-tile) deal, output-block all-gather") if balanced else
+                                      (f"head-parallel x{world} + NCCL all-gather" if world > 1 else "single GPU"),
                        "l2": l2_note(n),
-                       "launch": "timed steps replay a CUDA graph of selection + layer (PrefillPlan.graph); "
-                                 "stage_ms from eager steps with stage events",
+                       "launch": ("eager balanced steps (BalancedLayer.step); stage_ms from eager steps of this "
+                                  "rank's GQA-group plan with stage events") if balanced else
+                                 ("timed steps replay a CUDA graph of selection + layer (PrefillPlan.graph); "
+                                  "stage_ms from eager steps with stage events"),
                        "families_rank0": fam_counts},
             "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),

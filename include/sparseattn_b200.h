@@ -88,6 +88,9 @@ typedef struct {
                             (B, L, H*d) layout of runtime.py:194).  A larger
                             value writes a head group into a wider layer output;
                             must be a multiple of 8 (16-byte output rows). */
+  int32_t stop_after_tiles; /* 1 = selection, estimators and tile lists only (no
+                               attention): the realised index of these heads,
+                               e.g. for exchange between ranks (multigpu.py) */
 } sa_prefill_desc;
 
 /* Device views into a prefill workspace (valid after sa_prefill). */
@@ -201,6 +204,14 @@ int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float scale, const
                    const void* k, const void* v, void* out, const sa_head_index* index,
                    const int32_t* tile_off, const int32_t* tile_cnt, const uint32_t* tiles,
                    float* lse, void* stream);
+/* sa_attn_sparse over an explicit work list: items work[0 .. *n_work) (device
+ * int32, item = (b * heads + h) * nqt + query tile) in that order; other query
+ * tiles are not written.  `counter` is one device int32 of scratch per
+ * concurrent call.  Used by the balanced head-parallel path (multigpu.py). */
+int sa_attn_sparse_work(int batch, int heads, int kv_heads, int n, float scale, const void* q, const void* k,
+                        const void* v, void* out, const sa_head_index* index, const int32_t* tile_off,
+                        const int32_t* tile_cnt, const uint32_t* tiles, const int32_t* work,
+                        const int32_t* n_work, int32_t* counter, long long out_ld, void* stream);
 
 #ifdef __cplusplus
 }

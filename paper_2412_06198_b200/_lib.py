@@ -65,6 +65,7 @@ class sa_prefill_desc(ctypes.Structure):
         ("preselected", ctypes.c_int32),
         ("stage_events", ctypes.c_void_p * 6),
         ("out_ld", ctypes.c_int64),
+        ("stop_after_tiles", ctypes.c_int32),
     ]
 
 
@@ -113,6 +114,8 @@ _SIGNATURES = {
     "sa_build_tiles": (ctypes.c_int, [_IDX, _I, _I, _P, _P, _P, _P]),
     "sa_check_finite_bf16": (ctypes.c_int, [_P, _LL, _P, _P]),
     "sa_memcpy2d_async": (ctypes.c_int, [_P, _SZ, _P, _SZ, _SZ, _SZ, _P]),
+    "sa_attn_sparse_work": (ctypes.c_int, [_I, _I, _I, _I, _F, _P, _P, _P, _P, _IDX, _P, _P, _P, _P, _P, _P,
+                                           ctypes.c_int64, _P]),
     "sa_decode_workspace": (_SZ, [_I, _I, _I, _I, _I]),
     "sa_decode_attn": (ctypes.c_int, [_I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _I, _P, _P, _SZ, _P]),
     "sa_order_work": (ctypes.c_int, [_P, _I, _I, _P, _P]),

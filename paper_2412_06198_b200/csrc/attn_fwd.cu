@@ -637,3 +637,14 @@ extern "C" int sa_attn_sparse(int batch, int heads, int kv_heads, int n, float s
   return sa::launch_attn(batch, heads, kv_heads, n, scale, q, k, v, out, index, tile_off, tile_cnt,
                          tiles, nullptr, lse, reinterpret_cast<cudaStream_t>(stream));
 }
+
+extern "C" int sa_attn_sparse_work(int batch, int heads, int kv_heads, int n, float scale, const void* q,
+                                   const void* k, const void* v, void* out, const sa_head_index* index,
+                                   const int32_t* tile_off, const int32_t* tile_cnt, const uint32_t* tiles,
+                                   const int32_t* work, const int32_t* n_work, int32_t* counter, long long out_ld,
+                                   void* stream) {
+  // the persistent kernel fetches items through `counter` (zeroed on the stream)
+  if (!work || !n_work || !counter) return sa::fail(SA_ERR_DIMENSION, "null work list or counter");
+  return sa::launch_attn(batch, heads, kv_heads, n, scale, q, k, v, out, index, tile_off, tile_cnt, tiles, work,
+                         nullptr, reinterpret_cast<cudaStream_t>(stream), out_ld, counter, n_work);
+}

@@ -357,6 +357,7 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   // 4. executed tiles + attention
   if ((rc = sa_build_tiles(&V.index, p.hh, n, V.tile_off, V.tile_cnt, V.tiles, stream))) return rc;
   mark(3);
+  if (desc->stop_after_tiles) return SA_OK;
   // longest-first CTA order over the non-empty items (SA_ATTN_ORDER=0 keeps
   // the kernel's kv-group-major default, for A/B)
   static const bool lpt = [] {

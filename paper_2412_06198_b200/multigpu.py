@@ -8,6 +8,7 @@ the reference's (B, n, H*d) layout (runtime.py:194).
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -38,3 +39,165 @@ def gather_heads(local: torch.Tensor, world: int, group=None, out: torch.Tensor 
         dist.all_gather(parts, local.contiguous(), group=group)
         out.view(n, world, w).copy_(torch.stack(parts, 1))
     return out
+
+
+# ---------------------------------------------------------------- balanced layer
+def _view(buf: torch.Tensor, ptr: int, count: int, dtype) -> torch.Tensor:
+    """`count` elements of `dtype` at device pointer `ptr` inside `buf` (uint8)."""
+    esize = torch.empty(0, dtype=dtype).element_size()
+    off = ptr - buf.data_ptr()
+    if off < 0 or off + count * esize > buf.numel():
+        raise RuntimeError("pointer outside the workspace")
+    return buf[off: off + count * esize].view(dtype)
+
+
+class BalancedLayer:
+    """Head-parallel prefill of one layer with load-balanced attention.
+
+    Sharding whole kv groups leaves the ranks that own the vertical-slash heads
+    with most of the executed tiles.  Here each rank
+    (1) runs selection, estimators and tile lists for its own GQA group of
+    heads (`stop_after_tiles`), (2) exchanges the compact realised index of
+    those heads with every rank (one all-gather, ~tens of KB per head), (3)
+    rebuilds the tile lists of all heads, orders every (head, query tile) item
+    by executed tiles (stable, so identical on every rank) and deals them out
+    in a snake over the ranks, (4) runs the attention kernel on its items only
+    (`sa_attn_sparse_work`, Q/K/V of all heads resident on every rank), and
+    (5) all-gathers the produced 128-row output blocks into the reference
+    (n, H*d) layout.  The exchanges are methods so a single-GPU test can play
+    every rank in turn (tests/test_gpu_multigpu_sim.py)."""
+
+    def __init__(self, rank: int, world: int, heads: int, kv_heads: int, n: int, d: int, mode: str,
+                 fixed_pattern=None, device=None):
+        from . import runtime as R
+
+        self.rank, self.world = rank, world
+        self.H, self.HK, self.n, self.d = heads, kv_heads, n, d
+        self.q_sl, self.kv_sl = shard_heads(rank, world, heads, kv_heads)
+        self.h_l = heads // world
+        dev = torch.device("cuda") if device is None else device
+        self.local = R.PrefillPlan(1, self.h_l, kv_heads // world, n, d, mode, fixed_pattern=fixed_pattern)
+        self.local.desc.stop_after_tiles = 1
+        self.full = R.PrefillPlan(1, heads, kv_heads, n, d, mode, fixed_pattern=fixed_pattern)
+        self.ws_local = torch.empty(self.local.ws_bytes, dtype=torch.uint8, device=dev)
+        self.ws_full = torch.empty(self.full.ws_bytes, dtype=torch.uint8, device=dev)
+        self.vl = self.local.views(self.ws_local)
+        self.vf = self.full.views(self.ws_full)
+        if mode == "auto":
+            fams = [c.family for c in list(self.full.desc.full)[: self.full.desc.ncand]]
+        elif mode == "fixed":
+            fams = [self.full.desc.fixed.family]
+        else:
+            fams = []
+        self.any_block = 2 in fams
+        self.words = self.vf.index.vs_words
+        self.row_stride = self.vf.index.blk_row_stride
+        self.head_stride = int(self.vf.blk_head_stride)
+        self.nqt = (n + 127) // 128
+        self.items = heads * self.nqt
+        self.per = -(-self.items // world)  # block slots per rank in the output exchange
+        self.counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        # snake deal of the heaviest-first item order: rank r takes the positions
+        # p with owner(p) == r (fixed per shape, so no host sync per step)
+        p = np.arange(self.items)
+        lap, pos = p // world, p % world
+        owner = np.where(lap % 2 == 0, pos, world - 1 - pos)
+        self.positions = [torch.from_numpy(p[owner == r]).to(dev) for r in range(world)]
+        self.n_mine = torch.tensor([len(self.positions[rank])], dtype=torch.int32, device=dev)
+        self.out = torch.zeros((self.nqt * 128, heads * d), dtype=torch.bfloat16, device=dev)
+
+    # -- index fields of `nh` heads starting at head `h0` of a plan's views
+    def _fields(self, ws, view, h0: int, nh: int):
+        idx = view.index
+        i32 = torch.int32
+        f = [_view(ws, idx.family, h0 + nh, i32)[h0:], _view(ws, idx.tri_window, h0 + nh, i32)[h0:],
+             _view(ws, idx.tri_sinks, h0 + nh, i32)[h0:], _view(ws, idx.blk_b, h0 + nh, i32)[h0:],
+             _view(ws, idx.colbits, (h0 + nh) * self.words, i32)[h0 * self.words:],
+             _view(ws, idx.diagrev, (h0 + nh) * self.words, i32)[h0 * self.words:],
+             _view(ws, idx.blk_row_off, (h0 + nh) * self.row_stride, i32)[h0 * self.row_stride:]]
+        if self.any_block:
+            f.append(_view(ws, idx.blk_idx, (h0 + nh) * self.head_stride, i32)[h0 * self.head_stride:])
+        return f
+
+    def estimate(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+        """(1): this rank's heads; q/k/v hold every head (H|HK, n, 128).
+        Returns the packed index of this rank's heads (int32, same size on every rank)."""
+        ql, kl, vl = q[self.q_sl], k[self.kv_sl], v[self.kv_sl]
+        if self.local.mode == "auto":
+            self.local.select(ql, kl, self.ws_local)
+        self.local.run(ql, kl, vl, self.out, self.ws_local)  # stops after the tile lists
+        return torch.cat([x.reshape(-1) for x in self._fields(self.ws_local, self.vl, 0, self.h_l)])
+
+    def load_index(self, gathered: torch.Tensor) -> None:
+        """(2)-(3): `gathered` = the world's packed indices [world, L]; rebuild all tile lists."""
+        from . import _lib
+        from . import _device as Dv
+
+        for r in range(self.world):
+            pos = 0
+            dst = self._fields(self.ws_full, self.vf, r * self.h_l, self.h_l)
+            for i, x in enumerate(dst):
+                m = x.numel()
+                src = gathered[r, pos: pos + m]
+                if i == 6:  # row offsets are absolute into blk_idx: rebase by the head offset
+                    src = src + r * self.h_l * self.head_stride
+                x.copy_(src)
+                pos += m
+        _lib.call("sa_build_tiles", self.vf.index, self.H, self.n, self.vf.tile_off, self.vf.tile_cnt,
+                  self.vf.tiles, Dv.stream())
+        cnt = _view(self.ws_full, self.vf.tile_cnt, self.items, torch.int32)
+        order = torch.argsort(-cnt.long(), stable=True)  # stable: the same on every rank
+        self.owner_items = [order[pos].to(torch.int32) for pos in self.positions]
+        self.mine = self.owner_items[self.rank].contiguous()
+
+    def attend(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+        """(4): attention for this rank's items; returns its output blocks [per, 128, d]."""
+        from . import _lib
+        from . import _device as Dv
+
+        _lib.call("sa_attn_sparse_work", 1, self.H, self.HK, self.n, self.full.scale, q.data_ptr(), k.data_ptr(),
+                  v.data_ptr(), self.out.data_ptr(), self.vf.index, self.vf.tile_off, self.vf.tile_cnt,
+                  self.vf.tiles, self.mine.data_ptr(), self.n_mine.data_ptr(), self.counter.data_ptr(), 0,
+                  Dv.stream())
+        return self._pack(self.mine)
+
+    def _blocks(self, out):
+        return out.view(self.nqt, 128, self.H, self.d)
+
+    def _pack(self, items):
+        o4 = self._blocks(self.out)
+        buf = torch.zeros((self.per, 128, self.d), dtype=self.out.dtype, device=self.out.device)
+        hh, qt = items.long() // self.nqt, items.long() % self.nqt
+        buf[: items.numel()] = o4[qt, :, hh, :]
+        return buf
+
+    def assemble(self, gathered: torch.Tensor, final: torch.Tensor | None = None) -> torch.Tensor:
+        """(5): `gathered` = every rank's blocks [world, per, 128, d] -> (n, H*d)."""
+        if final is None:
+            final = torch.empty((self.nqt * 128, self.H * self.d), dtype=self.out.dtype, device=self.out.device)
+        f4 = self._blocks(final)
+        for r, items in enumerate(self.owner_items):
+            hh, qt = items.long() // self.nqt, items.long() % self.nqt
+            f4[qt, :, hh, :] = gathered[r, : items.numel()]
+        return final[: self.n]
+
+    @staticmethod
+    def _all_gather(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
+        """[world, *x.shape]: NCCL on device; gloo (tests, ranks sharing one GPU) through host copies."""
+        if dist.get_backend(group) == "nccl":
+            out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+            dist.all_gather_into_tensor(out, x.contiguous(), group=group)
+            return out
+        h = x.detach().cpu()
+        if h.dtype == torch.bfloat16:  # gloo has no bf16: move the bits as fp16 (a byte copy)
+            parts = [torch.empty_like(h.view(torch.float16)) for _ in range(world)]
+            dist.all_gather(parts, h.view(torch.float16).contiguous(), group=group)
+            return torch.stack(parts).view(torch.bfloat16).to(x.device)
+        parts = [torch.empty_like(h) for _ in range(world)]
+        dist.all_gather(parts, h.contiguous(), group=group)
+        return torch.stack(parts).to(x.device)
+
+    def step(self, q, k, v, group=None) -> torch.Tensor:
+        """One layer on this rank (all-gathers between the phases)."""
+        self.load_index(self._all_gather(self.estimate(q, k, v), self.world, group))
+        return self.assemble(self._all_gather(self.attend(q, k, v), self.world, group))
