@@ -30,6 +30,25 @@ namespace sa {
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Per-thread, per-device side stream and fork / join events (created on the
+// first call that needs them; the warm-up run before a graph capture does).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream* side_stream() {
+  static thread_local SideStream tab[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& x = tab[dev & 15];
+  if (!x.s) {
+    cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+  }
+  return &x;
+}
+
 struct Layout {
   size_t off[32];
   size_t total;
@@ -289,14 +308,30 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
     apply_choice_kernel<<<(p.hh + 127) / 128, 128, 0, st>>>(a);
     if ((rc = check_launch("apply_choice_kernel"))) return rc;
   }
-  auto mark = [&](int e) {
-    if (desc->stage_events[e]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(desc->stage_events[e]), st);
+  auto mark_on = [&](int e, cudaStream_t s) {
+    if (desc->stage_events[e]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(desc->stage_events[e]), s);
   };
+  auto mark = [&](int e) { mark_on(e, st); };
   mark(0);
+  // The VS and Block-Cluster estimators only share the per-head choice: with
+  // both present the VS chain (latency-bound, few CTAs) runs on a side stream
+  // beside the block GEMM (fork / join through events, graph-capturable).
+  // SA_OVERLAP_EST=0 keeps them serial.
+  static const bool overlap = [] {
+    const char* e = getenv("SA_OVERLAP_EST");
+    return !(e && e[0] == '0');
+  }();
+  SideStream* side = (overlap && p.any_vs && p.any_block) ? side_stream() : nullptr;
+  cudaStream_t vs_st = st;
+  if (side) {
+    cudaEventRecord(side->fork, st);
+    cudaStreamWaitEvent(side->s, side->fork, 0);
+    vs_st = side->s;
+  }
   // 2. vertical-slash estimator + stable top-k into bitmaps
   if (p.any_vs) {
-    cudaMemsetAsync(const_cast<uint32_t*>(V.index.colbits), 0, (size_t)p.hh * p.vs_words * 4, st);
-    cudaMemsetAsync(const_cast<uint32_t*>(V.index.diagrev), 0, (size_t)p.hh * p.vs_words * 4, st);
+    cudaMemsetAsync(const_cast<uint32_t*>(V.index.colbits), 0, (size_t)p.hh * p.vs_words * 4, vs_st);
+    cudaMemsetAsync(const_cast<uint32_t*>(V.index.diagrev), 0, (size_t)p.hh * p.vs_words * 4, vs_st);
     // estimated scoring over the last q_est rows, in groups of <= 128 rows
     const int r_first = n - p.q_est;
     for (int g = 0; g < p.tail_groups; ++g) {
@@ -304,7 +339,7 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
       const int r_lo = std::max(r_first, r_hi - 128);
       if ((rc = launch_score_tail(B, H, HK, n, desc->scale, q, k, r_lo, r_hi, V.col_scores,
                                   V.diag_scores, g > 0, V.family, SA_VERTICAL_SLASH,
-                                  b + L.off[W_TAIL], p.tail_ws, st)))
+                                  b + L.off[W_TAIL], p.tail_ws, vs_st)))
         return rc;
     }
     for (int c = 0; c < p.ncand; ++c) {
@@ -333,10 +368,10 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
       t.bits2 = const_cast<uint32_t*>(V.index.diagrev);
       t.bit_base2 = n + 127;
       t.bit_neg2 = 1;
-      if ((rc = launch_topk(t, st))) return rc;
+      if ((rc = launch_topk(t, vs_st))) return rc;
     }
   }
-  mark(1);
+  mark_on(1, vs_st);
   // 3. block estimator
   if (p.any_block) {
     for (int c = 0; c < p.ncand; ++c) {
@@ -352,6 +387,10 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
                                     p.blk_row_stride, gate, gval, b + L.off[W_BLKWS], p.blk_ws, st)))
         return rc;
     }
+  }
+  if (side) {  // join: the tile lists need both indexes
+    cudaEventRecord(side->join, vs_st);
+    cudaStreamWaitEvent(st, side->join, 0);
   }
   mark(2);
   // 4. executed tiles + attention
