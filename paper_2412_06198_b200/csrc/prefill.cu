@@ -34,7 +34,7 @@ static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 // first call that needs them; the warm-up run before a graph capture does).
 struct SideStream {
   cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork0 = nullptr, kdone = nullptr, fork = nullptr, join = nullptr;
 };
 static SideStream* side_stream() {
   static thread_local SideStream tab[16];
@@ -43,6 +43,8 @@ static SideStream* side_stream() {
   SideStream& x = tab[dev & 15];
   if (!x.s) {
     cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&x.fork0, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.kdone, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
   }
@@ -278,6 +280,24 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   const int n = p.n;
   const int B = desc->batch, H = desc->heads, HK = desc->kv_heads;
 
+  // The single Block-Cluster candidate's key pooling needs only K: it runs on
+  // the side stream from the start, beside the selector.
+  static const bool overlap = [] {
+    const char* e = getenv("SA_OVERLAP_EST");
+    return !(e && e[0] == '0');
+  }();
+  int nblk = 0, blk_c = -1;
+  for (int c = 0; c < p.ncand; ++c)
+    if (p.cand[c].family == SA_BLOCK_SPARSE) ++nblk, blk_c = c;
+  SideStream* side = (overlap && p.any_block && (p.any_vs || nblk == 1)) ? side_stream() : nullptr;
+  const bool kpool_early = side && nblk == 1;
+  if (kpool_early) {
+    cudaEventRecord(side->fork0, st);
+    cudaStreamWaitEvent(side->s, side->fork0, 0);
+    if ((rc = launch_block_pool(p.hk, n, p.cand[blk_c].p1, 1, k, b + L.off[W_KP], nullptr, nullptr, 0, side->s)))
+      return rc;
+    cudaEventRecord(side->kdone, side->s);
+  }
   // 1. per-head choice
   int32_t* choice = nullptr;
   if (desc->mode == SA_MODE_AUTO && desc->preselected) {
@@ -314,16 +334,12 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   auto mark = [&](int e) { mark_on(e, st); };
   mark(0);
   // The VS and Block-Cluster estimators only share the per-head choice: with
-  // both present the VS chain (latency-bound, few CTAs) runs on a side stream
+  // both present the VS chain (latency-bound, few CTAs) runs on the side stream
   // beside the block GEMM (fork / join through events, graph-capturable).
-  // SA_OVERLAP_EST=0 keeps them serial.
-  static const bool overlap = [] {
-    const char* e = getenv("SA_OVERLAP_EST");
-    return !(e && e[0] == '0');
-  }();
-  SideStream* side = (overlap && p.any_vs && p.any_block) ? side_stream() : nullptr;
+  // SA_OVERLAP_EST=0 keeps everything on the caller's stream.
   cudaStream_t vs_st = st;
-  if (side) {
+  const bool vs_side = side && p.any_vs;
+  if (vs_side) {
     cudaEventRecord(side->fork, st);
     cudaStreamWaitEvent(side->s, side->fork, 0);
     vs_st = side->s;
@@ -380,7 +396,11 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
       const int32_t* gate = choice ? choice : V.family;
       const int gval = choice ? c : SA_BLOCK_SPARSE;
       if ((rc = launch_block_pool(p.hh, n, bs, 0, q, b + L.off[W_QP], nullptr, gate, gval, st))) return rc;
-      if ((rc = launch_block_pool(p.hk, n, bs, 1, k, b + L.off[W_KP], nullptr, nullptr, 0, st))) return rc;
+      if (kpool_early) {
+        cudaStreamWaitEvent(st, side->kdone, 0);
+      } else if ((rc = launch_block_pool(p.hk, n, bs, 1, k, b + L.off[W_KP], nullptr, nullptr, 0, st))) {
+        return rc;
+      }
       if ((rc = launch_block_select(B, H, HK, n, bs, kb, desc->scale, b + L.off[W_QP],
                                     b + L.off[W_KP], const_cast<int32_t*>(V.index.blk_idx),
                                     p.blk_head_stride, const_cast<int32_t*>(V.index.blk_row_off),
@@ -388,8 +408,8 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
         return rc;
     }
   }
-  if (side) {  // join: the tile lists need both indexes
-    cudaEventRecord(side->join, vs_st);
+  if (side) {  // join the side stream (the tile lists need every index)
+    cudaEventRecord(side->join, side->s);
     cudaStreamWaitEvent(st, side->join, 0);
   }
   mark(2);
