@@ -493,7 +493,9 @@ def run_ours(args):
                                   "rank's GQA-group plan with stage events") if balanced else
                                  ("timed steps replay a CUDA graph of selection + layer (PrefillPlan.graph); "
                                   "stage_ms from eager steps with stage events"),
-                       "families_rank0": fam_counts},
+                       "families_rank0": fam_counts,
+                       "stage_note": "the VS and block estimator chains overlap on two streams: vs_estimator = "
+                                     "selection end -> VS chain end, block_estimator = the rest of the block chain"},
             "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                          "frac_sustained": round(achieved / peak_sus, 4), "peak_kind": peak_kind,
