@@ -432,14 +432,15 @@ def test_out_ld_row_layouts(sa, extra):
         plan.desc.out_ld = 0
 
 
-@pytest.mark.parametrize("H,HK,d,n,dt", [(8, 2, 128, 3000, "bf16"), (4, 4, 5, 300, "f32"), (32, 8, 128, 9000, "bf16"),
-                                         (16, 1, 64, 700, "f32")])
-def test_decode_step_split_k(sa, H, HK, d, n, dt):
+@pytest.mark.parametrize("H,HK,d,n,dt,B", [(8, 2, 128, 3000, "bf16", 1), (4, 4, 5, 300, "f32", 1),
+                                           (32, 8, 128, 9000, "bf16", 1), (16, 1, 64, 700, "f32", 1),
+                                           (8, 4, 128, 1000, "bf16", 3)])
+def test_decode_step_split_k(sa, H, HK, d, n, dt, B):
     """decode_step (split-K kernel over the cache, in place) equals dense
     attention of the last row: both GQA and MHA, bf16 and fp32 caches, odd
     head_dim, query heads per kv head above one pass (16)."""
     rng = np.random.default_rng(n + d)
-    q, k, v = (rng.uniform(-1, 1, (1, h, n, d)).astype(np.float32) for h in (H, HK, HK))
+    q, k, v = (rng.uniform(-1, 1, (B, h, n, d)).astype(np.float32) for h in (H, HK, HK))
     if dt == "bf16":
         q, k, v = (torch.from_numpy(x).bfloat16().cuda() for x in (q, k, v))
     else:
@@ -449,8 +450,8 @@ def test_decode_step_split_k(sa, H, HK, d, n, dt):
     dec = sa.decode_step(q[:, :, n - 1:], k[:, :, n - 1:], v[:, :, n - 1:], part.cache, cfg)
     assert dec.cache.length == n
     g = H // HK
-    kf, vf = k[0].float().repeat_interleave(g, 0), v[0].float().repeat_interleave(g, 0)
-    s = torch.einsum("hd,hjd->hj", q[0, :, n - 1].float(), kf) / math.sqrt(d)
-    want = torch.einsum("hj,hjd->hd", torch.softmax(s.double(), 1).float(), vf).reshape(1, 1, H * d)
+    kf, vf = k.float().repeat_interleave(g, 1), v.float().repeat_interleave(g, 1)
+    s = torch.einsum("bhd,bhjd->bhj", q[:, :, n - 1].float(), kf) / math.sqrt(d)
+    want = torch.einsum("bhj,bhjd->bhd", torch.softmax(s.double(), 2).float(), vf).reshape(B, 1, H * d)
     err = (dec.output.float() - want).abs()
     assert err.max().item() <= MAX_ABS and err.mean().item() <= MEAN_ABS, (err.max().item(), err.mean().item())
