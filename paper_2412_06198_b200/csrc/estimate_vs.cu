@@ -15,8 +15,9 @@
 //           the weights go to a skewed shared-memory buffer whose columns
 //           are the tile's diagonals; a final deterministic pass adds the
 //           (<= 3) per-tile partials of each diagonal in key order.
-// Work is split over (key-tile chunk, head); heads whose family != gate_val
-// exit at once, so one launch serves the device-selected VS heads of a layer.
+// Work is split over (unit = one head or a GQA pair of heads, key-tile chunk)
+// of a device-built list of the heads whose family == gate_val, so one launch
+// serves the device-selected VS heads of a layer.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -58,8 +59,9 @@ struct TailArgs {
   const int32_t* unit_count;  // device count of units
 };
 
-// warps 0-7: two per TMEM lane quarter, each row's 128 keys split in halves
-// (cpart = warp / 4); warp 8: TMA producer; warp 9: MMA issuer
+// warps 0-7: two per TMEM lane quarter (pass 1: warp / 4 = half of each row's
+// 128 keys; pass 2: warp / 4 = which half of the box's rows, keys on lanes);
+// warp 8: TMA producer; warp 9: MMA issuer
 constexpr int kTailThreads = 320;
 constexpr int kTailSoft = 256;
 constexpr int kTailSmemQ = 0;
