@@ -348,3 +348,32 @@ def test_block_top1_ties_and_overflow(sa, case):
     want = O.block_index(q.astype(np.float64), k.astype(np.float64), b, 1).block_rows
     for g, (r_got, r_want) in enumerate(zip(got, want)):
         assert r_got == r_want.tolist(), (g, r_got, r_want.tolist())
+
+
+@pytest.mark.parametrize("gain", [6.0, 25.0])
+def test_attention_large_logits(sa, gain):
+    """Logits far from O(1) (q, k scaled up: row maxima jump by hundreds in
+    log2 units within a row): the lazy rescale (stale max until it grows by
+    > 2^8) must keep every family within tolerance of the fp64 oracle."""
+    from paper_2412_06198_b200 import device_index as DI
+
+    H, HK, n = 4, 1, 700
+    q = O.bf16_round(rand_heads(71, H, n) * gain)
+    k = O.bf16_round(rand_heads(72, HK, n) * gain)
+    v = rand_heads(73, HK, n)
+    b = DI.HostIndexBuilder(n, H)
+    rng = np.random.default_rng(9)
+    cols = np.sort(rng.choice(n, 60, replace=False))
+    offs = np.sort(rng.choice(n, 50, replace=False))
+    idxs = [O.tri_index(n, n, 0), O.tri_index(n, 97, 5), O.Index(n, cols, offs),
+            O.block_index(q[3].astype(np.float64), k[0].astype(np.float64), 8, 3)]
+    b.set_dense(0)
+    b.set_triangular(1, 97, 5)
+    b.set_vertical_slash(2, cols, offs)
+    b.set_block(3, 8, [r.astype(np.int32) for r in idxs[3].block_rows])
+    got, _ = run_index(sa, q, k, v, b, H, HK)
+    for h in range(H):
+        want = O.masked_attention(q[h].astype(np.float64), k[0].astype(np.float64), v[0].astype(np.float64), idxs[h])
+        err = np.abs(got[h] - want)
+        assert np.isfinite(got[h]).all()
+        assert err.max() <= MAX_ABS and err.mean() <= MEAN_ABS, (h, err.max(), err.mean())
