@@ -119,19 +119,26 @@ struct BlockScoreArgs {
 };
 
 constexpr int kBsThreads = 192;
-constexpr int kBsSmemA = 0;        // 6 x 16 KB query operand
-constexpr int kBsSmemB = 98304;    // 4 x 32 KB key-chunk ring (two key tiles in flight)
-constexpr int kBsSmemBar = 229376;
-constexpr int kBsSmemBytes = kBsSmemBar + 256 + 1024;
+// Two CTAs per SM (one's prologue and epilogue under the other's MMAs):
+//   A: [qhi d0-63 | qhi d64-127 | qlo d0-63 | qlo d64-127], 4 x 16 KB (the
+//      third product reuses qhi, so the 384-wide operand's last third is not
+//      loaded);
+//   B: a ring of 3 x 16 KB key chunks, per key tile in the order khi d0, klo d0,
+//      khi d1, klo d1, each released right after its MMAs:
+//      (qhi.khi + qlo.khi) on a khi chunk, qhi.klo on a klo chunk.
+constexpr int kBsSmemA = 0;
+constexpr int kBsSmemB = 65536;
+constexpr int kBsRing = 3;
+constexpr int kBsSmemBar = kBsSmemB + kBsRing * 16384;  // 114688
+constexpr int kBsSmemBytes = kBsSmemBar + 256;            // base must be 1024-aligned
 
-enum BBar { BB_A = 0, BB_KF0, BB_KF1, BB_KF2, BB_KF3, BB_KE0, BB_KE1, BB_KE2, BB_KE3, BB_SF0, BB_SF1, BB_SE0, BB_SE1, BB_NUM };
+enum BBar { BB_A = 0, BB_KF0, BB_KE0 = BB_KF0 + kBsRing, BB_SF0 = BB_KE0 + kBsRing, BB_SF1, BB_SE0, BB_SE1, BB_NUM };
 
 template <int K, bool FUSED>
-__global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid_constant__ BlockScoreArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  // 1024-aligned offset into the dynamic shared array (pointer arithmetic on
-  // smem_raw keeps the shared address space, so accesses compile to LDS/STS)
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+__global__ void __launch_bounds__(kBsThreads, 2) block_score_kernel(const __grid_constant__ BlockScoreArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem) & 1023u) != 0u) __trap();  // SWIZZLE_128B tiles need 1024-byte alignment
   // grid (heads, query tiles): every head's heaviest tile is dispatched first
   const int hh = a.hh_base + blockIdx.x;
   if (a.gate && a.gate[hh] != a.gate_val) return;
@@ -148,7 +155,7 @@ __global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[BB_A], 1);
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < kBsRing; ++s) {
       mbar_init(&bars[BB_KF0 + s], 1);
       mbar_init(&bars[BB_KE0 + s], 1);
     }
@@ -166,16 +173,16 @@ __global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid
 
   if (warp == 4) {
     if (elect_one()) {
-      mbar_arrive_expect_tx(&bars[BB_A], 98304);
-      for (int c = 0; c < 6; ++c) tma_load_3d(sA + c * 16384, &a.tmap_qp, &bars[BB_A], 64 * c, qt * kTile, hh);
+      mbar_arrive_expect_tx(&bars[BB_A], 65536);
+      for (int c = 0; c < 4; ++c) tma_load_3d(sA + c * 16384, &a.tmap_qp, &bars[BB_A], 64 * c, qt * kTile, hh);
+      // key chunks of tile j at ring positions 4 j + c: khi d0, klo d0, khi d1, klo d1
+      constexpr int kCol[4] = {0, 128, 64, 192};
       for (int j = 0; j < cnt; ++j) {
-        for (int c = 0; c < 2; ++c) {  // c = 0: khi, c = 1: klo
-          const int slot = 2 * (j & 1) + c;
-          if (j >= 2) mbar_wait(&bars[BB_KE0 + slot], ((j >> 1) - 1) & 1);
-          uint8_t* dst = sB + slot * 32768;
-          mbar_arrive_expect_tx(&bars[BB_KF0 + slot], 32768);
-          tma_load_3d(dst, &a.tmap_kp, &bars[BB_KF0 + slot], 128 * c, j * kTile, hkv);
-          tma_load_3d(dst + 16384, &a.tmap_kp, &bars[BB_KF0 + slot], 128 * c + 64, j * kTile, hkv);
+        for (int c = 0; c < 4; ++c) {
+          const int g = 4 * j + c, slot = g % kBsRing;
+          if (g >= kBsRing) mbar_wait(&bars[BB_KE0 + slot], ((g / kBsRing) - 1) & 1);
+          mbar_arrive_expect_tx(&bars[BB_KF0 + slot], 16384);
+          tma_load_3d(sB + slot * 16384, &a.tmap_kp, &bars[BB_KF0 + slot], kCol[c], j * kTile, hkv);
         }
       }
     }
@@ -187,24 +194,22 @@ __global__ void __launch_bounds__(kBsThreads, 1) block_score_kernel(const __grid
       for (int j = 0; j < cnt; ++j) {
         const int buf = j & 1;
         if (j >= 2) mbar_wait(&bars[BB_SE0 + buf], ((j >> 1) - 1) & 1);
-        // passes: (A chunk 0 = qhi, khi), (A chunk 1 = qlo, khi), (A chunk 2 = qhi, klo)
-        for (int pass = 0; pass < 3; ++pass) {
-          const int c = pass < 2 ? 0 : 1;
-          const int slot = 2 * (j & 1) + c;
-          if (pass != 1) {
-            mbar_wait(&bars[BB_KF0 + slot], (j >> 1) & 1);
-            tc_fence_after();
-          }
-          const uint32_t b_addr = smem_u32(sB + slot * 32768);
+        for (int c = 0; c < 4; ++c) {
+          const int g = 4 * j + c, slot = g % kBsRing;
+          const int dh = c >> 1;           // d-half of this chunk
+          const bool lo = (c & 1) != 0;    // klo chunk
+          mbar_wait(&bars[BB_KF0 + slot], (g / kBsRing) & 1);
+          tc_fence_after();
+          const uint32_t b_addr = smem_u32(sB + slot * 16384);
+          // khi chunk: qhi.khi then qlo.khi; klo chunk: qhi.klo
+          for (int pass = 0; pass < (lo ? 1 : 2); ++pass) {
+            const uint32_t a_chunk = a_addr + (pass ? 32768u : 0u) + dh * 16384u;
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const int ka = 8 * pass + kk;  // k-step over the 384-wide A
-            const uint32_t aoff = (ka >> 2) * 16384 + (ka & 3) * 32;
-            const uint32_t boff = (kk >> 2) * 16384 + (kk & 3) * 32;
-            mma_ss(tbase + buf * 128, sdesc_sw128(a_addr + aoff, 16, 1024),
-                   sdesc_sw128(b_addr + boff, 16, 1024), idesc, (pass > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk)
+              mma_ss(tbase + buf * 128, sdesc_sw128(a_chunk + kk * 32, 16, 1024), sdesc_sw128(b_addr + kk * 32, 16, 1024),
+                     idesc, (c > 0 || pass > 0 || kk > 0) ? 1u : 0u);
           }
-          if (pass != 0) mma_commit(&bars[BB_KE0 + slot]);
+          mma_commit(&bars[BB_KE0 + slot]);
         }
         mma_commit(&bars[BB_SF0 + buf]);
       }
