@@ -38,63 +38,58 @@ namespace sa {
 constexpr int kSplitQ = 384;  // query operand [hi | lo | hi]
 constexpr int kSplitKey = 256;  // key operand [hi | lo]
 
-// One warp per (group, block): lane l pools d = 4l .. 4l+3 over the block's
-// rows with 8-byte loads (a 256-byte coalesced row per warp step), fp32 sums.
+// One half-warp per (group, block): lane l pools d = 8 (l % 16) .. + 7 over the
+// block's rows in order (fp32, like np.add.reduceat) with 16-byte loads (a
+// coalesced 256-byte row per half-warp step, 8 rows in flight).
 // out: side 0 -> [G, nb, 384] = [hi | lo | hi]; side 1 -> [G, nb, 256] = [hi | lo].
 __global__ void block_pool_kernel(const __nv_bfloat16* __restrict__ x, int G, int n, int b,
                                   int side, __nv_bfloat16* __restrict__ out, float* mean_out,
                                   const int32_t* gate, int gate_val) {
   const int nb = (n + b - 1) / b;
-  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // (g, block)
-  const int lane = threadIdx.x & 31;
+  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4;  // (g, block)
+  const int hl = threadIdx.x & 15;
   if (gid >= (long long)G * nb) return;
   const int g = (int)(gid / nb), blk = (int)(gid % nb);
   if (gate && gate[g] != gate_val) return;
   const int r0 = blk * b, r1 = min(n, r0 + b);
-  const uint2* src = reinterpret_cast<const uint2*>(x + ((long long)g * n + r0) * kHeadDim) + lane;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  int r = r0;
-  // 8 row loads in flight per lane (a whole b = 8 block: 2 KB per warp)
-  for (; r + 8 <= r1; r += 8) {
-    uint2 v[8];
+  const uint4* src = reinterpret_cast<const uint4*>(x + ((long long)g * n + r0) * kHeadDim) + hl;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  auto add = [&](const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (size_t)(r - r0 + u) * (kHeadDim / 4));
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const __nv_bfloat162 lo2 = *reinterpret_cast<const __nv_bfloat162*>(&v[u].x);
-      const __nv_bfloat162 hi2 = *reinterpret_cast<const __nv_bfloat162*>(&v[u].y);
-      acc[0] += __low2float(lo2);
-      acc[1] += __high2float(lo2);
-      acc[2] += __low2float(hi2);
-      acc[3] += __high2float(hi2);
+    for (int i = 0; i < 4; ++i) {
+      const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      acc[2 * i] += f2.x;
+      acc[2 * i + 1] += f2.y;
     }
-  }
-  for (; r < r1; ++r) {
-    const uint2 v = __ldg(src + (size_t)(r - r0) * (kHeadDim / 4));
-    const __nv_bfloat162 lo2 = *reinterpret_cast<const __nv_bfloat162*>(&v.x);
-    const __nv_bfloat162 hi2 = *reinterpret_cast<const __nv_bfloat162*>(&v.y);
-    acc[0] += __low2float(lo2);
-    acc[1] += __high2float(lo2);
-    acc[2] += __low2float(hi2);
-    acc[3] += __high2float(hi2);
-  }
-  const float inv_cnt = 1.0f / (float)(r1 - r0);
-  __nv_bfloat16 hi[4], lo[4];
-  float mean[4];
+  };
+  int r = r0;
+  for (; r + 8 <= r1; r += 8) {
+    uint4 v[8];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (size_t)(r - r0 + u) * (kHeadDim / 8));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) add(v[u]);
+  }
+  for (; r < r1; ++r) add(__ldg(src + (size_t)(r - r0) * (kHeadDim / 8)));
+  const float inv_cnt = 1.0f / (float)(r1 - r0);
+  __nv_bfloat16 hi[8], lo[8];
+  float mean[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
     mean[u] = acc[u] * inv_cnt;
     hi[u] = __float2bfloat16_rn(mean[u]);
     lo[u] = __float2bfloat16_rn(mean[u] - __bfloat162float(hi[u]));
   }
   const int width = side == 0 ? kSplitQ : kSplitKey;
-  __nv_bfloat16* o = out + ((long long)g * nb + blk) * width + 4 * lane;
-  *reinterpret_cast<uint2*>(o) = *reinterpret_cast<uint2*>(hi);
-  *reinterpret_cast<uint2*>(o + 128) = *reinterpret_cast<uint2*>(lo);
-  if (side == 0) *reinterpret_cast<uint2*>(o + 256) = *reinterpret_cast<uint2*>(hi);
+  __nv_bfloat16* o = out + ((long long)g * nb + blk) * width + 8 * hl;
+  *reinterpret_cast<uint4*>(o) = *reinterpret_cast<uint4*>(hi);
+  *reinterpret_cast<uint4*>(o + 128) = *reinterpret_cast<uint4*>(lo);
+  if (side == 0) *reinterpret_cast<uint4*>(o + 256) = *reinterpret_cast<uint4*>(hi);
   if (mean_out) {
-    float* mo = mean_out + ((long long)g * nb + blk) * kHeadDim + 4 * lane;
+    float* mo = mean_out + ((long long)g * nb + blk) * kHeadDim + 8 * hl;
     *reinterpret_cast<float4*>(mo) = make_float4(mean[0], mean[1], mean[2], mean[3]);
+    *reinterpret_cast<float4*>(mo + 4) = make_float4(mean[4], mean[5], mean[6], mean[7]);
   }
 }
 
@@ -404,8 +399,8 @@ int launch_block_pool(int groups, int n, int b, int side, const void* x, void* s
   if (groups < 1 || n < 1) return fail(SA_ERR_DIMENSION, "bad pool shape");
   if (b < 1 || b > n) return fail(SA_ERR_PATTERN_PARAM, "b must be in [1, %d], got %d", n, b);
   const int nb = (n + b - 1) / b;
-  const long long items = (long long)groups * nb;  // one warp each
-  const long long grid = (items * 32 + 255) / 256;
+  const long long items = (long long)groups * nb;  // one half-warp each
+  const long long grid = (items * 16 + 255) / 256;
   block_pool_kernel<<<(unsigned)grid, 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), groups, n, b, side,
       reinterpret_cast<__nv_bfloat16*>(split_out), mean_out, gate, gate_val);
