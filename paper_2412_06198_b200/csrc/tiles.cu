@@ -9,6 +9,7 @@
 // always_diagonal (forced (i, i)).
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 
 #include "sa_types.h"
@@ -174,7 +175,19 @@ __global__ void __launch_bounds__(1024) order_work_kernel(const int32_t* __restr
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   start[t] = 0;
   __syncthreads();
-  for (int i = t; i < items; i += blockDim.x) atomicAdd(&start[order_bin(cnt[i], shift)], 1);
+  // counts are loaded 8 per thread before use (one memory latency per batch)
+  constexpr int kB = 8;
+  for (int i0 = t; i0 < items; i0 += kB * (int)blockDim.x) {
+    int c[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      c[u] = i < items ? __ldg(cnt + i) : INT_MIN;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+      if (c[u] != INT_MIN) atomicAdd(&start[order_bin(c[u], shift)], 1);
+  }
   __syncthreads();
   // exclusive scan over position p = 1023 - bin (heaviest bin first)
   const int v = start[t];
@@ -200,9 +213,16 @@ __global__ void __launch_bounds__(1024) order_work_kernel(const int32_t* __restr
   start[t] = wsum[w] + x - v;
   if (t == 1023 && n_work) *n_work = start[t];
   __syncthreads();
-  for (int i = t; i < items; i += blockDim.x) {
-    const int pos = atomicAdd(&start[order_bin(cnt[i], shift)], 1);
-    work[pos] = i;
+  for (int i0 = t; i0 < items; i0 += kB * (int)blockDim.x) {
+    int c[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      c[u] = i < items ? __ldg(cnt + i) : INT_MIN;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+      if (c[u] != INT_MIN) work[atomicAdd(&start[order_bin(c[u], shift)], 1)] = i0 + u * (int)blockDim.x;
   }
 }
 
