@@ -154,6 +154,19 @@ int sa_topk_stable_rows_f32(const float* scores, int rows, long long ld, const i
                             const int32_t* ks, int32_t* idx_out, long long out_ld,
                             int32_t* count_out, void* stream);
 
+/* ---- pattern choice on given errors: search.py:245-250 ------------------- */
+/* err [rows, ld] float64 (device): choice_out[r] = strict-< argmin over the
+ * first ncand columns (earlier candidate wins ties, NaN never wins). */
+int sa_select_family(const double* err, long long ld, int rows, int ncand, int32_t* choice_out, void* stream);
+
+/* ---- block index from given fp32 block weights (patterns.py:309-321) ------ */
+/* w [nb, ld] fp32 (device, row gq valid on columns 0..gq): blk_out [nb, k_b + 1]
+ * = stable top-min(k_b, gq + 1) of row gq plus gq, ascending, INT32_MAX padded.
+ * Bit-exact given identical fp32 weights. */
+size_t sa_block_topk_workspace(int nb, int k_b);
+int sa_block_topk_f32(const float* w, int nb, long long ld, int k_b, int32_t* blk_out, void* ws, size_t ws_bytes,
+                      void* stream);
+
 /* ---- Block estimator: patterns.block_mean / build_block_index
  *      (patterns.py:279-321) ------------------------------------------------ */
 /* side 0 = query operand [hi|lo|hi] ([groups, nb, 384] bf16), side 1 = key

@@ -539,3 +539,40 @@ extern "C" int sa_block_select(int batch, int heads, int kv_heads, int n, int b,
                                  (long long)nb * (k_b + 1), blk_row_off, nb + 1, nullptr, 0, ws,
                                  ws_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
+
+// build_block_index's selection on given fp32 block weights (patterns.py:309-321):
+// row gq keeps the stable top-min(k_b, gq + 1) of w[gq, :gq + 1] plus gq itself,
+// ascending, in fixed-stride rows of k_b + 1 padded with INT32_MAX.
+extern "C" size_t sa_block_topk_workspace(int nb, int k_b) {
+  if (nb < 1 || k_b < 1) return 0;
+  return ((size_t)nb * (2 + (size_t)k_b)) * 4 + 256;
+}
+
+extern "C" int sa_block_topk_f32(const float* w, int nb, long long ld, int k_b, int32_t* blk_out, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  using namespace sa;
+  if (nb < 1 || ld < nb) return fail(SA_ERR_DIMENSION, "bad block weight shape");
+  if (k_b < 1 || k_b > nb) return fail(SA_ERR_PATTERN_PARAM, "k_b must be in [1, %d], got %d", nb, k_b);
+  if (!w || !blk_out || !ws || ws_bytes < sa_block_topk_workspace(nb, k_b))
+    return fail(SA_ERR_DIMENSION, "null pointer or workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int32_t* lens = reinterpret_cast<int32_t*>(ws);
+  int32_t* ks = lens + nb;
+  int32_t* topk = ks + nb;
+  seg_lens_kernel<<<(nb + 255) / 256, 256, 0, st>>>(lens, ks, nb, nb, k_b);
+  int rc;
+  if ((rc = check_launch("seg_lens_kernel"))) return rc;
+  TopkArgs t{};
+  t.scores = w;
+  t.ld = ld;
+  t.rows = nb;
+  t.n = nb;
+  t.lens = lens;
+  t.ks = ks;
+  t.idx_out = topk;
+  t.out_ld = k_b;
+  if ((rc = launch_topk(t, st))) return rc;
+  merge_diag_kernel<<<(nb + 255) / 256, 256, 0, st>>>(topk, k_b, nb, blk_out, (long long)nb * (k_b + 1), 0, 1,
+                                                     nullptr, 0);
+  return check_launch("merge_diag_kernel");
+}

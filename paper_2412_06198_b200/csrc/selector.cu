@@ -366,3 +366,33 @@ extern "C" int sa_select_windowed(int batch, int heads, int kv_heads, int n, int
                            cand_p1_host, cand_p2_host, choice_out, family_out, err_out,
                            reinterpret_cast<cudaStream_t>(stream));
 }
+
+// search.py:245-250: per row the strict-< argmin over the candidates' errors
+// (the earlier candidate wins ties; NaN never wins; all-NaN -> candidate 0).
+namespace sa {
+__global__ void select_family_kernel(const double* err, long long ld, int rows, int ncand, int32_t* out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double best = INFINITY;
+  int bc = 0;
+  for (int c = 0; c < ncand; ++c) {
+    const double e = err[(size_t)r * ld + c];
+    if (e < best) {
+      best = e;
+      bc = c;
+    }
+  }
+  out[r] = bc;
+}
+}  // namespace sa
+
+extern "C" int sa_select_family(const double* err, long long ld, int rows, int ncand, int32_t* choice_out,
+                                void* stream) {
+  using namespace sa;
+  if (rows < 0 || ncand < 1 || ncand > 3 || ld < ncand) return fail(SA_ERR_SEARCH, "bad error matrix shape");
+  if (rows == 0) return SA_OK;
+  if (!err || !choice_out) return fail(SA_ERR_DIMENSION, "null pointer");
+  select_family_kernel<<<(rows + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(err, ld, rows, ncand,
+                                                                                              choice_out);
+  return check_launch("select_family_kernel");
+}

@@ -377,3 +377,48 @@ def test_attention_large_logits(sa, gain):
         err = np.abs(got[h] - want)
         assert np.isfinite(got[h]).all()
         assert err.max() <= MAX_ABS and err.mean() <= MEAN_ABS, (h, err.max(), err.mean())
+
+
+def test_select_family_on_given_errors(sa):
+    """sa_select_family: strict-< argmin, earlier candidate wins ties, NaN never
+    wins (search.py:245-250), on identical fp64 errors."""
+    from paper_2412_06198_b200 import _lib
+
+    rng = np.random.default_rng(5)
+    err = rng.integers(0, 4, (500, 3)).astype(np.float64) * 0.25  # many exact ties
+    err[7] = np.nan
+    err[8, 0] = np.nan
+    err[9, 1:] = np.inf
+    want = np.zeros(500, np.int32)
+    for r in range(500):
+        best, bc = np.inf, 0
+        for c in range(3):
+            if err[r, c] < best:
+                best, bc = err[r, c], c
+        want[r] = bc
+    d = torch.from_numpy(err).cuda()
+    out = torch.empty(500, dtype=torch.int32, device="cuda")
+    _lib.call("sa_select_family", d.data_ptr(), 3, 500, 3, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    np.testing.assert_array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("nb,k_b,ties", [(1, 1, False), (37, 3, True), (300, 1, False), (300, 8, True), (2000, 51, True)])
+def test_block_topk_on_given_weights(sa, nb, k_b, ties):
+    """sa_block_topk_f32: the Block-Cluster row selection of build_block_index
+    (patterns.py:309-321) on identical fp32 weights, bit-exact."""
+    from paper_2412_06198_b200 import _lib
+
+    rng = np.random.default_rng(nb + k_b)
+    w = (rng.integers(0, 5, (nb, nb)) * 0.5 if ties else rng.standard_normal((nb, nb))).astype(np.float32)
+    want = np.full((nb, k_b + 1), np.iinfo(np.int32).max, np.int64)
+    for gq in range(nb):
+        top = np.argsort(-w[gq, : gq + 1], kind="stable")[: min(k_b, gq + 1)]
+        sel = sorted(set(top.tolist()) | {gq})
+        want[gq, : len(sel)] = sel
+    d = torch.from_numpy(w).cuda()
+    out = torch.empty((nb, k_b + 1), dtype=torch.int32, device="cuda")
+    lib = _lib.load()
+    ws = torch.empty(int(lib.sa_block_topk_workspace(nb, k_b)), dtype=torch.uint8, device="cuda")
+    _lib.call("sa_block_topk_f32", d.data_ptr(), nb, nb, k_b, out.data_ptr(), ws.data_ptr(), ws.numel(),
+              torch.cuda.current_stream().cuda_stream)
+    np.testing.assert_array_equal(out.cpu().numpy().astype(np.int64), want)
