@@ -284,23 +284,8 @@ __device__ __forceinline__ uint32_t word_range(int lo, int hi) {
 
 // Set bits [a, b) (clipped to [0,128)) in a 128-bit mask held as 4 words.
 __device__ __forceinline__ void mask_set_range(uint32_t (&m)[4], int a, int b) {
-#ifdef SA_BRANCHY_RANGE
-  a = a < 0 ? 0 : a;
-  b = b > 128 ? 128 : b;
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    int lo = a - 32 * w, hi = b - 32 * w;
-    lo = lo < 0 ? 0 : lo;
-    hi = hi > 32 ? 32 : hi;
-    if (hi > lo) {
-      uint32_t bits = (hi - lo == 32) ? 0xffffffffu : (((1u << (hi - lo)) - 1u) << lo);
-      m[w] |= bits;
-    }
-  }
-#else
 #pragma unroll
   for (int w = 0; w < 4; ++w) m[w] |= word_range(a - 32 * w, b - 32 * w);
-#endif
 }
 
 }  // namespace sa
