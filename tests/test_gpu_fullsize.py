@@ -240,3 +240,24 @@ def test_fullsize_128k_auto_layer():
     e = torch.stack(errs)
     assert e.max().item() <= MAX_ABS and e.mean().item() <= MEAN_ABS, (e.max().item(), e.mean().item())
     _check_vs_estimator_and_index(q, k, fam, pats, view, n)
+
+
+def test_max_length_256k_auto_layer():
+    """The largest supported length (262144 = the tile-map limit): 8 q / 2 kv
+    heads in auto mode, sampled rows against exact attention over the realised
+    index, and the VS top-k bit-exact on the device scores."""
+    global H, HK
+    saved = (H, HK)
+    H, HK = 8, 2
+    try:
+        n = 262144
+        g = torch.Generator(device="cuda")
+        g.manual_seed(11)
+        q, k, v = ((torch.rand((h, n, D), generator=g, device="cuda") * 2 - 1).bfloat16() for h in (H, HK, HK))
+        plan, ws, out = _run_layer(q, k, v, n)
+        makers, fam, pats, view = _key_sets(plan, ws, n)
+        assert torch.isfinite(out.float()).all()
+        _check_rows(q, k, v, out, makers, [0, 1, 128 * 1024 + 5, n - 129, n - 1], n)
+        _check_vs_estimator_and_index(q, k, fam, pats, view, n)
+    finally:
+        H, HK = saved
