@@ -22,7 +22,7 @@
 
 namespace sa {
 
-constexpr int kDecChunk = 256;    // keys per CTA
+constexpr int kDecChunkMax = 1024;  // keys per CTA: 256 .. 1024, about 2048 CTAs per call
 constexpr int kDecThreads = 256;
 constexpr int kDecMaxG = 4;       // query heads per kv head and pass (registers: 4 x 8 accumulators)
 constexpr int kDecMaxD = 128;
@@ -73,19 +73,19 @@ template <class T, int W>
 __global__ void __launch_bounds__(kDecThreads, 3) decode_partial_kernel(const float* __restrict__ q, const T* __restrict__ kc,
                                                                      const T* __restrict__ vc, int heads, int kv_heads, int n,
                                                                      int d, int cap, float scale_log2, int h_off, int g,
-                                                                     float* __restrict__ part) {
+                                                                     int chunk, float* __restrict__ part) {
   // this pass: query heads [h_off, h_off + g) of each kv group (g <= kDecMaxG)
   const int bkh = blockIdx.x, split = blockIdx.y, nsplit = gridDim.y;
   const int gt = heads / kv_heads;
   const int b = bkh / kv_heads, kh = bkh % kv_heads;
-  const int c0 = split * kDecChunk, len = min(kDecChunk, n - c0);
+  const int c0 = split * chunk, len = min(chunk, n - c0);
   constexpr int kCols = kDecMaxD / W;           // column groups of a V row
   constexpr int kKq = kDecThreads / kCols;      // key interleave of the P·V pass
   // partial P·V slots: one per key interleave, or per warp when W = 8 (two
   // interleaves per warp are folded with a shuffle first)
   constexpr int kSlots = W == 8 ? kDecThreads / 32 : kKq;
   __shared__ float qs[kDecMaxG][kDecMaxD];
-  __shared__ float sc[kDecMaxG][kDecChunk];
+  __shared__ float sc[kDecMaxG][kDecChunkMax];
   __shared__ float stat[kDecMaxG][2];
   __shared__ float po[kSlots][kDecMaxG][kDecMaxD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(kDecThreads, 3) decode_partial_kernel(const fl
   __syncthreads();
   const size_t base = ((size_t)bkh * cap) * d;
   // 1. scores (log2 domain), thread per key
-  if (tid < len) {
-    const T* kr = kc + base + (size_t)(c0 + tid) * d;
+  for (int key = tid; key < len; key += kDecThreads) {
+    const T* kr = kc + base + (size_t)(c0 + key) * d;
     float acc[kDecMaxG];
 #pragma unroll
     for (int h = 0; h < kDecMaxG; ++h) acc[h] = 0.f;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kDecThreads, 3) decode_partial_kernel(const fl
     }
 #pragma unroll
     for (int h = 0; h < kDecMaxG; ++h)
-      if (h < g) sc[h][tid] = acc[h];
+      if (h < g) sc[h][key] = acc[h];
   }
   __syncthreads();
   // 2. chunk max / exp / sum per head (warp per head)
@@ -245,7 +245,14 @@ __global__ void __launch_bounds__(kDecThreads, 3) decode_partial_kernel(const fl
 // chunks s.  All chunk statistics are read in parallel (the weights land in
 // shared memory), then thread c sums column c over the chunks with 8 loads in
 // flight.
-constexpr int kDecMaxSplit = 1024;  // 262144 keys / 256
+constexpr int kDecMaxSplit = 1024;  // chunks per kv head (262144 keys / 256 at most)
+
+// keys per CTA for n cached rows over `groups` = batch * kv_heads
+static int dec_chunk(int n, int groups) {
+  int c = 256;
+  while (c < kDecChunkMax && (long long)n * groups / c > 2048) c *= 2;
+  return c;
+}
 __global__ void __launch_bounds__(128) decode_combine_kernel(const float* __restrict__ part, int heads, int kv_heads,
                                                              int d, int nsplit, int h_off, int g, float* __restrict__ out) {
   // CTA (batch * kv head, head of this pass)
@@ -293,7 +300,8 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const float* __rest
 
 extern "C" size_t sa_decode_workspace(int batch, int heads, int kv_heads, int n, int d) {
   if (batch < 1 || heads < 1 || kv_heads < 1 || n < 1 || d < 1) return 0;
-  const size_t nsplit = (size_t)(n + sa::kDecChunk - 1) / sa::kDecChunk;
+  const int chunk = sa::dec_chunk(n, batch * kv_heads);
+  const size_t nsplit = (size_t)(n + chunk - 1) / chunk;
   const size_t g = (size_t)(heads / kv_heads < sa::kDecMaxG ? heads / kv_heads : sa::kDecMaxG);
   return (size_t)batch * kv_heads * g * nsplit * (d + 2) * sizeof(float);
 }
@@ -306,11 +314,12 @@ extern "C" int sa_decode_attn(int batch, int heads, int kv_heads, int n, int d, 
     return fail(SA_ERR_DIMENSION, "bad decode shape (batch %d, heads %d, kv_heads %d, n %d)", batch, heads, kv_heads, n);
   if (d < 1 || d > kDecMaxD) return fail(SA_ERR_DIMENSION, "decode head_dim must be in [1, 128], got %d", d);
   if (capacity < n) return fail(SA_ERR_DIMENSION, "cache capacity %d below length %d", capacity, n);
-  if (n > kDecMaxSplit * kDecChunk) return fail(SA_ERR_DIMENSION, "decode supports up to %d cached rows", kDecMaxSplit * kDecChunk);
+  if (n > kDecMaxSplit * 256) return fail(SA_ERR_DIMENSION, "decode supports up to %d cached rows", kDecMaxSplit * 256);
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(SA_ERR_DIMENSION, "bad scale");
   if (!q || !k_cache || !v_cache || !out || !ws) return fail(SA_ERR_DIMENSION, "null pointer argument");
   if (ws_bytes < sa_decode_workspace(batch, heads, kv_heads, n, d)) return fail(SA_ERR_DIMENSION, "decode workspace too small");
-  const int nsplit = (n + kDecChunk - 1) / kDecChunk;
+  const int chunk = dec_chunk(n, batch * kv_heads);
+  const int nsplit = (n + chunk - 1) / chunk;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const float sl2 = scale * 1.4426950408889634f;
   dim3 grid(batch * kv_heads, nsplit);
@@ -324,7 +333,7 @@ extern "C" int sa_decode_attn(int batch, int heads, int kv_heads, int n, int d, 
 #define SA_DEC(T, W)                                                                                          \
   decode_partial_kernel<T, W><<<grid, kDecThreads, 0, st>>>(q, reinterpret_cast<const T*>(k_cache),         \
                                                             reinterpret_cast<const T*>(v_cache), heads,       \
-                                                            kv_heads, n, d, capacity, sl2, h_off, g, part)
+                                                            kv_heads, n, d, capacity, sl2, h_off, g, chunk, part)
     if (kv_dtype == 0) {
       if (w == 8) SA_DEC(float, 8); else if (w == 2) SA_DEC(float, 2); else SA_DEC(float, 1);
     } else if (kv_dtype == 1) {
