@@ -206,7 +206,7 @@ int sa_order_work(const int32_t* tile_cnt, int items, int max_cnt, int32_t* work
 /* One decode step (reference runtime.py:209-242 decode_step): the new token's
  * queries q [batch * heads, d] fp32 attend densely over the first n rows of a
  * KV cache laid out [batch, kv_heads, capacity, d] (kv_dtype 0 = fp32,
- * 1 = bf16), out [batch * heads, d] fp32.  Split-K over 256-key chunks, K/V
+ * 1 = bf16), out [batch * heads, d] fp32.  Split-K over 256-1024-key chunks, K/V
  * read in place once per kv head; ws >= sa_decode_workspace(...). */
 size_t sa_decode_workspace(int batch, int heads, int kv_heads, int n, int d);
 int sa_decode_attn(int batch, int heads, int kv_heads, int n, int d, int capacity, float scale, const float* q,
