@@ -325,14 +325,10 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const __grid_cons
         cur_unit = item / a.nchunks;
         const int sl0 = a.paired ? 64 : 64 * hf;  // stats lane of rl = 0
         const float* src = a.lse2 + (size_t)max(hx, 0) * 128 + sl0;
+        // rows outside [rl_lo, rl_hi) were never written by pass 1: not read
 #pragma unroll
-        for (int rl = 0; rl < 64; rl += 4) {
-          const float4 v = *reinterpret_cast<const float4*>(src + rl);
-          const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            nl[rl + q] = (hx >= 0 && rl + q >= rl_lo && rl + q < rl_hi) ? -vv[q] : -INFINITY;
-        }
+        for (int rl = 0; rl < 64; ++rl)
+          nl[rl] = (hx >= 0 && rl >= rl_lo && rl < rl_hi) ? -src[rl] : -INFINITY;
       }
       for (int kt = kt_lo; kt < kt_hi; ++kt, ++jg) {
         const int slot = jg & 1;
