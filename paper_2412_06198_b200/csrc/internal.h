@@ -68,6 +68,6 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
 
 // tiles.cu: heaviest-first order of the items with a nonzero cost; *n_work = their number
 int launch_order_work(const int32_t* cost, int items, int max_cost, int32_t* work, int32_t* n_work,
-                      cudaStream_t st);
+                      cudaStream_t st, int nqt = 0, int group = 0);
 
 }  // namespace sa

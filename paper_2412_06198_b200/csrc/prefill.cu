@@ -427,7 +427,14 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   int* counter = wbase;
   int32_t* n_work = wbase + 1;
   int32_t* work = wbase + 64;
-  if (lpt && (rc = launch_order_work(V.tile_cnt, p.hh * p.nqt, p.nqt, work, n_work, st))) return rc;
+  // GQA siblings adjacent within a cost bin (SA_SIBLING_ORDER=0: head-major, for A/B)
+  static const bool sib = [] {
+    const char* e = getenv("SA_SIBLING_ORDER");
+    return !(e && e[0] == '0');
+  }();
+  if (lpt && (rc = launch_order_work(V.tile_cnt, p.hh * p.nqt, p.nqt, work, n_work, st, p.nqt,
+                                     sib ? H / HK : 1)))
+    return rc;
   rc = launch_attn(B, H, HK, n, desc->scale, q, k, v, out, &V.index, V.tile_off, V.tile_cnt, V.tiles,
                    lpt ? work : nullptr, nullptr, st, desc->out_ld, counter, lpt ? n_work : nullptr);
   mark(4);

@@ -164,9 +164,17 @@ __global__ void build_tiles_kernel(TileBuildArgs a) {
 __device__ __forceinline__ int order_bin(int c, int shift) {
   return c > 0 ? 1022 - min(c >> shift, 1022) : 1023;
 }
+// Within a bin the items are scattered in (kv group, query tile, head of the
+// group) order, `g` heads per group, so the GQA siblings of a query tile (same
+// K/V tiles) sit next to each other and run concurrently: their shared K/V
+// tiles are read from HBM once and hit L2 for the others.
+__device__ __forceinline__ int sibling_item(int p, int nqt, int g) {
+  const int grp = p / (nqt * g), r = p % (nqt * g);
+  return (grp * g + r % g) * nqt + r / g;
+}
 __global__ void __launch_bounds__(1024) order_work_kernel(const int32_t* __restrict__ cnt, int items,
                                                           int max_cnt, int32_t* __restrict__ work,
-                                                          int32_t* __restrict__ n_work) {
+                                                          int32_t* __restrict__ n_work, int nqt, int g) {
   // bins: tile count >> shift, at most 1023 (one per thread) plus the empty bin, heaviest first
   __shared__ int start[1024];
   __shared__ int wsum[32];
@@ -213,16 +221,25 @@ __global__ void __launch_bounds__(1024) order_work_kernel(const int32_t* __restr
   start[t] = wsum[w] + x - v;
   if (t == 1023 && n_work) *n_work = start[t];
   __syncthreads();
-  for (int i0 = t; i0 < items; i0 += kB * (int)blockDim.x) {
-    int c[kB];
+  // scatter: warp-aggregated, so lanes of one bin take consecutive positions in lane order
+  for (int p0 = t - lane; p0 < items; p0 += kB * (int)blockDim.x) {
+    int c[kB], it[kB];
 #pragma unroll
     for (int u = 0; u < kB; ++u) {
-      const int i = i0 + u * (int)blockDim.x;
-      c[u] = i < items ? __ldg(cnt + i) : INT_MIN;
+      const int p = p0 + u * (int)blockDim.x + lane;
+      it[u] = p < items ? sibling_item(p, nqt, g) : -1;
+      c[u] = it[u] >= 0 ? __ldg(cnt + it[u]) : INT_MIN;
     }
 #pragma unroll
-    for (int u = 0; u < kB; ++u)
-      if (c[u] != INT_MIN) work[atomicAdd(&start[order_bin(c[u], shift)], 1)] = i0 + u * (int)blockDim.x;
+    for (int u = 0; u < kB; ++u) {
+      const int bin = c[u] != INT_MIN ? order_bin(c[u], shift) : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      const int leader = __ffs(peers) - 1;
+      int base = 0;
+      if (lane == leader && bin >= 0) base = atomicAdd(&start[bin], __popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (bin >= 0) work[base + __popc(peers & ((1u << lane) - 1u))] = it[u];
+    }
   }
 }
 
@@ -260,14 +277,18 @@ extern "C" int sa_order_work(const int32_t* tile_cnt, int items, int max_cnt, in
   if (items < 1 || max_cnt < 0 || max_cnt > 65536) return fail(SA_ERR_DIMENSION, "bad work-order sizes");
   if (!tile_cnt || !work) return fail(SA_ERR_DIMENSION, "null pointer");
   order_work_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      tile_cnt, items, max_cnt, work, nullptr);
+      tile_cnt, items, max_cnt, work, nullptr, items, 1);
   return check_launch("order_work_kernel");
 }
 
 namespace sa {
 int launch_order_work(const int32_t* cost, int items, int max_cost, int32_t* work, int32_t* n_work,
-                      cudaStream_t st) {
-  order_work_kernel<<<1, 1024, 0, st>>>(cost, items, max_cost, work, n_work);
+                      cudaStream_t st, int nqt, int group) {
+  if (nqt < 1 || group < 1 || items % (nqt * group) != 0) {
+    nqt = items;
+    group = 1;
+  }
+  order_work_kernel<<<1, 1024, 0, st>>>(cost, items, max_cost, work, n_work, nqt, group);
   return check_launch("order_work_kernel");
 }
 }  // namespace sa
