@@ -331,6 +331,13 @@ def run_ours(args):
 
         qf, kf, vf = (torch.from_numpy(np.ascontiguousarray(x)).bfloat16().to(dev) for x in (q, k, v))
         layer = BalancedLayer(rank, world, H, HK, n, D, mode, fixed_pattern=fixed, device=dev)
+    # SA_MG_EXCHANGE=peer: the output all-gather fused into the attention epilogue
+    # (stores into every rank's CUDA-IPC-mapped output; multigpu.PeerOutputs)
+    peer = None
+    if balanced and os.environ.get("SA_MG_EXCHANGE", "nccl") == "peer":
+        from paper_2412_06198_b200.multigpu import PeerOutputs
+
+        peer = PeerOutputs(rank, world, n, H * D)
 
     def step(events=None):
         if events is not None:
@@ -352,7 +359,10 @@ def run_ours(args):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    if balanced:
+    if balanced and peer is not None:
+        def gstep():
+            layer.step_peers(qf, kf, vf, peer)
+    elif balanced:
         def gstep():
             layer.step(qf, kf, vf)
     else:
@@ -422,7 +432,10 @@ def run_ours(args):
         for _ in range(args.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            layer.attend(qf, kf, vf)
+            if peer is not None:
+                layer.attend_peers(qf, kf, vf, peer)
+            else:
+                layer.attend(qf, kf, vf)
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
@@ -486,7 +499,10 @@ def run_ours(args):
             "config": {"workload": f"llama3-8b-attn-layer-{n // 1024}k-{args.mode}", "heads": H, "kv_heads": HK,
                        "head_dim": D, "seq_len": n, "batch": 1, "mode": args.mode,
                        "parallelism": (f"balanced head-parallel x{world}: per-group estimation, index all-gather, "
-                                       f"heaviest-first (head, q-tile) deal, output-block all-gather") if balanced else
+                                       f"heaviest-first (head, q-tile) deal, " +
+                                       ("output rows stored into every rank's IPC-mapped buffer by the attention "
+                                        "epilogue (fused all-gather)" if peer is not None else
+                                        "output-block all-gather")) if balanced else
                                       (f"head-parallel x{world} + NCCL all-gather" if world > 1 else "single GPU"),
                        "l2": l2_note(n),
                        "launch": ("eager balanced steps (BalancedLayer.step); stage_ms from eager steps of this "
@@ -510,6 +526,8 @@ def run_ours(args):
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        peer.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -226,6 +226,30 @@ int sa_attn_sparse_work(int batch, int heads, int kv_heads, int n, float scale, 
                         const int32_t* tile_cnt, const uint32_t* tiles, const int32_t* work,
                         const int32_t* n_work, int32_t* counter, long long out_ld, void* stream);
 
+/* Fused output all-gather for the head-parallel layer (the
+ * reference has no multi-GPU path, runtime.py:174-195 runs heads serially; the
+ * north star names an NVLink all-gather of per-head outputs).  Same as
+ * sa_attn_sparse_work, plus: every output row the kernel produces is also
+ * stored, from the epilogue, at the same offset into each of the `n_peers`
+ * (<= 7) buffers in `peer_out` — other ranks' output buffers mapped with
+ * sa_ipc_open — so no separate all-gather follows.  The caller orders the
+ * peers' reads after this kernel (stream sync + a host barrier). */
+int sa_attn_sparse_work_peers(int batch, int heads, int kv_heads, int n, float scale, const void* q,
+                              const void* k, const void* v, void* out, void* const* peer_out, int n_peers,
+                              const sa_head_index* index, const int32_t* tile_off, const int32_t* tile_cnt,
+                              const uint32_t* tiles, const int32_t* work, const int32_t* n_work,
+                              int32_t* counter, long long out_ld, void* stream);
+
+/* CUDA IPC helpers for the peer buffers: sa_ipc_alloc allocates `bytes` of
+ * device memory and writes its SA_IPC_HANDLE_BYTES-byte handle; another
+ * process maps it with sa_ipc_open (same or peer GPU) and unmaps it with
+ * sa_ipc_close; the owner frees it with sa_ipc_free. */
+#define SA_IPC_HANDLE_BYTES 64
+int sa_ipc_alloc(size_t bytes, void** ptr, void* handle);
+int sa_ipc_free(void* ptr);
+int sa_ipc_open(const void* handle, void** ptr);
+int sa_ipc_close(void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -119,6 +119,12 @@ _SIGNATURES = {
     "sa_block_topk_f32": (ctypes.c_int, [_P, _I, ctypes.c_int64, _I, _P, _P, _SZ, _P]),
     "sa_attn_sparse_work": (ctypes.c_int, [_I, _I, _I, _I, _F, _P, _P, _P, _P, _IDX, _P, _P, _P, _P, _P, _P,
                                            ctypes.c_int64, _P]),
+    "sa_attn_sparse_work_peers": (ctypes.c_int, [_I, _I, _I, _I, _F, _P, _P, _P, _P, _P, _I, _IDX, _P, _P, _P,
+                                                 _P, _P, _P, ctypes.c_int64, _P]),
+    "sa_ipc_alloc": (ctypes.c_int, [_SZ, _P, _P]),
+    "sa_ipc_free": (ctypes.c_int, [_P]),
+    "sa_ipc_open": (ctypes.c_int, [_P, _P]),
+    "sa_ipc_close": (ctypes.c_int, [_P]),
     "sa_decode_workspace": (_SZ, [_I, _I, _I, _I, _I]),
     "sa_decode_attn": (ctypes.c_int, [_I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _I, _P, _P, _SZ, _P]),
     "sa_order_work": (ctypes.c_int, [_P, _I, _I, _P, _P]),

@@ -95,4 +95,42 @@ const char* sa_last_error(void) { return sa::g_last_error.c_str(); }
 
 int sa_version(void) { return 1; }
 
+// CUDA IPC for the fused output all-gather (multigpu.PeerOutputs): a rank's
+// output buffer is its own cudaMalloc allocation, so the opened mapping starts
+// at the buffer (no sub-allocation offset to carry).
+int sa_ipc_alloc(size_t bytes, void** ptr, void* handle) {
+  if (!ptr || !handle || bytes == 0) return sa::fail(SA_ERR_DIMENSION, "sa_ipc_alloc: bad arguments");
+  if (sizeof(cudaIpcMemHandle_t) > SA_IPC_HANDLE_BYTES) return sa::fail(SA_ERR_CUDA, "IPC handle size");
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess) return sa::fail(SA_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, *ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    return sa::fail(SA_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  }
+  memset(handle, 0, SA_IPC_HANDLE_BYTES);
+  memcpy(handle, &h, sizeof(h));
+  return SA_OK;
+}
+
+int sa_ipc_free(void* ptr) {
+  const cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? SA_OK : sa::fail(SA_ERR_CUDA, "cudaFree: %s", cudaGetErrorString(e));
+}
+
+int sa_ipc_open(const void* handle, void** ptr) {
+  if (!ptr || !handle) return sa::fail(SA_ERR_DIMENSION, "sa_ipc_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? SA_OK : sa::fail(SA_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+}
+
+int sa_ipc_close(void* ptr) {
+  const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? SA_OK : sa::fail(SA_ERR_CUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+}
+
 }  // extern "C"

@@ -37,6 +37,8 @@
 
 namespace sa {
 
+constexpr int kMaxPeers = 7;  // an 8-GPU NVSwitch domain
+
 struct AttnArgs {
   CUtensorMap tmap_q;  // [HH, n, 128] bf16, box {64, 128, 1}, SW128
   CUtensorMap tmap_k;  // [HK, n, 128], box {64, 64, 1}
@@ -62,6 +64,8 @@ struct AttnArgs {
   int* counter;              // optional work-item counter (zeroed before launch): dynamic fetch
   const int32_t* n_work;     // optional device count of `work` entries (default hh_total * nqt)
   int st256;                 // output rows 32-byte aligned: 256-bit stores
+  int n_peers;               // > 0: every output row is also stored into these buffers (same layout),
+  __nv_bfloat16* peer_out[kMaxPeers];  // other ranks' outputs mapped over NVLink (fused all-gather)
 };
 
 constexpr int kThreads = 192;
@@ -498,8 +502,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       tc_fence_after();
       const float inv = 1.0f / l;
       const bool valid = i < a.n && cur_cnt > 0;  // cnt == 0: query tile not requested
-      __nv_bfloat16* orow = a.out + (long long)bidx * a.out_batch_stride +
-                            (long long)i * a.out_row_stride + (long long)h * kHeadDim;
+      const long long ooff = (long long)bidx * a.out_batch_stride + (long long)i * a.out_row_stride +
+                             (long long)h * kHeadDim;
+      __nv_bfloat16* orow = a.out + ooff;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t o[32];
@@ -514,14 +519,21 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 #pragma unroll
           for (int t = 0; t < 16; ++t)
             pk[t] = pack_bf16(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
-          if (a.st256) {  // 32-byte stores: whole L2 sectors per lane
+          auto store = [&](__nv_bfloat16* row) {
+            if (a.st256) {  // 32-byte stores: whole L2 sectors per lane
 #pragma unroll
-            for (int t = 0; t < 2; ++t) st_global_v8(orow + 32 * c + 16 * t, pk + 8 * t);
-          } else {
-            uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
+              for (int t = 0; t < 2; ++t) st_global_v8(row + 32 * c + 16 * t, pk + 8 * t);
+            } else {
+              uint4* dst = reinterpret_cast<uint4*>(row + 32 * c);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
-          }
+              for (int t = 0; t < 4; ++t)
+                dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+            }
+          };
+          store(orow);
+          // fused all-gather: the same bytes straight into every peer's output over NVLink
+#pragma unroll 1
+          for (int pr = 0; pr < a.n_peers; ++pr) store(a.peer_out[pr] + ooff);
         }
       }
       if (valid && a.lse != nullptr) a.lse[(size_t)hh * a.n + i] = (m_used + log2f(l)) * 0.69314718055994531f;
@@ -554,7 +566,8 @@ namespace sa {
 int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const void* q, const void* k,
                 const void* v, void* out, const sa_head_index* index, const int32_t* tile_off,
                 const int32_t* tile_cnt, const uint32_t* tiles, const int32_t* work, float* lse,
-                cudaStream_t cs, long long out_ld, int* counter, const int32_t* n_work) {
+                cudaStream_t cs, long long out_ld, int* counter, const int32_t* n_work,
+                void* const* peer_out, int n_peers) {
   if (batch < 1 || heads < 1 || kv_heads < 1 || n < 1)
     return fail(SA_ERR_DIMENSION, "need batch, heads, kv_heads, n >= 1");
   if (heads % kv_heads != 0)
@@ -577,6 +590,15 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   if (a.out_row_stride % 8 != 0 || (reinterpret_cast<uintptr_t>(out) & 15) != 0)
     return fail(SA_ERR_DIMENSION, "output rows must be 16-byte aligned (out_ld %% 8 == 0)");
   a.st256 = (a.out_row_stride % 16 == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0) ? 1 : 0;
+  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && !peer_out))
+    return fail(SA_ERR_DIMENSION, "n_peers must be in [0, %d]", kMaxPeers);
+  a.n_peers = n_peers;
+  for (int p = 0; p < n_peers; ++p) {
+    const uintptr_t pp = reinterpret_cast<uintptr_t>(peer_out[p]);
+    if (!pp || (pp & 15) != 0) return fail(SA_ERR_DIMENSION, "peer output %d null or not 16-byte aligned", p);
+    if ((pp & 31) != 0) a.st256 = 0;
+    a.peer_out[p] = reinterpret_cast<__nv_bfloat16*>(peer_out[p]);
+  }
   a.n = n;
   a.heads = heads;
   a.kv_heads = kv_heads;
@@ -647,4 +669,16 @@ extern "C" int sa_attn_sparse_work(int batch, int heads, int kv_heads, int n, fl
   if (!work || !n_work || !counter) return sa::fail(SA_ERR_DIMENSION, "null work list or counter");
   return sa::launch_attn(batch, heads, kv_heads, n, scale, q, k, v, out, index, tile_off, tile_cnt, tiles, work,
                          nullptr, reinterpret_cast<cudaStream_t>(stream), out_ld, counter, n_work);
+}
+
+extern "C" int sa_attn_sparse_work_peers(int batch, int heads, int kv_heads, int n, float scale, const void* q,
+                                         const void* k, const void* v, void* out, void* const* peer_out,
+                                         int n_peers, const sa_head_index* index, const int32_t* tile_off,
+                                         const int32_t* tile_cnt, const uint32_t* tiles, const int32_t* work,
+                                         const int32_t* n_work, int32_t* counter, long long out_ld,
+                                         void* stream) {
+  if (!work || !n_work || !counter) return sa::fail(SA_ERR_DIMENSION, "null work list or counter");
+  return sa::launch_attn(batch, heads, kv_heads, n, scale, q, k, v, out, index, tile_off, tile_cnt, tiles, work,
+                         nullptr, reinterpret_cast<cudaStream_t>(stream), out_ld, counter, n_work, peer_out,
+                         n_peers);
 }

@@ -8,6 +8,8 @@ the reference's (B, n, H*d) layout (runtime.py:194).
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -39,6 +41,59 @@ def gather_heads(local: torch.Tensor, world: int, group=None, out: torch.Tensor 
         dist.all_gather(parts, local.contiguous(), group=group)
         out.view(n, world, w).copy_(torch.stack(parts, 1))
     return out
+
+
+# ---------------------------------------------------------------- fused output exchange
+class _DeviceArray:
+    """`__cuda_array_interface__` over a raw device allocation (int16 words)."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<i2", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class PeerOutputs:
+    """Every rank's final (rows, cols) bf16 output, mapped into every rank.
+
+    Each rank allocates its output with sa_ipc_alloc and all-gathers the CUDA
+    IPC handle once; the others map it (sa_ipc_open: NVLink/NVSwitch peer
+    memory, or the same GPU when ranks share one in tests).  The attention
+    epilogue then stores every row it produces into all of them
+    (sa_attn_sparse_work_peers), which replaces the output all-gather."""
+
+    def __init__(self, rank: int, world: int, rows: int, cols: int, group=None):
+        from . import _lib
+
+        lib = _lib.load()
+        self.rank, self.world, self.rows, self.cols = rank, world, rows, cols
+        self._group = group
+        ptr = ctypes.c_void_p()
+        handle = (ctypes.c_uint8 * 64)()
+        _lib.check(lib.sa_ipc_alloc(rows * cols * 2, ctypes.byref(ptr), handle))
+        self._ptr = ptr.value
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        self.peer_ptrs = []
+        for r in range(world):
+            if r != rank:
+                p = ctypes.c_void_p()
+                _lib.check(lib.sa_ipc_open(ctypes.c_char_p(handles[r]), ctypes.byref(p)))
+                self.peer_ptrs.append(p.value)
+        self.peers = (ctypes.c_void_p * max(1, len(self.peer_ptrs)))(*self.peer_ptrs)
+        self.local = torch.as_tensor(_DeviceArray(self._ptr, (rows, cols)), device="cuda").view(torch.bfloat16)
+
+    def close(self) -> None:
+        """Unmap the peers and free this rank's buffer (collective)."""
+        from . import _lib
+
+        lib = _lib.load()
+        torch.cuda.synchronize()
+        dist.barrier(group=self._group)  # no rank still stores into a peer
+        for p in self.peer_ptrs:
+            _lib.check(lib.sa_ipc_close(ctypes.c_void_p(p)))
+        dist.barrier(group=self._group)  # no rank still maps this buffer
+        self.local = None
+        _lib.check(lib.sa_ipc_free(ctypes.c_void_p(self._ptr)))
 
 
 # ---------------------------------------------------------------- balanced layer
@@ -201,3 +256,26 @@ class BalancedLayer:
         """One layer on this rank (all-gathers between the phases)."""
         self.load_index(self._all_gather(self.estimate(q, k, v), self.world, group))
         return self.assemble(self._all_gather(self.attend(q, k, v), self.world, group))
+
+    def attend_peers(self, q, k, v, peer: PeerOutputs) -> None:
+        """(4)+(5) fused: attention for this rank's items, each output row
+        stored into this rank's and every peer's output buffer."""
+        from . import _lib
+        from . import _device as Dv
+
+        if peer.rows < self.n or peer.cols != self.H * self.d:
+            raise ValueError("peer output buffers have the wrong shape")
+        _lib.call("sa_attn_sparse_work_peers", 1, self.H, self.HK, self.n, self.full.scale, q.data_ptr(),
+                  k.data_ptr(), v.data_ptr(), peer.local.data_ptr(), peer.peers, len(peer.peer_ptrs),
+                  self.vf.index, self.vf.tile_off, self.vf.tile_cnt, self.vf.tiles, self.mine.data_ptr(),
+                  self.n_mine.data_ptr(), self.counter.data_ptr(), 0, Dv.stream())
+
+    def step_peers(self, q, k, v, peer: PeerOutputs, group=None) -> torch.Tensor:
+        """One layer with the output all-gather fused into the attention
+        epilogue; the stream sync + barrier order every rank's peer stores
+        before any rank reads its output."""
+        self.load_index(self._all_gather(self.estimate(q, k, v), self.world, group))
+        self.attend_peers(q, k, v, peer)
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=group)
+        return peer.local[: self.n]

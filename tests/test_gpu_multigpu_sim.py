@@ -50,10 +50,12 @@ def test_balanced_layer_matches_single_gpu(n, world, mode):
     assert max(loads) <= 1.05 * cnt.sum() / world + cnt.max()
 
 
-def test_bench_two_ranks_share_one_gpu():
+@pytest.mark.parametrize("exchange", ["nccl", "peer"])
+def test_bench_two_ranks_share_one_gpu(exchange):
     """Dry run of `bench.py --gpus 2` under torchrun: two ranks on the one GPU
-    with gloo collectives (SA_DIST_BACKEND=gloo) through the balanced layer,
-    ending in one JSON line from rank 0."""
+    with gloo collectives (SA_DIST_BACKEND=gloo) through the balanced layer
+    (output exchange by all-gather, or fused into the attention epilogue over
+    CUDA IPC: SA_MG_EXCHANGE=peer), ending in one JSON line from rank 0."""
     import json
     import os
     import socket
@@ -65,7 +67,7 @@ def test_bench_two_ranks_share_one_gpu():
     port = s.getsockname()[1]
     s.close()
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SA_DIST_BACKEND="gloo")
+    env = dict(os.environ, SA_DIST_BACKEND="gloo", SA_MG_EXCHANGE=exchange)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--ctx", "8192", "--steps", "3",
            "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
@@ -74,3 +76,30 @@ def test_bench_two_ranks_share_one_gpu():
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2
     assert lines[0]["config"]["parallelism"].startswith("balanced head-parallel x2")
+    assert ("fused all-gather" in lines[0]["config"]["parallelism"]) == (exchange == "peer")
+
+
+@pytest.mark.parametrize("world,n,mode", [(2, 4096, "auto"), (4, 2500, "fixed")])
+def test_fused_peer_exchange(world, n, mode):
+    """The fused output all-gather: `world` ranks share the GPU, map each
+    other's output buffers over CUDA IPC and store their rows into all of them
+    from the attention epilogue; every rank's buffer must equal the
+    single-GPU layer bit for bit (twice: the mappings are reused)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "tests/peer_worker.py", str(n), mode]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert sorted(x["rank"] for x in lines) == list(range(world))
+    assert all(x["ok"] == [True, True] for x in lines), lines
