@@ -107,7 +107,8 @@ struct BlockScoreArgs {
   long long head_stride;
   int row_stride;
   // MATERIALIZE output
-  float* logits;         // [HH_group, nb, nb] (row-major), indexed by hh - hh_base
+  float* logits;         // [HH_group, nb, logits_ld] (row-major), indexed by hh - hh_base
+  int logits_ld;         // nb rounded up to 4: 16-byte aligned rows for the float4 stores
   int hh_base, hh_count;
   const int32_t* gate;
   int gate_val;
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kBsThreads, 2) block_score_kernel(const __grid
             }
           }
       } else {
-        float* row = a.logits + ((size_t)(hh - a.hh_base) * a.nb + gq) * a.nb + g0;
+        float* row = a.logits + ((size_t)(hh - a.hh_base) * a.nb + gq) * a.logits_ld + g0;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -408,8 +409,10 @@ int launch_block_pool(int groups, int n, int b, int side, const void* x, void* s
 }
 
 // MATERIALIZE path: logits of up to kMatHeads heads at a time (<= ~1 GB).
+static int logits_ld(int nb) { return (nb + 3) & ~3; }
+
 static int mat_heads(int nb, int hh_total) {
-  const long long per = (long long)nb * nb * 4 + (long long)nb * 64;
+  const long long per = (long long)nb * logits_ld(nb) * 4 + (long long)nb * 64;
   long long g = (1ll << 30) / per;
   if (g < 1) g = 1;
   if (g > hh_total) g = hh_total;
@@ -420,7 +423,7 @@ size_t block_select_ws(int n, int b, int k_b, int hh_total) {
   const int nb = (n + b - 1) / b;
   if (k_b <= 8) return 256;
   const long long g = mat_heads(nb, hh_total);
-  return (size_t)g * ((size_t)nb * nb * 4 + (size_t)nb * k_b * 4 + (size_t)nb * 8) + 1024;
+  return (size_t)g * ((size_t)nb * logits_ld(nb) * 4 + (size_t)nb * k_b * 4 + (size_t)nb * 8) + 1024;
 }
 
 int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b, float scale,
@@ -485,13 +488,15 @@ int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_
   if (!ws || ws_bytes < need) return fail(SA_ERR_DIMENSION, "block_select workspace too small");
   char* p = reinterpret_cast<char*>(ws);
   float* logits = reinterpret_cast<float*>(p);
-  p += (size_t)G * nb * nb * 4;
+  if ((reinterpret_cast<uintptr_t>(logits) & 15) != 0) return fail(SA_ERR_DIMENSION, "workspace not 16-byte aligned");
+  p += (size_t)G * nb * logits_ld(nb) * 4;
   int32_t* topk = reinterpret_cast<int32_t*>(p);
   p += (size_t)G * nb * k_b * 4;
   int32_t* lens = reinterpret_cast<int32_t*>(p);
   int32_t* ks = lens + (size_t)G * nb;
   seg_lens_kernel<<<(G * nb + 255) / 256, 256, 0, st>>>(lens, ks, G * nb, nb, k_b);
   a.logits = logits;
+  a.logits_ld = logits_ld(nb);
   for (int h0 = 0; h0 < hh_total; h0 += G) {
     const int cnt = std::min(G, hh_total - h0);
     a.hh_base = h0;
@@ -501,7 +506,7 @@ int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_
     if ((rc = check_launch("block_score_kernel<materialize>"))) return rc;
     TopkArgs t{};
     t.scores = logits;
-    t.ld = nb;
+    t.ld = a.logits_ld;
     t.rows = cnt * nb;
     t.n = nb;
     t.lens = lens;

@@ -269,7 +269,8 @@ def device_block_rows(q, k, b, k_b):
 
 
 @pytest.mark.parametrize("n,b,k_b", [(13, 4, 2), (1000, 8, 1), (4096, 8, 1), (4096, 64, 6), (3000, 7, 3),
-                                     (4096, 64, 13), (2000, 128, 2), (600, 200, 1)])
+                                     (4096, 64, 13), (2000, 128, 2), (600, 200, 1),
+                                     (2564, 16, 60), (1001, 8, 9)])  # materialized rows, nb % 4 != 0
 def test_block_estimator(sa, n, b, k_b):
     q, k = rand_heads(11, 1, n)[0], rand_heads(12, 1, n)[0]
     got = device_block_rows(q, k, b, k_b)
