@@ -25,6 +25,9 @@ ap.add_argument("--cases", type=int, default=40)
 ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--max-n", type=int, default=6000)
 ap.add_argument("--only", type=int, nargs="*", default=None, help="run only these case numbers")
+ap.add_argument("--api-mix", action="store_true",
+                help="also randomise the batch (1-3) and the input kind (numpy / CPU torch, pinned or not / "
+                     "CUDA torch bf16 or fp32): the host-streamed and device entry paths")
 args = ap.parse_args()
 rng = np.random.default_rng(args.seed)
 LAYOUTS = [(4, 4), (8, 2), (8, 1), (6, 3), (2, 1), (16, 4)]
@@ -120,23 +123,45 @@ for c in range(args.cases):
     seed = int(rng.integers(1 << 30))
     q, k, v = (O.bf16_round(x) for x in O.synth_qkv_gqa(seed, n, H, HK, d))
     fixed = rand_fixed(n) if mode == "fixed" else None
+    B, kind = 1, "numpy"
+    if args.api_mix:
+        B = int(rng.integers(1, 4))
+        kind = str(rng.choice(["numpy", "cpu", "cpu_pinned", "cuda_bf16", "cuda_f32"]))
+        if B > 1:
+            extra = [[O.bf16_round(x) for x in O.synth_qkv_gqa(seed + 1 + b, n, H, HK, d)] for b in range(B - 1)]
+            q, k, v = (np.concatenate([t] + [e[i] for e in extra]) for i, t in enumerate((q, k, v)))
     if args.only is not None and c not in args.only:
         continue
     rec = {"case": c, "H": H, "HK": HK, "n": n, "d": d, "mode": mode, "fixed": conv(fixed), "seed": seed}
+    if args.api_mix:
+        rec.update(batch=B, inputs=kind)
     try:
         want, wplans = O.prefill(q, k, v, mode, fixed_pattern=fixed)
         cfg = sa.ModelConfig(n_heads=H, d_model=H * d, d_head=d, max_context=max(n, 1))
         kw = {"fixed_pattern": to_sa(fixed)} if fixed is not None else {}
-        res = sa.prefill(q, k, v, cfg, mode=mode, **kw)
-        got = np.asarray(res.outputs, np.float64)
+        qi, ki, vi = q, k, v
+        if kind != "numpy":
+            import torch
+
+            qi, ki, vi = (torch.from_numpy(np.ascontiguousarray(x)) for x in (q, k, v))
+            if kind == "cpu_pinned":
+                qi, ki, vi = (x.pin_memory() for x in (qi, ki, vi))
+            elif kind == "cuda_bf16":
+                qi, ki, vi = (x.cuda().bfloat16() for x in (qi, ki, vi))
+            elif kind == "cuda_f32":
+                qi, ki, vi = (x.cuda() for x in (qi, ki, vi))
+        res = sa.prefill(qi, ki, vi, cfg, mode=mode, **kw)
+        o = res.outputs
+        got = (o.float().cpu().numpy() if hasattr(o, "cpu") else np.asarray(o)).astype(np.float64)
         err = np.abs(got - want)
-        gplans = [conv(hp.pattern) for hp in res.plans[0]]
+        gplans = [[conv(hp.pattern) for hp in row] for row in res.plans]
         rec.update(max_abs=float(err.max()), mean_abs=float(err.mean()),
-                   plans_equal=gplans == [conv(p) for p in wplans[0]])
+                   plans_equal=gplans == [[conv(p) for p in row] for row in wplans])
         rec["ok"] = bool(rec["max_abs"] <= 2e-2 and rec["mean_abs"] <= 2e-3 and rec["plans_equal"])
         rec["kind"] = "ok" if rec["ok"] else "fail"
         if not rec["ok"] and rec["plans_equal"]:
-            rec["diag"] = diagnose(q, k, v, wplans[0], got, d)
+            rec["diag"] = [dict(x, batch=b) for b in range(B)
+                           for x in diagnose(q[b:b + 1], k[b:b + 1], v[b:b + 1], wplans[b], got[b:b + 1], d)]
             # an estimator near-tie (float64 gap below fp32 resolution) realised differently,
             # with the kernels exact on the device's own index
             if rec["diag"] and all(x.get("max_abs_vs_device_index", 1.0) <= 2e-2 and
