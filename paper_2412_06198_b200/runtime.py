@@ -409,9 +409,12 @@ def prefill(q, k, v, cfg: ModelConfig, search: SearchSpace | None = None, mode: 
     outputs = D.to_host_or_keep(y, q)
     cache = KvCache(batch, cfg.n_heads, cfg.d_head, cfg.max_context,
                     dtype=(k.dtype if D.is_torch(k) else np.asarray(k).dtype), kv_heads=kv_heads)
-    # fill from the staged device copies (no second host->device transfer)
-    cache.append(kd.view(batch, kv_heads, length, D.HEAD_DIM)[..., : cfg.d_head],
-                 vd.view(batch, kv_heads, length, D.HEAD_DIM)[..., : cfg.d_head])
+    if D.is_torch(k) and k.dtype == torch.bfloat16:
+        # fill from the staged device copies (no second host->device transfer)
+        cache.append(kd.view(batch, kv_heads, length, D.HEAD_DIM)[..., : cfg.d_head],
+                     vd.view(batch, kv_heads, length, D.HEAD_DIM)[..., : cfg.d_head])
+    else:  # the reference caches the rows as given (runtime.py:197), not their bf16 rounding
+        cache.append(k, v)
     cache._np = not D.is_torch(k)
     ev_end = torch.cuda.Event(enable_timing=True)
     ev_end.record()
@@ -528,6 +531,9 @@ def _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window
         raise NonFiniteError("q, k or v contains NaN or Inf")
     cache.length = n
     cache._np = False
+    if k.dtype != bf:  # the reference caches the rows as given (runtime.py:197), not their bf16 rounding
+        cache._k[:, :, :n].copy_(k)
+        cache._v[:, :, :n].copy_(v)
     if auto:
         nh = batch * H
         plans = plan.plans_from(small[1:1 + nh].astype(np.int64), small[1 + nh:].reshape(nh, 3), batch, H)

@@ -455,3 +455,28 @@ def test_decode_step_split_k(sa, H, HK, d, n, dt, B):
     want = torch.einsum("bhj,bhjd->bhd", torch.softmax(s.double(), 2).float(), vf).reshape(B, 1, H * d)
     err = (dec.output.float() - want).abs()
     assert err.max().item() <= MAX_ABS and err.mean().item() <= MEAN_ABS, (err.max().item(), err.mean().item())
+
+
+@pytest.mark.parametrize("kind", ["numpy", "cpu_torch", "cuda_f32"])
+def test_prefill_cache_keeps_input_rows(sa, kind):
+    """The reference caches k/v as given (runtime.py:197): fp32 inputs are not
+    replaced by their bf16 rounding, so a following decode is fp32-exact."""
+    import torch
+
+    rng = np.random.default_rng(91)
+    H, HK, n, d = 4, 2, 300, 128
+    q, k, v = (rng.uniform(-1, 1, (1, h, n + 1, d)).astype(np.float32) for h in (H, HK, HK))
+    conv = {"numpy": lambda x: x, "cpu_torch": lambda x: torch.from_numpy(np.ascontiguousarray(x)),
+            "cuda_f32": lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()}[kind]
+    cfg = sa.ModelConfig(n_heads=H, d_model=H * d, d_head=d, max_context=n + 1)
+    res = sa.prefill(conv(q[:, :, :n]), conv(k[:, :, :n]), conv(v[:, :, :n]), cfg, mode="dense")
+    keys = res.cache.keys()
+    keys = keys.cpu().numpy() if hasattr(keys, "cpu") else np.asarray(keys)
+    np.testing.assert_array_equal(keys, k[:, :, :n])
+    dec = sa.decode_step(conv(q[:, :, n:]), conv(k[:, :, n:]), conv(v[:, :, n:]), res.cache, cfg)
+    out = dec.output.cpu().numpy() if hasattr(dec.output, "cpu") else np.asarray(dec.output)
+    kk, vv = np.repeat(k, H // HK, axis=1)[0].astype(np.float64), np.repeat(v, H // HK, axis=1)[0].astype(np.float64)
+    s = np.einsum("hd,hnd->hn", q[0, :, n].astype(np.float64), kk) / np.sqrt(d)
+    w = np.exp(s - s.max(-1, keepdims=True))
+    w /= w.sum(-1, keepdims=True)
+    np.testing.assert_allclose(out.reshape(H, d), np.einsum("hn,hnd->hd", w, vv), atol=1e-5)
