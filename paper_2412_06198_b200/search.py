@@ -263,6 +263,13 @@ def select_pattern(m: AttnMatrices, s: SearchSpace, *, metric: str = "weights", 
         raise SearchError(f"n={m.n} exceeds the dense evaluation cap {dense_cap}; use select_pattern_windowed")
     cost_q_est = 0 if scoring == "exact" else min(q_est, m.n)
     refined = refined_candidates(s, m.n, m.d_head, cost_q_est)
+    if any(isinstance(rc.pattern, VerticalSlash) for rc in refined):
+        # the reference reaches this check in build_index of its first VS
+        # candidate (patterns.py:182-189); raising it before any device work
+        # keeps the same exception for the same call
+        from .patterns import _check_scoring_args
+
+        _check_scoring_args(m, scoring, min(q_est, m.n))
     fast = (metric == "weights" and scoring == "exact" and m.n <= SELECTOR_CAL_MAX
             and len(refined) <= 3 and counter is None)
     if fast:

@@ -80,6 +80,22 @@ CASES = {
     "space_density": lambda m: m.default_search_space(64, 8, density=0.0),
     "space_n": lambda m: m.default_search_space(0, 8),
     "flops_unknown": lambda m: m.estimate_flops(object(), 64, 8),
+    "flops_n": lambda m: m.estimate_flops(m.Triangular(4), 0, 8),
+    "refine_eps": lambda m: m.refine_candidate(m.Triangular(4), 64, 8, 1000, -1.0, 8),
+    "refine_iters": lambda m: m.refine_candidate(m.VerticalSlash(4, 4), 64, 8, 1000, 0.05, -1),
+    "select_metric": lambda m: m.select_pattern(_m(m), m.default_search_space(16, 8), metric="bogus"),
+    "select_scoring": lambda m: m.select_pattern(_m(m), m.default_search_space(16, 8), scoring="bogus"),
+    "select_qest0": lambda m: m.select_pattern(_m(m), m.default_search_space(16, 8), scoring="estimated", q_est=0),
+    "select_cap": lambda m: m.select_pattern(_m(m), m.default_search_space(16, 8), dense_cap=8),
+    "windowed_cal0": lambda m: m.select_pattern_windowed(_m(m), m.default_search_space(16, 8), 0),
+    "windowed_cal_big": lambda m: m.select_pattern_windowed(_m(m), m.default_search_space(16, 8), 17),
+    "prefill_cal_cap": lambda m: m.prefill(*_qkv((1, 2, 16, 8)), _cfg(m), mode="auto", cal_window=16,
+                                           dense_cap=8),
+    "sparse_block_kernel_vs": lambda m: m.vertical_slash_attention(
+        _m(m), m.SparseIndex(n=16, blocks=((0, 0),), block_size=16, always_diagonal=False)),
+    "index_col_range": lambda m: m.SparseIndex(n=16, columns=(16,)),
+    "index_causal": lambda m: m.SparseIndex(n=16, blocks=((0, 1),), block_size=8),
+    "realized_n": lambda m: m.realized_size(m.SparseIndex(n=16, columns=(1,)), 15),
 }
 
 
