@@ -480,3 +480,26 @@ def test_prefill_cache_keeps_input_rows(sa, kind):
     w = np.exp(s - s.max(-1, keepdims=True))
     w /= w.sum(-1, keepdims=True)
     np.testing.assert_allclose(out.reshape(H, d), np.einsum("hn,hnd->hd", w, vv), atol=1e-5)
+
+
+def test_decode_and_cache_errors(sa):
+    """Decode / KvCache error classes as the reference raises them
+    (runtime.py:222-225 decode_step, runtime.py:69-78 KvCache.append)."""
+    rng = np.random.default_rng(93)
+    H, d, n = 2, 8, 16
+    cfg = sa.ModelConfig(n_heads=H, d_model=H * d, d_head=d, max_context=n)
+    q, k, v = (rng.uniform(-1, 1, (1, H, n, d)).astype(np.float32) for _ in range(3))
+    res = sa.prefill(q, k, v, cfg, mode="dense")
+    one = (rng.uniform(-1, 1, (1, H, 1, d)).astype(np.float32) for _ in range(3))
+    with pytest.raises(sa.CacheOverflowError):  # capacity max_context = n is full
+        sa.decode_step(*one, res.cache, cfg)
+    two = [rng.uniform(-1, 1, (1, H, 2, d)).astype(np.float32) for _ in range(3)]
+    with pytest.raises(sa.DimensionError):
+        sa.decode_step(*two, res.cache, cfg)
+    empty = sa.KvCache(1, H, d, 8)
+    with pytest.raises(sa.SparseAttnError):
+        sa.decode_step(*(x[:, :, :1] for x in two), empty, cfg)
+    with pytest.raises(sa.DimensionError):
+        empty.append(two[1], two[2][:, :, :1])
+    with pytest.raises(sa.DimensionError):
+        empty.append(two[1][:, :1], two[2][:, :1])
