@@ -27,7 +27,8 @@
 namespace sa {
 
 constexpr int kCalMax = 64;
-constexpr int kSelThreads = 256;
+constexpr int kSelThreads = 512;
+constexpr int kLogitRows = kCalMax / (kSelThreads / 16);  // register tile rows per thread
 
 struct SelectArgs {
   const __nv_bfloat16* q;  // [HH, n, 128]
@@ -129,30 +130,30 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     }
   }
   __syncthreads();
-  // dense causal logits: each thread a 4x4 register tile of (row, column)
+  // dense causal logits: each thread a kLogitRows x 4 register tile of (row, column)
   {
-    const int tr = tid / 16, tc = tid % 16;  // rows tr + 16 i, columns tc + 16 j
-    float acc[4][4] = {};
+    constexpr int kRowStep = kSelThreads / 16;
+    const int tr = tid / 16, tc = tid % 16;  // rows tr + kRowStep i, columns tc + 16 j
+    float acc[kLogitRows][4] = {};
     if (tr < cal) {
 #pragma unroll 4
       for (int d = 0; d < kHeadDim; ++d) {
-        float qv[4], kv[4];
+        float qv[kLogitRows], kv[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          qv[i] = S.q[min(tr + 16 * i, kCalMax - 1)][d];
-          kv[i] = S.k[min(tc + 16 * i, kCalMax - 1)][d];
-        }
+        for (int i = 0; i < kLogitRows; ++i) qv[i] = S.q[min(tr + kRowStep * i, kCalMax - 1)][d];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) kv[j] = S.k[min(tc + 16 * j, kCalMax - 1)][d];
+#pragma unroll
+        for (int i = 0; i < kLogitRows; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(qv[i], kv[j], acc[i][j]);
       }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < kLogitRows; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int r = tr + 16 * i, c = tc + 16 * j;
+        const int r = tr + kRowStep * i, c = tc + 16 * j;
         if (r < cal && c < cal) S.L[r][c] = (c <= r) ? acc[i][j] * a.scale : 0.f;
       }
   }
