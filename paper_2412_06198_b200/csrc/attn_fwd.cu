@@ -150,7 +150,6 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 
   const long long t_entry = kProf ? clock64() : 0;
   const int warp = warp_id();
-  const int n_items = a.n_work ? *a.n_work : a.hh_total * a.nqt;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[B_Q], 1);
@@ -175,6 +174,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
+  // programmatic dependent launch: the prologue above overlapped the previous
+  // kernel; everything below may read its results
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int n_items = a.n_work ? *a.n_work : a.hh_total * a.nqt;
 
   if (warp == 4) {
     // ------------------------------------------------------------ producer
@@ -567,7 +570,7 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
                 const void* v, void* out, const sa_head_index* index, const int32_t* tile_off,
                 const int32_t* tile_cnt, const uint32_t* tiles, const int32_t* work, float* lse,
                 cudaStream_t cs, long long out_ld, int* counter, const int32_t* n_work,
-                void* const* peer_out, int n_peers) {
+                void* const* peer_out, int n_peers, bool counter_zeroed) {
   if (batch < 1 || heads < 1 || kv_heads < 1 || n < 1)
     return fail(SA_ERR_DIMENSION, "need batch, heads, kv_heads, n >= 1");
   if (heads % kv_heads != 0)
@@ -611,7 +614,9 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   a.work = work;
   a.counter = counter;
   a.n_work = n_work;
-  if (counter) cudaMemsetAsync(counter, 0, sizeof(int), cs);
+  // (a memset between the work-order kernel and this launch would defeat PDL:
+  // callers whose previous kernel already zeroed the counter say so)
+  if (counter && !counter_zeroed) cudaMemsetAsync(counter, 0, sizeof(int), cs);
   a.idx = *index;
   a.lse = lse;
   a.prof = reinterpret_cast<unsigned long long*>(sa_attn_dbg_ptr);
@@ -639,13 +644,33 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   }();
   const int grid = (int)std::min<long long>(2LL * num_sms, (long long)a.hh_total * a.nqt);
   // the need_weights path derives weights from lse: keep exact MUFU exps there
+  void (*kern)(AttnArgs);
   switch (lse != nullptr ? 0 : poly) {
-    case 2: attn_fwd_kernel<2><<<grid, kThreads, kSmemBytes, cs>>>(a); break;
-    case 3: attn_fwd_kernel<3><<<grid, kThreads, kSmemBytes, cs>>>(a); break;
-    case 4: attn_fwd_kernel<4><<<grid, kThreads, kSmemBytes, cs>>>(a); break;
-    case 8: attn_fwd_kernel<8><<<grid, kThreads, kSmemBytes, cs>>>(a); break;
-    default: attn_fwd_kernel<0><<<grid, kThreads, kSmemBytes, cs>>>(a); break;
+    case 2: kern = attn_fwd_kernel<2>; break;
+    case 3: kern = attn_fwd_kernel<3>; break;
+    case 4: kern = attn_fwd_kernel<4>; break;
+    case 8: kern = attn_fwd_kernel<8>; break;
+    default: kern = attn_fwd_kernel<0>; break;
   }
+  // programmatic dependent launch: the CTAs become resident and run their
+  // prologue (barriers, TMEM, tensor-map prefetch) while the previous kernel
+  // in the stream (the work-order kernel) finishes; griddepcontrol.wait in the
+  // kernel orders every global read after it (SA_PDL=0: plain launch)
+  static const bool pdl = [] {
+    const char* e = getenv("SA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = cs;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && counter_zeroed) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, a);
   return check_launch("attn_fwd_kernel");
 }
 

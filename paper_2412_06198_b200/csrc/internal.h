@@ -64,10 +64,11 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
                 const void* v, void* out, const sa_head_index* index, const int32_t* tile_off,
                 const int32_t* tile_cnt, const uint32_t* tiles, const int32_t* work, float* lse,
                 cudaStream_t st, long long out_ld = 0, int* counter = nullptr,
-                const int32_t* n_work = nullptr, void* const* peer_out = nullptr, int n_peers = 0);
+                const int32_t* n_work = nullptr, void* const* peer_out = nullptr, int n_peers = 0,
+                bool counter_zeroed = false);
 
 // tiles.cu: heaviest-first order of the items with a nonzero cost; *n_work = their number
 int launch_order_work(const int32_t* cost, int items, int max_cost, int32_t* work, int32_t* n_work,
-                      cudaStream_t st, int nqt = 0, int group = 0);
+                      cudaStream_t st, int nqt = 0, int group = 0, int32_t* zero_counter = nullptr);
 
 }  // namespace sa

@@ -433,10 +433,11 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
     return !(e && e[0] == '0');
   }();
   if (lpt && (rc = launch_order_work(V.tile_cnt, p.hh * p.nqt, p.nqt, work, n_work, st, p.nqt,
-                                     sib ? H / HK : 1)))
+                                     sib ? H / HK : 1, counter)))
     return rc;
   rc = launch_attn(B, H, HK, n, desc->scale, q, k, v, out, &V.index, V.tile_off, V.tile_cnt, V.tiles,
-                   lpt ? work : nullptr, nullptr, st, desc->out_ld, counter, lpt ? n_work : nullptr);
+                   lpt ? work : nullptr, nullptr, st, desc->out_ld, counter, lpt ? n_work : nullptr, nullptr, 0,
+                   lpt);
   mark(4);
   return rc;
 }

@@ -174,7 +174,8 @@ __device__ __forceinline__ int sibling_item(int p, int nqt, int g) {
 }
 __global__ void __launch_bounds__(1024) order_work_kernel(const int32_t* __restrict__ cnt, int items,
                                                           int max_cnt, int32_t* __restrict__ work,
-                                                          int32_t* __restrict__ n_work, int nqt, int g) {
+                                                          int32_t* __restrict__ n_work, int nqt, int g,
+                                                          int32_t* __restrict__ zero_counter) {
   // bins: tile count >> shift, at most 1023 (one per thread) plus the empty bin, heaviest first
   __shared__ int start[1024];
   __shared__ int wsum[32];
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(1024) order_work_kernel(const int32_t* __restr
   __syncthreads();
   start[t] = wsum[w] + x - v;
   if (t == 1023 && n_work) *n_work = start[t];
+  if (t == 0 && zero_counter) *zero_counter = 0;  // the attention kernel's item counter
   __syncthreads();
   // scatter: warp-aggregated, so lanes of one bin take consecutive positions in lane order
   for (int p0 = t - lane; p0 < items; p0 += kB * (int)blockDim.x) {
@@ -277,18 +279,18 @@ extern "C" int sa_order_work(const int32_t* tile_cnt, int items, int max_cnt, in
   if (items < 1 || max_cnt < 0 || max_cnt > 65536) return fail(SA_ERR_DIMENSION, "bad work-order sizes");
   if (!tile_cnt || !work) return fail(SA_ERR_DIMENSION, "null pointer");
   order_work_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      tile_cnt, items, max_cnt, work, nullptr, items, 1);
+      tile_cnt, items, max_cnt, work, nullptr, items, 1, nullptr);
   return check_launch("order_work_kernel");
 }
 
 namespace sa {
 int launch_order_work(const int32_t* cost, int items, int max_cost, int32_t* work, int32_t* n_work,
-                      cudaStream_t st, int nqt, int group) {
+                      cudaStream_t st, int nqt, int group, int32_t* zero_counter) {
   if (nqt < 1 || group < 1 || items % (nqt * group) != 0) {
     nqt = items;
     group = 1;
   }
-  order_work_kernel<<<1, 1024, 0, st>>>(cost, items, max_cost, work, n_work, nqt, group);
+  order_work_kernel<<<1, 1024, 0, st>>>(cost, items, max_cost, work, n_work, nqt, group, zero_counter);
   return check_launch("order_work_kernel");
 }
 }  // namespace sa
