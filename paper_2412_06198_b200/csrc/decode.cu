@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kDecThreads, 3) decode_partial_kernel(const fl
 // chunks s.  All chunk statistics are read in parallel (the weights land in
 // shared memory), then thread c sums column c over the chunks with 8 loads in
 // flight.
-constexpr int kDecMaxSplit = 1024;  // chunks per kv head (262144 keys / 256 at most)
+constexpr int kDecMaxSplit = 8192;  // chunks per kv head: up to 8M cached rows at 1024 keys per chunk
 
 // keys per CTA for n cached rows over `groups` = batch * kv_heads
 static int dec_chunk(int n, int groups) {
@@ -314,7 +314,8 @@ extern "C" int sa_decode_attn(int batch, int heads, int kv_heads, int n, int d, 
     return fail(SA_ERR_DIMENSION, "bad decode shape (batch %d, heads %d, kv_heads %d, n %d)", batch, heads, kv_heads, n);
   if (d < 1 || d > kDecMaxD) return fail(SA_ERR_DIMENSION, "decode head_dim must be in [1, 128], got %d", d);
   if (capacity < n) return fail(SA_ERR_DIMENSION, "cache capacity %d below length %d", capacity, n);
-  if (n > kDecMaxSplit * 256) return fail(SA_ERR_DIMENSION, "decode supports up to %d cached rows", kDecMaxSplit * 256);
+  if ((long long)n > (long long)kDecMaxSplit * kDecChunkMax)
+    return fail(SA_ERR_DIMENSION, "decode supports up to %lld cached rows", (long long)kDecMaxSplit * kDecChunkMax);
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(SA_ERR_DIMENSION, "bad scale");
   if (!q || !k_cache || !v_cache || !out || !ws) return fail(SA_ERR_DIMENSION, "null pointer argument");
   if (ws_bytes < sa_decode_workspace(batch, heads, kv_heads, n, d)) return fail(SA_ERR_DIMENSION, "decode workspace too small");

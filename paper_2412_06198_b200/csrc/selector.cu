@@ -62,15 +62,6 @@ struct SelectSmem {
   double red[kSelThreads / 32];
 };
 
-// stable top-k by rank: selected iff #{better} < k, better = larger score or
-// equal score at a lower index (patterns.py:231-234)
-__device__ __forceinline__ bool rank_selected(const double* s, int len, int j, int k) {
-  int better = 0;
-  const double v = s[j];
-  for (int i = 0; i < len; ++i) better += (s[i] > v) || (s[i] == v && i < j);
-  return better < k;
-}
-
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -177,19 +168,44 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
   const int p1 = ci == 0 ? a.cand_p1[0] : (ci == 1 ? a.cand_p1[1] : a.cand_p1[2]);
   const int p2 = ci == 0 ? a.cand_p2[0] : (ci == 1 ? a.cand_p2[1] : a.cand_p2[2]);
   if (fam == FAM_VS) {
-    // exact scoring over all cal rows (patterns.py:182-202), float64 sums
-    for (int j = tid; j < cal; j += kSelThreads) {
-      double cs = 0.0, ds = 0.0;
-      for (int r = 0; r < cal; ++r) cs += (double)S.Wd[r][j];
-      for (int r = j; r < cal; ++r) ds += (double)S.Wd[r][r - j];
+    // exact scoring over all cal rows (patterns.py:182-202), float64 sums;
+    // 8 threads per column / offset j, each over every 8th row, lane-reduced
+    static_assert(kSelThreads >= 8 * kCalMax, "one 8-lane group per column");
+    const int j = tid >> 3, part = tid & 7;
+    double cs = 0.0, ds = 0.0;
+    if (j < cal)
+      for (int r = part; r < cal; r += 8) {
+        cs += (double)S.Wd[r][j];
+        if (r >= j) ds += (double)S.Wd[r][r - j];
+      }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      cs += __shfl_xor_sync(0xffffffffu, cs, o);
+      ds += __shfl_xor_sync(0xffffffffu, ds, o);
+    }
+    if (part == 0 && j < cal) {
       S.colscore[j] = cs;
       S.diagscore[j] = ds;
     }
     __syncthreads();
+    // stable top-k by rank (patterns.py:231-234): selected iff #{better} < k
     const int kv = min(p1, cal), ks = min(p2, cal);
-    for (int j = tid; j < cal; j += kSelThreads) {
-      S.colsel[j] = rank_selected(S.colscore, cal, j, kv);
-      S.diagsel[j] = rank_selected(S.diagscore, cal, j, ks);
+    int bc = 0, bd = 0;
+    if (j < cal) {
+      const double vc = S.colscore[j], vd = S.diagscore[j];
+      for (int i = part; i < cal; i += 8) {
+        bc += (S.colscore[i] > vc) || (S.colscore[i] == vc && i < j);
+        bd += (S.diagscore[i] > vd) || (S.diagscore[i] == vd && i < j);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      bc += __shfl_xor_sync(0xffffffffu, bc, o);
+      bd += __shfl_xor_sync(0xffffffffu, bd, o);
+    }
+    if (part == 0 && j < cal) {
+      S.colsel[j] = bc < kv;
+      S.diagsel[j] = bd < ks;
     }
     __syncthreads();
   } else if (fam == FAM_BLOCK) {

@@ -2,7 +2,7 @@
 // need_weights=True return of patterns.py:422-434 / 466-467 and core.py:152),
 // plus an fp32 block_mean for the per-head API (patterns.py:279-287).
 //
-// Weights are a debug/selection-size path (n <= 4096, search.DENSE_EVAL_CAP):
+// Weights are a debug/selection-size path (typically n <= 4096, search.DENSE_EVAL_CAP):
 // w[i, j] = exp(q_i . k_j * scale - lse_i) on the index, 0 elsewhere, with the
 // row log-sum-exp taken from the attention kernel so rows match its softmax.
 #include <cuda_bf16.h>
@@ -81,7 +81,9 @@ extern "C" int sa_attn_weights(int heads, int kv_heads, int n, int hh, float sca
                                const void* k, const float* lse, const sa_head_index* index,
                                float* w, void* stream) {
   using namespace sa;
-  if (n < 1 || n > 16384) return fail(SA_ERR_DIMENSION, "weights path supports 1 <= n <= 16384");
+  // the dense n x n result is what the reference returns (numpy, any n); the
+  // only limit here is the 16-row grid (y < 65536 blocks)
+  if (n < 1 || n > 65535 * 16) return fail(SA_ERR_DIMENSION, "weights path supports 1 <= n <= %d", 65535 * 16);
   if (heads < 1 || kv_heads < 1 || heads % kv_heads) return fail(SA_ERR_DIMENSION, "bad head layout");
   if (!q || !k || !lse || !index || !w) return fail(SA_ERR_DIMENSION, "null pointer argument");
   const int b = hh / heads, h = hh % heads;

@@ -503,3 +503,25 @@ def test_decode_and_cache_errors(sa):
         empty.append(two[1], two[2][:, :, :1])
     with pytest.raises(sa.DimensionError):
         empty.append(two[1][:, :1], two[2][:, :1])
+
+
+def test_decode_past_prefill_limit(sa):
+    """A cache filled to the prefill limit (262144 rows) keeps decoding: the
+    split-K kernel takes up to 8M cached rows (1024-key chunks)."""
+    H, HK, d, n = 4, 1, 128, 262144 + 1000
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    k, v = ((torch.rand((1, HK, n, d), generator=g, device="cuda") * 2 - 1).bfloat16() for _ in range(2))
+    q = (torch.rand((1, H, 1, d), generator=g, device="cuda") * 2 - 1).bfloat16()
+    cfg = sa.ModelConfig(n_heads=H, d_model=H * d, d_head=d, max_context=n + 1)
+    cache = sa.KvCache(1, H, d, n + 1, dtype=torch.bfloat16, kv_heads=HK)
+    cache.append(k, v)
+    kn, vn = ((torch.rand((1, HK, 1, d), generator=g, device="cuda") * 2 - 1).bfloat16() for _ in range(2))
+    dec = sa.decode_step(q, kn, vn, cache, cfg)
+    kf = torch.cat([k, kn], 2).float().repeat_interleave(H // HK, 1)[0]
+    vf = torch.cat([v, vn], 2).float().repeat_interleave(H // HK, 1)[0]
+    s = torch.einsum("hd,hjd->hj", q[0, :, 0].float(), kf) / math.sqrt(d)
+    want = torch.einsum("hj,hjd->hd", torch.softmax(s.double(), 1).float(), vf).reshape(1, 1, H * d)
+    err = (dec.output.float() - want).abs()
+    assert dec.cache.length == n + 1
+    assert err.max().item() <= MAX_ABS and err.mean().item() <= MEAN_ABS
