@@ -182,7 +182,7 @@ int sa_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b, f
 
 /* Dense [n, n] fp32 weights of head hh under `index` (need_weights=True of
  * patterns.py:422-434, 466-467; core.py:152), rows normalised by the lse that
- * sa_attn_sparse returned.  n <= 16384. */
+ * sa_attn_sparse returned.  n <= 1048560 (the caller owns the n * n * 4 bytes). */
 int sa_attn_weights(int heads, int kv_heads, int n, int hh, float scale, const void* q,
                     const void* k, const float* lse, const sa_head_index* index, float* w,
                     void* stream);
@@ -207,7 +207,7 @@ int sa_order_work(const int32_t* tile_cnt, int items, int max_cnt, int32_t* work
  * queries q [batch * heads, d] fp32 attend densely over the first n rows of a
  * KV cache laid out [batch, kv_heads, capacity, d] (kv_dtype 0 = fp32,
  * 1 = bf16), out [batch * heads, d] fp32.  Split-K over 256-1024-key chunks, K/V
- * read in place once per kv head; ws >= sa_decode_workspace(...). */
+ * read in place once per kv head; n <= 8388608; ws >= sa_decode_workspace(...). */
 size_t sa_decode_workspace(int batch, int heads, int kv_heads, int n, int d);
 int sa_decode_attn(int batch, int heads, int kv_heads, int n, int d, int capacity, float scale, const float* q,
                    const void* k_cache, const void* v_cache, int kv_dtype, float* out, void* ws, size_t ws_bytes,
