@@ -63,6 +63,11 @@ typedef struct {
   int32_t p1, p2;
 } sa_pattern;
 
+/* Most candidates one auto-mode selection holds (cand / full below, the
+ * [HH, SA_MAX_CAND] error rows of sa_prefill_view).  The reference's default
+ * search space has 3 (search.py:322-357). */
+#define SA_MAX_CAND 16
+
 typedef enum { SA_MODE_DENSE = 0, SA_MODE_FIXED = 1, SA_MODE_AUTO = 2 } sa_prefill_mode;
 
 /* One layer of runtime.prefill (runtime.py:134-206).  `cand` are the
@@ -76,9 +81,9 @@ typedef struct {
   sa_pattern fixed;      /* SA_MODE_FIXED                                    */
   int32_t q_est;         /* estimated-scoring rows (runtime.py:170)          */
   int32_t cal;           /* SA_MODE_AUTO: calibration window (<= 64)         */
-  int32_t ncand;         /* SA_MODE_AUTO: 1..3                               */
-  sa_pattern cand[3];
-  sa_pattern full[3];
+  int32_t ncand;         /* SA_MODE_AUTO: 1..SA_MAX_CAND                     */
+  sa_pattern cand[SA_MAX_CAND];
+  sa_pattern full[SA_MAX_CAND];
   int32_t preselected;   /* SA_MODE_AUTO: 1 = the caller already wrote the
                             per-head choice into view.choice (skip the selector) */
   void* stage_events[6]; /* optional cudaEvent_t, recorded on `stream` after:
@@ -97,7 +102,7 @@ typedef struct {
 typedef struct {
   int32_t* choice;      /* [HH] chosen candidate (auto)                      */
   int32_t* family;      /* [HH]                                              */
-  double* errors;       /* [HH, 3] window Frobenius errors (auto)            */
+  double* errors;       /* [HH, SA_MAX_CAND] window Frobenius errors (auto)  */
   float* col_scores;    /* [HH, n] estimated column mass (VS heads)          */
   float* diag_scores;   /* [HH, n] estimated diagonal mass (VS heads)        */
   int32_t* col_idx;     /* [HH, col_ld] selected columns, ascending          */
@@ -130,7 +135,7 @@ int sa_memcpy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, 
 
 /* ---- selector: search.select_pattern_windowed (search.py:276-319) -------- */
 /* Candidate arrays are HOST arrays of length ncand (refined at window scale).
- * choice_out / family_out: [HH]; err_out: [HH, 3] float64 (nullable). */
+ * choice_out / family_out: [HH]; err_out: [HH, SA_MAX_CAND] float64 (nullable). */
 int sa_select_windowed(int batch, int heads, int kv_heads, int n, int cal, float scale,
                        const void* q, const void* k, int ncand, const int32_t* cand_fam_host,
                        const int32_t* cand_p1_host, const int32_t* cand_p2_host,

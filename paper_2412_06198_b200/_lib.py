@@ -44,6 +44,9 @@ class sa_head_index(ctypes.Structure):
     ]
 
 
+MAX_CAND = 16  # SA_MAX_CAND (include/sparseattn_b200.h): candidates per auto selection
+
+
 class sa_pattern(ctypes.Structure):
     _fields_ = [("family", ctypes.c_int32), ("p1", ctypes.c_int32), ("p2", ctypes.c_int32)]
 
@@ -60,8 +63,8 @@ class sa_prefill_desc(ctypes.Structure):
         ("q_est", ctypes.c_int32),
         ("cal", ctypes.c_int32),
         ("ncand", ctypes.c_int32),
-        ("cand", sa_pattern * 3),
-        ("full", sa_pattern * 3),
+        ("cand", sa_pattern * MAX_CAND),
+        ("full", sa_pattern * MAX_CAND),
         ("preselected", ctypes.c_int32),
         ("stage_events", ctypes.c_void_p * 6),
         ("out_ld", ctypes.c_int64),

@@ -626,22 +626,16 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
     const int v = e ? atoi(e) : kDefaultPoly;
     return (v == 0 || v == 2 || v == 3 || v == 4 || v == 8) ? v : kDefaultPoly;
   }();
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_done{0};
+  once_per_device(attr_done, [] {
     cudaFuncSetAttribute(attn_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     cudaFuncSetAttribute(attn_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     cudaFuncSetAttribute(attn_fwd_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     cudaFuncSetAttribute(attn_fwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     cudaFuncSetAttribute(attn_fwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    attr_set = true;
-  }
+  });
   // persistent: two CTAs per SM (113 KB shared memory and 256 TMEM columns each)
-  static const int num_sms = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
+  const int num_sms = device_sm_count();
   const int grid = (int)std::min<long long>(2LL * num_sms, (long long)a.hh_total * a.nqt);
   // the need_weights path derives weights from lse: keep exact MUFU exps there
   void (*kern)(AttnArgs);

@@ -463,15 +463,14 @@ int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_
         blk_row_off, hh_total, nb, k_b + 1, row_stride, head_stride, gate, gate_val);
     if ((rc = check_launch("fixed_row_off_kernel"))) return rc;
   }
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_done{0};
+  once_per_device(attr_done, [] {
     cudaFuncSetAttribute(block_score_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);
     cudaFuncSetAttribute(block_score_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);
     cudaFuncSetAttribute(block_score_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);
     cudaFuncSetAttribute(block_score_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);
     cudaFuncSetAttribute(block_score_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);
-    attr = true;
-  }
+  });
   if (k_b <= 8) {
     a.hh_base = 0;
     a.hh_count = hh_total;

@@ -580,18 +580,12 @@ int launch_score_tail(int batch, int heads, int kv_heads, int n, float scale, co
     // columns past the last scored row never receive mass
     cudaMemsetAsync(col_out, 0, (size_t)a.hh_total * n * sizeof(float), st);
   }
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_done{0};
+  once_per_device(attr_done, [] {
     cudaFuncSetAttribute(tail_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem_bytes(1));
     cudaFuncSetAttribute(tail_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem_bytes(2));
-    attr = true;
-  }
-  static int num_sms = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
+  });
+  const int num_sms = device_sm_count();
   const int grid = std::min(num_sms, a.hh_total * a.nchunks);
   tail_kernel<1><<<grid, kTailThreads, tail_smem_bytes(1), st>>>(a);
   if ((rc = check_launch("tail_kernel<1>"))) return rc;

@@ -2,11 +2,40 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "sparseattn_b200.h"
 
 namespace sa {
+
+// Kernel attributes (cudaFuncSetAttribute) and the SM count belong to a device
+// context, so one-time setup is remembered per device: `once_per_device(done,
+// f)` runs f the first time the calling thread's current device is seen (two
+// threads racing both run f, which is idempotent).
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+template <class F>
+inline void once_per_device(std::atomic<uint64_t>& done, F&& f) {
+  const uint64_t bit = 1ull << (current_device() & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  f();
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
+inline int device_sm_count() {
+  static std::atomic<int> sms[64];
+  const int dev = current_device();
+  int v = sms[dev & 63].load(std::memory_order_relaxed);
+  if (v == 0) {
+    v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 
 struct TopkArgs {
   const float* scores;

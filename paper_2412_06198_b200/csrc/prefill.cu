@@ -6,7 +6,7 @@
 // synchronisation: the per-head choice lives in device memory and gates the
 // estimator launches.
 //
-//   [auto]  select_kernel            -> choice[HH], family[HH], errors[HH, 3]
+//   [auto]  select_kernel            -> choice[HH], family[HH], errors[HH, SA_MAX_CAND]
 //   apply_choice_kernel              -> family / Triangular params / block side per head
 //   [VS]    score_tail (gated)       -> col[HH, n], diag[HH, n]
 //           topk (gated per cand)    -> column bitmap, reversed diagonal bitmap, id lists
@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -65,7 +66,7 @@ enum WsSlot {
 struct Plan {
   int hh, hk, n, nqt;
   int ncand;
-  sa_pattern cand[3];  // patterns at full n (clamped like build_index)
+  sa_pattern cand[SA_MAX_CAND];  // patterns at full n (clamped like build_index)
   int q_est;
   int vs_words;
   int any_vs, any_block;
@@ -127,7 +128,8 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
     p->ncand = 1;
     if ((rc = clamp_pattern(d->fixed, n, &p->cand[0]))) return rc;
   } else if (d->mode == SA_MODE_AUTO) {
-    if (d->ncand < 1 || d->ncand > 3) return fail(SA_ERR_SEARCH, "candidate list must hold 1..3 patterns");
+    if (d->ncand < 1 || d->ncand > SA_MAX_CAND)
+      return fail(SA_ERR_SEARCH, "candidate list must hold 1..%d patterns", SA_MAX_CAND);
     if (d->cal < 1 || d->cal > n) return fail(SA_ERR_SEARCH, "cal_window must be in [1, %d]", n);
     p->ncand = d->ncand;
     for (int c = 0; c < d->ncand; ++c) {
@@ -156,6 +158,10 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
       blk_ws = std::max(blk_ws, block_select_ws(n, pt.p1, pt.p2, p->hh));
     }
   }
+  // block rows are addressed with int32 offsets (hh * head_stride + row * stride)
+  if ((long long)p->hh * head_stride > INT32_MAX)
+    return fail(SA_ERR_DIMENSION, "block index of %d heads x %lld entries exceeds the int32 row offsets",
+                p->hh, head_stride);
   p->blk_row_stride = p->max_nb + 1;
   p->blk_head_stride = head_stride;
   p->blk_ws = blk_ws;
@@ -169,7 +175,7 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
   const size_t hh = p->hh;
   sz[W_CHOICE] = hh * 4;
   sz[W_FAMILY] = hh * 4;
-  sz[W_ERR] = hh * 3 * 8;
+  sz[W_ERR] = hh * SA_MAX_CAND * 8;
   sz[W_TRIW] = hh * 4;
   sz[W_TRIS] = hh * 4;
   sz[W_COLBITS] = hh * p->vs_words * 4;
@@ -201,7 +207,7 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
 struct ApplyArgs {
   int hh;
   int ncand;
-  sa_pattern cand[3];
+  sa_pattern cand[SA_MAX_CAND];
   const int32_t* choice;  // null -> candidate 0 for every head
   int32_t* family;
   int32_t* tri_w;
@@ -304,7 +310,7 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
     choice = V.choice;
   } else if (desc->mode == SA_MODE_AUTO) {
     choice = V.choice;
-    int32_t fam[3], p1[3], p2[3];
+    int32_t fam[SA_MAX_CAND], p1[SA_MAX_CAND], p2[SA_MAX_CAND];
     for (int c = 0; c < p.ncand; ++c) {
       fam[c] = desc->cand[c].family;
       p1[c] = desc->cand[c].p1;

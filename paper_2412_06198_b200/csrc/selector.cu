@@ -37,12 +37,12 @@ struct SelectArgs {
   int cal;
   float scale;
   int ncand;
-  int cand_fam[3];  // family of candidate c (0 tri, 1 vs, 2 block)
-  int cand_p1[3];   // tri window / vs k_v / block b
-  int cand_p2[3];   // tri sinks / vs k_s / block k_b
+  int cand_fam[SA_MAX_CAND];  // family of candidate c (0 tri, 1 vs, 2 block)
+  int cand_p1[SA_MAX_CAND];   // tri window / vs k_v / block b
+  int cand_p2[SA_MAX_CAND];   // tri sinks / vs k_s / block k_b
   int32_t* choice_out;  // [HH] index of the chosen candidate
   int32_t* family_out;  // [HH] family of the chosen candidate (optional)
-  double* err_out;      // [HH, 3] Frobenius errors (optional)
+  double* err_out;      // [HH, SA_MAX_CAND] Frobenius errors (optional)
 };
 
 struct SelectSmem {
@@ -294,26 +294,29 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
   if (tid == 0) {
     double tot = 0.0;
     for (int w = 0; w < kWarps; ++w) tot += S.red[w];
-    a.err_out[(size_t)hh * 3 + ci] = sqrt(tot);
+    a.err_out[(size_t)hh * SA_MAX_CAND + ci] = sqrt(tot);
   }
 }
 
 // strict-< argmin in candidate order (search.py:245-250: earlier wins ties)
-__global__ void select_argmin_kernel(const double* err, int hh_total, int ncand, const int32_t* fam,
-                                     int32_t* choice_out, int32_t* family_out, int f0, int f1, int f2) {
+struct CandFamilies {
+  int f[SA_MAX_CAND];
+};
+__global__ void select_argmin_kernel(const double* err, int hh_total, int ncand, int32_t* choice_out,
+                                     int32_t* family_out, CandFamilies fam) {
   const int hh = blockIdx.x * blockDim.x + threadIdx.x;
   if (hh >= hh_total) return;
   double best = INFINITY;
   int best_c = 0;
   for (int c = 0; c < ncand; ++c) {
-    const double e = err[(size_t)hh * 3 + c];
+    const double e = err[(size_t)hh * SA_MAX_CAND + c];
     if (e < best) {
       best = e;
       best_c = c;
     }
   }
   choice_out[hh] = best_c;
-  if (family_out) family_out[hh] = best_c == 0 ? f0 : (best_c == 1 ? f1 : f2);
+  if (family_out) family_out[hh] = fam.f[best_c];
 }
 
 }  // namespace sa
@@ -327,7 +330,8 @@ int launch_select(int batch, int heads, int kv_heads, int n, int cal, float scal
     return fail(SA_ERR_DIMENSION, "bad head layout");
   if (cal < 1 || cal > n) return fail(SA_ERR_SEARCH, "cal_window must be in [1, %d], got %d", n, cal);
   if (cal > kCalMax) return fail(SA_ERR_SEARCH, "device selector supports cal_window <= %d", kCalMax);
-  if (ncand < 1 || ncand > 3) return fail(SA_ERR_SEARCH, "candidate list must hold 1..3 patterns");
+  if (ncand < 1 || ncand > SA_MAX_CAND)
+    return fail(SA_ERR_SEARCH, "candidate list must hold 1..%d patterns", SA_MAX_CAND);
   SelectArgs a{};
   a.q = reinterpret_cast<const __nv_bfloat16*>(q);
   a.k = reinterpret_cast<const __nv_bfloat16*>(k);
@@ -347,29 +351,33 @@ int launch_select(int batch, int heads, int kv_heads, int n, int cal, float scal
   a.choice_out = choice_out;
   a.family_out = family_out;
   a.err_out = err_out;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(SelectSmem));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  once_per_device(attr_done, [] {
+    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SelectSmem));
+  });
   if (!a.err_out) {  // callers that do not want the errors still need a scratch row per head
-    static double* scratch = nullptr;
-    static int scratch_heads = 0;
-    if (scratch_heads < a.hh_total) {
-      if (scratch) cudaFree(scratch);
-      if (cudaMalloc(&scratch, (size_t)a.hh_total * 3 * sizeof(double)) != cudaSuccess)
+    // per (thread, device): a buffer freed while another stream uses it would race
+    struct Scratch {
+      double* p = nullptr;
+      int heads = 0;
+    };
+    static thread_local Scratch tab[64];
+    Scratch& s = tab[current_device() & 63];
+    if (s.heads < a.hh_total) {
+      if (s.p) cudaFree(s.p);
+      if (cudaMalloc(&s.p, (size_t)a.hh_total * SA_MAX_CAND * sizeof(double)) != cudaSuccess)
         return fail(SA_ERR_CUDA, "selector scratch allocation failed");
-      scratch_heads = a.hh_total;
+      s.heads = a.hh_total;
     }
-    a.err_out = scratch;
+    a.err_out = s.p;
   }
   select_kernel<<<dim3(a.hh_total, ncand), kSelThreads, sizeof(SelectSmem), stream>>>(a);
   int rc = check_launch("select_kernel");
   if (rc) return rc;
-  select_argmin_kernel<<<(a.hh_total + 127) / 128, 128, 0, stream>>>(
-      a.err_out, a.hh_total, ncand, nullptr, choice_out, family_out, a.cand_fam[0],
-      ncand > 1 ? a.cand_fam[1] : 0, ncand > 2 ? a.cand_fam[2] : 0);
+  CandFamilies fams{};
+  for (int c = 0; c < ncand; ++c) fams.f[c] = a.cand_fam[c];
+  select_argmin_kernel<<<(a.hh_total + 127) / 128, 128, 0, stream>>>(a.err_out, a.hh_total, ncand, choice_out,
+                                                                    family_out, fams);
   return check_launch("select_argmin_kernel");
 }
 }  // namespace sa
@@ -406,7 +414,7 @@ __global__ void select_family_kernel(const double* err, long long ld, int rows, 
 extern "C" int sa_select_family(const double* err, long long ld, int rows, int ncand, int32_t* choice_out,
                                 void* stream) {
   using namespace sa;
-  if (rows < 0 || ncand < 1 || ncand > 3 || ld < ncand) return fail(SA_ERR_SEARCH, "bad error matrix shape");
+  if (rows < 0 || ncand < 1 || ld < ncand) return fail(SA_ERR_SEARCH, "bad error matrix shape");
   if (rows == 0) return SA_OK;
   if (!err || !choice_out) return fail(SA_ERR_DIMENSION, "null pointer");
   select_family_kernel<<<(rows + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(err, ld, rows, ncand,

@@ -656,14 +656,13 @@ int launch_topk(const TopkArgs& a, cudaStream_t st) {
   // longer plain rows by a cluster of kClusterC CTAs
   constexpr int kCacheMax = 49152;
   const int cl_per = (((a.n + kClusterC - 1) / kClusterC) + 3) & ~3;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_done{0};
+  once_per_device(attr_done, [] {
     cudaFuncSetAttribute(topk_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kTopkSmem + kCacheMax * 4);
     cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kTopkSmem + ((262144 / kClusterC) + 4) * 4);
-    attr = true;
-  }
+  });
   if (a.lens == nullptr && a.ks == nullptr && a.n >= kClusterMin && a.n <= 262144 && threads == kTopkThreads) {
     topk_cluster_kernel<<<rows * kClusterC, kTopkThreads, kTopkSmem + cl_per * 4, st>>>(a);
     return check_launch("topk_cluster_kernel");

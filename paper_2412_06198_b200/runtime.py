@@ -20,8 +20,8 @@ import torch
 
 from . import _device as D
 from . import _lib
-from .errors import CacheOverflowError, DimensionError, NonFiniteError, SparseAttnError
-from .patterns import BlockSparse, Triangular, VerticalSlash
+from .errors import CacheOverflowError, DimensionError, NonFiniteError, SearchError, SparseAttnError
+from .patterns import BlockSparse, PatternParamError, Triangular, VerticalSlash
 from .search import (
     DENSE_EVAL_CAP,
     SELECTOR_CAL_MAX,
@@ -186,6 +186,8 @@ class PrefillPlan:
         self.scale = 1.0 / math.sqrt(d_head)
         self.cal = min(cal_window, length)
         self.q_est = min(q_est, length)
+        if mode == "auto" and self.cal < 1:  # select_pattern_windowed (search.py:290-291)
+            raise SearchError(f"cal_window must be in [1, {length}], got {self.cal}")
         d = _lib.sa_prefill_desc()
         d.batch, d.heads, d.kv_heads, d.n = batch, heads, kv_heads, length
         d.scale = self.scale
@@ -203,8 +205,9 @@ class PrefillPlan:
         else:
             d.mode = MODE_AUTO
             space = search if search is not None else default_search_space(self.cal, d_head)
-            if len(space.candidates) > 3:
-                raise SparseAttnError("the device selector supports up to 3 candidates")
+            if len(space.candidates) > _lib.MAX_CAND:
+                raise SearchError(f"the device selector holds at most {_lib.MAX_CAND} candidates, "
+                                  f"got {len(space.candidates)}")
             # select_pattern(scoring="exact") refines with cost_q_est = 0 (search.py:235)
             self.refined = refined_candidates(space, self.cal, d_head, 0)
             if self.cal == length:
@@ -216,10 +219,16 @@ class PrefillPlan:
                 d.cand[c].family, d.cand[c].p1, d.cand[c].p2 = pattern_params(rc.pattern)
                 d.full[c].family, d.full[c].p1, d.full[c].p2 = pattern_params(fp)
             d.preselected = 1
+        # build_index(mode="estimated", q_est) of a vertical-slash head rejects
+        # q_est < 1 (runtime.py:187, patterns.py:182-189); raised before any work
+        vs_possible = (mode == "fixed" and isinstance(fixed_pattern, VerticalSlash)) or \
+            (mode == "auto" and any(isinstance(p, VerticalSlash) for p in self.full))
+        if vs_possible and self.q_est < 1:
+            raise PatternParamError(f"q_est must be in [1, {length}], got {self.q_est}")
         self.desc = d
         self.ws_bytes = int(_lib.load().sa_prefill_workspace_size(d))
-        if self.ws_bytes == 0:
-            _lib.check(1 if "exceeds" in _lib.load().sa_last_error().decode() else 4)
+        if self.ws_bytes == 0:  # the plan was rejected: re-run it for its status code
+            _lib.check(_lib.load().sa_prefill_views(d, None, None))
 
     @property
     def hh(self) -> int:
@@ -234,35 +243,41 @@ class PrefillPlan:
         """Per-head selection into the workspace's choice slot (auto mode)."""
         v = self.views(ws)
         if self.cal <= SELECTOR_CAL_MAX:
-            fam = (_ct_i32 * 3)()
-            p1 = (_ct_i32 * 3)()
-            p2 = (_ct_i32 * 3)()
+            fam = (_ct_i32 * _lib.MAX_CAND)()
+            p1 = (_ct_i32 * _lib.MAX_CAND)()
+            p2 = (_ct_i32 * _lib.MAX_CAND)()
             for c, rc in enumerate(self.refined):
                 fam[c], p1[c], p2[c] = pattern_params(rc.pattern)
             _lib.call("sa_select_windowed", self.batch, self.heads, self.kv_heads, self.length, self.cal,
                       self.scale, q.data_ptr(), k.data_ptr(), len(self.refined), fam, p1, p2, v.choice,
                       None, v.errors, D.stream())
             return
-        # wide calibration windows: composed device selection per head
+        # wide calibration windows: composed device selection per head, the
+        # weights in fp32 like the reference's (search.py:242-250); every
+        # candidate's error lands in the error rows like the selector kernel's
         from .core import AttnMatrices, dense_attention, frob_norm_diff
         from .patterns import build_index, sparse_attention
 
         g = self.heads // self.kv_heads
         choices = []
+        errs = torch.full((self.hh, _lib.MAX_CAND), math.inf, dtype=torch.float64)
         for hh in range(self.hh):
             b, h = divmod(hh, self.heads)
             kvh = b * self.kv_heads + h // g
-            sub = AttnMatrices(q[hh, -self.cal:, : self.d_head], k[kvh, -self.cal:, : self.d_head],
-                               k[kvh, -self.cal:, : self.d_head])
+            qs = q[hh, -self.cal:, : self.d_head].float()
+            ks = k[kvh, -self.cal:, : self.d_head].float()
+            sub = AttnMatrices(qs, ks, ks)  # weights only: v is not read
             dw, _ = dense_attention(sub)
             best, best_err = 0, math.inf
             for c, rc in enumerate(self.refined):
                 w, _ = sparse_attention(sub, build_index(sub, rc.pattern, mode="exact"))
                 e = frob_norm_diff(w, dw)
+                errs[hh, c] = e
                 if e < best_err:  # strict <: the earlier candidate wins ties (search.py:249)
                     best, best_err = c, e
             choices.append(best)
         _copy_into(v.choice, torch.tensor(choices, dtype=torch.int32, device=q.device))
+        _copy_into(v.errors, errs.to(q.device).reshape(-1))
 
     def run(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor, ws: torch.Tensor) -> None:
         _lib.call("sa_prefill", self.desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
@@ -295,7 +310,7 @@ class PrefillPlan:
         if self.mode != "auto":
             return self.plans_from(None, None, self.batch, self.heads, with_search)
         choice = _read_i32(v.choice, hh)
-        errs = _read_f64(v.errors, hh * 3).reshape(hh, 3)
+        errs = _read_f64(v.errors, hh * _lib.MAX_CAND).reshape(hh, _lib.MAX_CAND)
         return self.plans_from(choice, errs, self.batch, self.heads, with_search)
 
     def plans_from(self, choice, errs, batch: int, heads: int, with_search: bool = True):
@@ -368,6 +383,28 @@ def _flat(x, g, L, d):
     return np.ascontiguousarray(x).reshape(g, L, d)
 
 
+def _check_plan_args(mode, fixed_pattern, search, cal_window, q_est, length, d_head):
+    """The reference's argument errors that surface inside its per-head loop,
+    raised up front: select_pattern_windowed's window check (search.py:290-291)
+    and build_index's q_est check for a vertical-slash head (runtime.py:187,
+    patterns.py:182-189)."""
+    cal = min(cal_window, length)
+    if mode == "auto" and cal < 1:
+        raise SearchError(f"cal_window must be in [1, {length}], got {cal}")
+    qe = min(q_est, length)
+    if qe >= 1:
+        return
+    if mode == "fixed":
+        vs = isinstance(fixed_pattern, VerticalSlash)
+    elif mode == "auto":
+        space = search if search is not None else default_search_space(cal, d_head)
+        vs = any(isinstance(c, VerticalSlash) for c in space.candidates)
+    else:
+        vs = False
+    if vs:
+        raise PatternParamError(f"q_est must be in [1, {length}], got {qe}")
+
+
 def prefill(q, k, v, cfg: ModelConfig, search: SearchSpace | None = None, mode: str = "dense", *,
             fixed_pattern=None, cal_window: int = 64, q_est: int = 64, dense_cap: int = DENSE_EVAL_CAP) -> PrefillResult:
     """Process all prompt tokens at once; the TTFT analog is elapsed_s (runtime.py:134-206)."""
@@ -379,9 +416,8 @@ def prefill(q, k, v, cfg: ModelConfig, search: SearchSpace | None = None, mode: 
     if mode == "fixed" and fixed_pattern is None:
         raise SparseAttnError("mode 'fixed' requires fixed_pattern")
     if mode == "auto" and min(cal_window, length) > dense_cap:
-        from .errors import SearchError
-
         raise SearchError(f"cal_window {cal_window} exceeds the dense evaluation cap {dense_cap}")
+    _check_plan_args(mode, fixed_pattern, search, cal_window, q_est, length, cfg.d_head)
     dev = D.require_cuda()
     if (D.is_torch(q) and D.is_torch(k) and D.is_torch(v) and not q.is_cuda and not k.is_cuda
             and not v.is_cuda and cfg.d_head == D.HEAD_DIM):
@@ -472,7 +508,7 @@ def _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window
     view = plan.views(ws)
     auto = mode == "auto"
     choice_all = torch.zeros(batch * H, dtype=torch.int32, device=dev)
-    err_all = torch.zeros((batch * H, 3), dtype=torch.float64, device=dev)
+    err_all = torch.zeros((batch * H, _lib.MAX_CAND), dtype=torch.float64, device=dev)
     cache = KvCache(batch, H, d, cfg.max_context, dtype=k.dtype, kv_heads=HK)
     comp = torch.cuda.current_stream()
     h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
@@ -507,7 +543,7 @@ def _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window
         plan.run(qg, kg, vg, og, ws)
         if auto:
             choice_all[h0:h0 + g].copy_(_wrap(view.choice, g, torch.int32))
-            err_all[h0:h0 + g].copy_(_wrap(view.errors, g * 3, torch.float64).view(g, 3))
+            err_all[h0:h0 + g].copy_(_wrap(view.errors, g * _lib.MAX_CAND, torch.float64).view(g, _lib.MAX_CAND))
         cache._k[b, kh, :n].copy_(kd[grp])
         cache._v[b, kh, :n].copy_(vd[grp])
         done = torch.cuda.Event(enable_timing=tl is not None)
@@ -536,7 +572,7 @@ def _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window
         cache._v[:, :, :n].copy_(v)
     if auto:
         nh = batch * H
-        plans = plan.plans_from(small[1:1 + nh].astype(np.int64), small[1 + nh:].reshape(nh, 3), batch, H)
+        plans = plan.plans_from(small[1:1 + nh].astype(np.int64), small[1 + nh:].reshape(nh, _lib.MAX_CAND), batch, H)
     else:
         plans = plan.plans_from(None, None, batch, H)
     select_s = sum(a.elapsed_time(z) for a, z in sel) / 1e3

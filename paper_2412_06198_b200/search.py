@@ -232,15 +232,15 @@ def refined_candidates(s: SearchSpace, n: int, d_h: int, cost_q_est: int):
 
 def _device_select(q, k, heads, kv_heads, n, scale, refined, batch=1):
     """Selector kernel on staged (B*H, n, 128) bf16 q / (B*HK, n, 128) k with
-    cal = n: returns (choice[HH] int32 cuda, errors[HH, 3] float64 cuda)."""
+    cal = n: returns (choice[HH] int32 cuda, errors[HH, MAX_CAND] float64 cuda)."""
     hh = batch * heads
-    fam = (ctypes_int * 3)()
-    p1 = (ctypes_int * 3)()
-    p2 = (ctypes_int * 3)()
+    fam = (ctypes_int * _lib.MAX_CAND)()
+    p1 = (ctypes_int * _lib.MAX_CAND)()
+    p2 = (ctypes_int * _lib.MAX_CAND)()
     for c, rc in enumerate(refined):
         fam[c], p1[c], p2[c] = pattern_params(rc.pattern)
     choice = torch.empty(hh, dtype=torch.int32, device=q.device)
-    errs = torch.empty((hh, 3), dtype=torch.float64, device=q.device)
+    errs = torch.empty((hh, _lib.MAX_CAND), dtype=torch.float64, device=q.device)
     _lib.call("sa_select_windowed", batch, heads, kv_heads, n, n, scale, q.data_ptr(), k.data_ptr(),
               len(refined), fam, p1, p2, choice.data_ptr(), None, errs.data_ptr(), D.stream())
     return choice, errs
@@ -271,7 +271,7 @@ def select_pattern(m: AttnMatrices, s: SearchSpace, *, metric: str = "weights", 
 
         _check_scoring_args(m, scoring, min(q_est, m.n))
     fast = (metric == "weights" and scoring == "exact" and m.n <= SELECTOR_CAL_MAX
-            and len(refined) <= 3 and counter is None)
+            and len(refined) <= _lib.MAX_CAND and counter is None)
     if fast:
         q, k, _ = m.staged()
         choice, errs = _device_select(q, k, 1, 1, m.n, m.scale, refined)

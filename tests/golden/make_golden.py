@@ -170,6 +170,48 @@ def main():
                    "errors": [p.search.error if p.search else None for p in res.plans[0]]})
     meta["cases"]["prefill"] = pf
 
+    # 7) BASELINE C1 exactly: synth_qkv(seed=0, 4096, 8 heads, d=128), auto.
+    #    bf16-rounded (the GPU-side inputs) -> full plans + sampled outputs; the
+    #    unrounded fp32 plans are kept for the record.
+    q, k, v = synth_qkv(0, 4096, 8, 128)
+    cfg = ref.ModelConfig(n_heads=8, d_model=8 * 128, d_head=128, max_context=4096)
+    raw = ref.prefill(q, k, v, cfg, mode="auto")
+    qb, kb, vb = (bf16_round(x) for x in (q, k, v))
+    res = ref.prefill(qb, kb, vb, cfg, mode="auto")
+    arrays["c1_rows"] = res.outputs[0, ::64]
+    arrays["c1_rowsum"] = res.outputs[0].astype(np.float64).sum(axis=1)
+    meta["cases"]["c1"] = {
+        "seed": 0, "ctx": 4096, "H": 8, "mode": "auto",
+        "plans": [pat_json(p.pattern) for p in res.plans[0]],
+        "errors": [p.search.error for p in res.plans[0]],
+        "plans_fp32": [pat_json(p.pattern) for p in raw.plans[0]],
+    }
+
+    # 8) Full-size per-head selection (BASELINE C2 32K seeds 0/1, C3 128K seed
+    #    0; GQA 32 q / 8 kv, bf16-rounded).  The windowed search reads only the
+    #    trailing 64 rows (search.py:276-319), so the reference runs it on the
+    #    full-size matrices directly.  For every VS head the reference's own
+    #    estimated index (runtime.py:187, patterns.py:237-259) is stored too.
+    fw = []
+    for seed, ctx in [(0, 32768), (1, 32768), (0, 131072)]:
+        q, k, v = synth_qkv_gqa(seed, ctx, 32, 8, 128)
+        q, k, v = (bf16_round(x)[0] for x in (q, k, v))
+        space = ref.default_search_space(64, 128)
+        heads = []
+        for h in range(32):
+            m = ref.AttnMatrices(q[h], k[h // 4], v[h // 4], causal=True)
+            r = ref.select_pattern_windowed(m, space, 64)
+            e = {"chosen": pat_json(r.chosen), "error": r.error, "flops": r.realized_flops}
+            if isinstance(r.chosen, ref.VerticalSlash) and ctx <= 32768:
+                idx = ref.build_index(m, r.chosen, mode="estimated", q_est=64)
+                arrays[f"full_{seed}_{ctx}_{h}_cols"] = np.array(idx.columns, np.int32)
+                arrays[f"full_{seed}_{ctx}_{h}_diags"] = np.array(idx.diagonals, np.int32)
+                e["vs_index"] = True
+            heads.append(e)
+        fw.append({"seed": seed, "ctx": ctx, "H": 32, "HK": 8, "heads": heads})
+        del q, k, v
+    meta["cases"]["fullsize_select"] = fw
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1)

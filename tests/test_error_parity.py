@@ -96,6 +96,12 @@ CASES = {
     "index_col_range": lambda m: m.SparseIndex(n=16, columns=(16,)),
     "index_causal": lambda m: m.SparseIndex(n=16, blocks=((0, 1),), block_size=8),
     "realized_n": lambda m: m.realized_size(m.SparseIndex(n=16, columns=(1,)), 15),
+    # argument errors the reference meets inside its per-head loop
+    "prefill_cal0": lambda m: m.prefill(*_qkv((1, 2, 16, 8)), _cfg(m), mode="auto", cal_window=0),
+    "prefill_cal_neg": lambda m: m.prefill(*_qkv((1, 2, 16, 8)), _cfg(m), mode="auto", cal_window=-3),
+    "prefill_qest0_fixed_vs": lambda m: m.prefill(*_qkv((1, 2, 16, 8)), _cfg(m), mode="fixed",
+                                                  fixed_pattern=m.VerticalSlash(2, 2), q_est=0),
+    "prefill_qest_neg_auto": lambda m: m.prefill(*_qkv((1, 2, 16, 8)), _cfg(m), mode="auto", q_est=-1),
 }
 
 

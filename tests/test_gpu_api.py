@@ -184,11 +184,30 @@ def test_select_pattern_matches_oracle(sa):
 
 
 def test_windowed_rescale(sa):
-    m, _ = mats(sa, 77, 256, 8)
+    """search.py:261-319: the window choice, its parameters rescaled by n/cal
+    and its error equal the oracle's (reference test_search.py:255-273)."""
+    m, (q, k, v) = mats(sa, 77, 256, 8)
     res = sa.select_pattern_windowed(m, sa.default_search_space(64, 8), 64)
-    assert res.chosen.__class__ in (sa.Triangular, sa.VerticalSlash, sa.BlockSparse)
-    if isinstance(res.chosen, sa.BlockSparse):
-        assert res.chosen.b == 8
+    want, err, _ = O.select_windowed(q, k, v, O.default_space(64, 8), 64)
+    assert (type(res.chosen).__name__[0], *res.chosen.__dict__.values()) == \
+        (type(want).__name__[0], *want.__dict__.values())
+    assert abs(res.error - err) <= 1e-4 * max(1.0, err)
+
+
+def test_windowed_proportional_rescale(sa):
+    """test_search.py:261-266: VS(4,4) chosen on a 64-row window of 256 -> VS(16,16)."""
+    m, _ = mats(sa, 51, 256, 4)
+    p = sa.VerticalSlash(4, 4)
+    s = sa.SearchSpace([p], target_flops=sa.estimate_flops(p, 64, 4).total)
+    assert sa.select_pattern_windowed(m, s, 64).chosen == sa.VerticalSlash(16, 16)
+
+
+def test_windowed_block_geometry_kept(sa):
+    """test_search.py:268-273: a block candidate keeps its geometry."""
+    m, _ = mats(sa, 52, 128, 4)
+    p = sa.BlockSparse(b=8, k_b=2)
+    s = sa.SearchSpace([p], target_flops=sa.estimate_flops(p, 64, 4).total)
+    assert sa.select_pattern_windowed(m, s, 64).chosen == p
 
 
 # ---- runtime (test_runtime.py, golden prefill) -----------------------------------
@@ -525,3 +544,44 @@ def test_decode_past_prefill_limit(sa):
     err = (dec.output.float() - want).abs()
     assert dec.cache.length == n + 1
     assert err.max().item() <= MAX_ABS and err.mean().item() <= MEAN_ABS
+
+
+# ---- wide calibration windows and long candidate lists ---------------
+
+@pytest.mark.parametrize("cal", [128, 200])
+def test_prefill_wide_calibration_window(sa, cal):
+    """cal_window > 64 takes the composed selection (fp32 weights): the per-head
+    choice AND its window error equal the oracle's (search.py:276-319)."""
+    q, k, v = O.synth_qkv_gqa(21, 600, 4, 2, 128)
+    q, k, v = (O.bf16_round(x) for x in (q, k, v))
+    cfg = sa.ModelConfig(n_heads=4, d_model=4 * 128, d_head=128, max_context=600)
+    res = sa.prefill(q, k, v, cfg, mode="auto", cal_window=cal)
+    kx, vx = O.expand_kv(k, 4), O.expand_kv(v, 4)
+    space = O.default_space(cal, 128)
+    for h, hp in enumerate(res.plans[0]):
+        want, err, _ = O.select_windowed(q[0, h], kx[0, h], vx[0, h], space, cal)
+        assert (type(hp.pattern).__name__[0], *hp.pattern.__dict__.values()) == \
+            (type(want).__name__[0], *want.__dict__.values())
+        assert abs(hp.search.error - err) <= 1e-4 * max(1.0, err), (h, hp.search.error, err)
+    want_out, _ = O.prefill(q, k, v, "auto", cal_window=cal)
+    close(res.outputs, want_out)
+
+
+def test_prefill_many_candidates(sa):
+    """A search space with more than 3 candidates (repeated families, as the
+    reference accepts): the device selects among all of them with the
+    reference's refinement and strict-< argmin (earlier wins ties)."""
+    q, k, v = O.synth_qkv_gqa(22, 512, 4, 2, 128)
+    q, k, v = (O.bf16_round(x) for x in (q, k, v))
+    cfg = sa.ModelConfig(n_heads=4, d_model=4 * 128, d_head=128, max_context=512)
+    target = O.default_space(64, 128)[1]
+    cands = [sa.Triangular(16), sa.VerticalSlash(2, 2), sa.BlockSparse(8, 1), sa.Triangular(8),
+             sa.VerticalSlash(4, 1), sa.BlockSparse(8, 2), sa.Triangular(16)]
+    ocands = [O.Tri(16, 0), O.VS(2, 2), O.Blk(8, 1), O.Tri(8, 0), O.VS(4, 1), O.Blk(8, 2), O.Tri(16, 0)]
+    res = sa.prefill(q, k, v, cfg, sa.SearchSpace(cands, target_flops=target), mode="auto")
+    kx, vx = O.expand_kv(k, 4), O.expand_kv(v, 4)
+    for h, hp in enumerate(res.plans[0]):
+        want, err, _ = O.select_windowed(q[0, h], kx[0, h], vx[0, h], (ocands, target, 0.05, 8), 64)
+        assert (type(hp.pattern).__name__[0], *hp.pattern.__dict__.values()) == \
+            (type(want).__name__[0], *want.__dict__.values()), h
+        assert abs(hp.search.error - err) <= 1e-4 * max(1.0, err)

@@ -275,8 +275,9 @@ def test_block_estimator(sa, n, b, k_b):
     q, k = rand_heads(11, 1, n)[0], rand_heads(12, 1, n)[0]
     got = device_block_rows(q, k, b, k_b)
     want = O.block_index(q.astype(np.float64), k.astype(np.float64), b, k_b).block_rows
-    # pooled logits in split-bf16 precision: rows whose top-k margin is below the
-    # split error may legitimately differ; everything else must match exactly
+    # pooled logits in split-bf16 precision (~16 mantissa bits of each pooled
+    # mean: |logit error| <= ~2^-16 * sum|q||k| * scale ~ 1e-6 here): rows whose
+    # top-k margin is below that bound may differ; everything else is exact
     qb, kb = O.block_mean(q.astype(np.float64), b), O.block_mean(k.astype(np.float64), b)
     logit = qb @ kb.T / np.sqrt(128)
     mism = 0
@@ -286,7 +287,7 @@ def test_block_estimator(sa, n, b, k_b):
         row = np.sort(logit[g, : g + 1])[::-1]
         keff = min(k_b, g + 1)
         margin = row[keff - 1] - row[keff] if keff < g + 1 else np.inf
-        assert margin < 1e-4, (g, r_got, r_want.tolist(), margin)
+        assert margin < 1e-5, (g, r_got, r_want.tolist(), margin)
         mism += 1
     assert mism <= max(1, len(got) // 200)
 
