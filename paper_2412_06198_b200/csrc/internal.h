@@ -74,8 +74,7 @@ int launch_score_tail(int batch, int heads, int kv_heads, int n, float scale, co
                       const void* k, int r_lo, int r_hi, float* col_out, float* diag_out,
                       int accumulate, const int32_t* gate, int gate_val, void* ws, size_t ws_bytes,
                       cudaStream_t st);
-size_t tail_workspace_bytes(int hh_total, int n, int r_hi, int nchunks);
-int tail_pick_chunks(int r_hi);
+size_t tail_workspace_bytes(int hh_total, int n, int r_hi);
 
 int launch_block_pool(int groups, int n, int b, int side, const void* x, void* split_out,
                       float* mean_out, const int32_t* gate, int gate_val, cudaStream_t st);

@@ -167,7 +167,7 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
   p->blk_ws = blk_ws;
   p->tail_groups = (p->q_est + 127) / 128;
   const int r_hi_max = n;
-  p->tail_ws = p->any_vs ? tail_workspace_bytes(p->hh, n, r_hi_max, tail_pick_chunks(r_hi_max)) : 256;
+  p->tail_ws = p->any_vs ? tail_workspace_bytes(p->hh, n, r_hi_max) : 256;
   p->qp_elems = p->any_block ? (size_t)p->hh * p->max_nb * 384 : 128;
   p->kp_elems = p->any_block ? (size_t)p->hk * p->max_nb * 256 : 128;
 
