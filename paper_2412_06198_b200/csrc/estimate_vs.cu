@@ -25,11 +25,12 @@
 //     free), and each (tile, head, diagonal) partial is added to the zeroed
 //     output with one red.add — a diagonal touches at most two key tiles and
 //     0 + a + b == 0 + b + a, so the result is deterministic.
-// Work items (unit, pass, key chunk) come from one atomic queue ordered
-//   P1(0) | P1(1) P2(0) | P1(2) P2(1) | ... | P2(U-1)
-// so a unit's pass 2 re-reads K that its pass 1 brought into L2 one unit ago
-// (K is read from HBM about once), and CTAs that finish pass 1 early have the
-// next unit's pass 1 to work on while the statistics are merged.
+// Schedule: units run in waves of W (W units' K fit in L2 together: 64 MB);
+// within a wave each unit owns grid / W CTAs and each CTA one contiguous range
+// of key tiles, which it streams for pass 1 and again (from L2) for pass 2, so
+// K is read from HBM about once.  A CTA keeps its unit's Q in shared memory for
+// both passes; 16 softmax warps (four groups of four, two per 128-row slot)
+// hide the TMEM / shared-memory / MUFU latencies.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -47,31 +48,31 @@
 
 namespace sa {
 
-constexpr int kVsThreads = 320;  // warps 0-3: slot A, 4-7: slot B, 8: TMA producer, 9: MMA issuer
-constexpr int kVsSoft = 256;
-constexpr int kVsRing = 2;       // work-item ring: the producer claims one item ahead
-constexpr int kVsKSlots = 2;
-constexpr int kVsGroup = 16;     // pass-1 chunks merged per first-level group
-constexpr int kVsMaxChunks = kVsGroup * kVsGroup;  // chunks per unit (two-level merge)
-// shared memory: Q [2 buffers][64 KB] | K [2 slots][32 KB] | D [8 warps][16 x 32] f32 |
-// C [2 groups][2 buffers][4 warps][6][32] f32 | misc
-constexpr int kVsOffK = 2 * 65536;
+constexpr int kVsSoftWarps = 16;
+constexpr int kVsSoft = kVsSoftWarps * 32;       // 512 softmax threads
+constexpr int kVsThreads = kVsSoft + 64;         // + warp 16 TMA producer, warp 17 MMA issuer
+constexpr int kVsKSlots = 3;
+constexpr int kVsGroup = 16;                     // pass-1 chunks merged per first-level group
+constexpr int kVsMaxCta = 16 * kVsGroup;         // CTAs per unit (two-level merge)
+constexpr size_t kVsWaveBytes = 64ull << 20;     // K bytes of one wave (L2-resident between passes)
+// shared memory: Q [64 KB] | K [3 slots][32 KB] | D [16 warps][16 x 32] f32 |
+// C [4 groups][2 buffers][4 warps][6][32] f32 | misc (barriers, flags, -lse2, merge exchange)
+constexpr int kVsOffK = 65536;
 constexpr int kVsOffD = kVsOffK + kVsKSlots * 32768;
-constexpr int kVsOffC = kVsOffD + 8 * 2048;
-constexpr int kVsOffMisc = kVsOffC + 2 * 2 * 768 * 4;
-constexpr int kVsOffNl = kVsOffMisc + 256;  // [2 groups][128] -lse2 of the slot's rows
-constexpr int kVsSmemBytes = kVsOffMisc + 1536 + 1024;
+constexpr int kVsOffC = kVsOffD + kVsSoftWarps * 2048;
+constexpr int kVsOffMisc = kVsOffC + 4 * 2 * 768 * 4;
+constexpr int kVsOffNl = kVsOffMisc + 256;       // [4 groups][64] -lse2 of the group's rows
+constexpr int kVsOffX = kVsOffNl + 1024;         // [256] float2 merge exchange
+constexpr int kVsSmemBytes = kVsOffX + 2048 + 1024;
 
 enum VBar {
-  V_QF = 0,              // [2] Q buffer loaded
-  V_QE = 2,              // [2] MMAs done with a Q buffer
-  V_KF = 4,              // [2] K slot loaded
-  V_KE = 6,              // [2] MMAs done with a K slot
-  V_SF = 8,              // [slot * 2 + buf] S ready
-  V_SE = 12,             // [slot * 2 + buf] S consumed (128 arrivals)
-  V_IF = 16,             // [4] ring entry written
-  V_IE = 20,             // [4] ring entry read (MMA + 8 softmax warps)
-  V_NUM = 24
+  V_QF = 0,    // Q loaded
+  V_QE = 1,    // MMAs of a wave done with Q
+  V_KF = 2,    // [3] K slot loaded
+  V_KE = 5,    // [3] MMAs done with a K slot
+  V_SF = 8,    // [slot * 2 + buf] S ready
+  V_SE = 12,   // [slot * 2 + buf] S consumed (256 arrivals: two groups)
+  V_NUM = 16
 };
 
 struct TailArgs {
@@ -81,14 +82,11 @@ struct TailArgs {
   int r_lo, r_hi;      // scored rows, r_hi - r_lo <= 64
   int qrow0;           // global row of Q box row 0 (r_hi - 64, may be negative)
   int nkt;             // key tiles with a causal key: ceil(r_hi / 128)
-  int t1, c1;          // pass-1 tiles per item, items per unit
-  int t2, c2;          // pass-2 tiles per item, items per unit
-  int look;            // units between a unit's pass 1 and its pass 2 in the queue
+  int wave_units;      // most units per wave
   float scale_log2;
-  float2* stats;       // [U, c1, 256] per-(chunk, row) (max2, sum)
+  float2* stats;       // [U, kVsMaxCta, 2 key halves, 256] per-(chunk, row) (max2, sum)
   float2* stats2;      // [U, 16, 256] per-(group, row)
   float* lse2;         // [U, 256] log2-sum-exp per row (+inf: no weight)
-  int* next;           // work-queue head
   int* grp_done;       // [U, 16]
   int* unit_done;      // [U]
   int* ready;          // [U] pass 2 may start
@@ -98,36 +96,6 @@ struct TailArgs {
   const int4* units;
   const int32_t* unit_count;
 };
-
-struct VsItem {
-  int pass, unit, chunk, t_lo, t_hi;
-};
-
-// queue position -> (pass, unit, chunk): block b holds P1(b) (b < U) then
-// P2(b - L) (L <= b < U + L); the look-ahead L keeps the claimed-but-unfinished
-// window of the grid inside the pass-1 items of later units
-__device__ __forceinline__ int vs_block_start(int b, int U, const TailArgs& a) {
-  return min(b, U) * a.c1 + max(0, min(b, U + a.look) - a.look) * a.c2;
-}
-__device__ __forceinline__ VsItem vs_item(int i, int U, const TailArgs& a) {
-  VsItem w;
-  int blk = 0;
-  while (vs_block_start(blk + 1, U, a) <= i) ++blk;
-  const int r = i - vs_block_start(blk, U, a);
-  if (blk < U && r < a.c1) {
-    w.pass = 1;
-    w.unit = blk;
-    w.chunk = r;
-  } else {
-    w.pass = 2;
-    w.unit = blk - a.look;
-    w.chunk = blk < U ? r - a.c1 : r;
-  }
-  const int T = w.pass == 1 ? a.t1 : a.t2;
-  w.t_lo = w.chunk * T;
-  w.t_hi = min(a.nkt, w.t_lo + T);
-  return w;
-}
 
 // 2^x for a pair on the FMA pipe: x = j + f (j = rint x by the 1.5*2^23 magic
 // add), 2^f by a degree-5 fit on [-0.5, 0.5] (max relative error 2.4e-7 in
@@ -175,419 +143,398 @@ __device__ __forceinline__ void red_add(float* p, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// this CTA's place in the wave schedule (identical in every role)
+struct VsPlace {
+  int U, W, cpu, ws, rank, t_lo, t_hi, nwaves;
+};
+__device__ __forceinline__ VsPlace vs_place(const TailArgs& a) {
+  VsPlace p;
+  p.U = *a.unit_count;
+  p.W = min(p.U, a.wave_units);
+  p.cpu = p.W > 0 ? min((int)gridDim.x / p.W, min(a.nkt, kVsMaxCta)) : 0;
+  p.ws = p.cpu > 0 ? (int)blockIdx.x / p.cpu : 0;
+  p.rank = p.cpu > 0 ? (int)blockIdx.x % p.cpu : 0;
+  p.t_lo = p.cpu > 0 ? (int)(((long long)p.rank * a.nkt) / p.cpu) : 0;
+  p.t_hi = p.cpu > 0 ? (int)(((long long)(p.rank + 1) * a.nkt) / p.cpu) : 0;
+  p.nwaves = p.W > 0 ? (p.U + p.W - 1) / p.W : 0;
+  return p;
+}
+
 __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __grid_constant__ TailArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;
   uint8_t* sK = smem + kVsOffK;
-  float* sD = reinterpret_cast<float*>(smem + kVsOffD);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kVsOffMisc);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + V_NUM);
-  volatile int* ring = reinterpret_cast<volatile int*>(tmem_holder + 4);
-  volatile int* flag = ring + kVsRing;
+  volatile int* flag = reinterpret_cast<volatile int*>(tmem_holder + 4);
   const int warp = warp_id();
-  const int U = *a.unit_count;
-  const int total = U * (a.c1 + a.c2);
-  if ((int)blockIdx.x >= total) return;
+  const VsPlace pl = vs_place(a);
+  if (pl.W == 0 || pl.ws >= pl.W) return;  // idle CTA (uniform exit)
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&bars[V_QF + s], 1);
-      mbar_init(&bars[V_QE + s], 1);
+    mbar_init(&bars[V_QF], 1);
+    mbar_init(&bars[V_QE], 1);
+    for (int s = 0; s < kVsKSlots; ++s) {
       mbar_init(&bars[V_KF + s], 1);
       mbar_init(&bars[V_KE + s], 1);
     }
     for (int s = 0; s < 4; ++s) {
       mbar_init(&bars[V_SF + s], 1);
-      mbar_init(&bars[V_SE + s], 128);
-      if (s < kVsRing) {
-        mbar_init(&bars[V_IF + s], 1);
-        mbar_init(&bars[V_IE + s], 1 + 8);
-      }
+      mbar_init(&bars[V_SE + s], 256);
     }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc(tmem_holder, 512);
+  if (warp == kVsSoftWarps + 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
-  if (warp == 8) {
+  if (warp == kVsSoftWarps) {
     // ------------------------------------------------------------ producer
     if (elect_one()) {
-      int cur_unit = -1, qb = -1, kj = 0;
-      int quse0 = 0, quse1 = 0;  // loads into each Q buffer
-      for (int it = 0;; ++it) {
-        const int rs = it & (kVsRing - 1);
-        if (it >= kVsRing) mbar_wait_backoff<32>(&bars[V_IE + rs], ((it / kVsRing) - 1) & 1);
-        int item = atomicAdd(a.next, 1);
-        if (item >= total) item = -1;
-        ring[rs] = item;
-        mbar_arrive(&bars[V_IF + rs]);
-        if (item < 0) break;
-        const VsItem w = vs_item(item, U, a);
-        const int4 un = a.units[w.unit];
-        if (w.unit != cur_unit) {
-          qb = qb < 0 ? 0 : qb ^ 1;
-          const int qu = qb ? quse1 : quse0;
-          if (qu > 0) mbar_wait_backoff<32>(&bars[V_QE + qb], (qu - 1) & 1);
-          if (qb) ++quse1;
-          else ++quse0;
-          const int nslot = un.z >= 0 ? 2 : 1;
-          uint8_t* q = sQ + qb * 65536;
-          mbar_arrive_expect_tx(&bars[V_QF + qb], 32768 * nslot);
-          for (int s = 0; s < nslot; ++s) {
-            const int h0 = s ? un.z : un.x;
-            const int h1r = s ? un.w : un.y;
-            const int h1 = h1r >= 0 ? h1r : h0;  // a lone head fills both halves (rows inactive)
+      int kj = 0;
+      for (int v = 0; v < pl.nwaves; ++v) {
+        const int u = v * pl.W + pl.ws;
+        if (u >= pl.U) break;
+        const int4 un = a.units[u];
+        if (v > 0) mbar_wait_backoff<64>(&bars[V_QE], (v - 1) & 1);  // previous wave's MMAs read Q
+        const int nslot = un.z >= 0 ? 2 : 1;
+        mbar_arrive_expect_tx(&bars[V_QF], 32768 * nslot);
+        for (int s = 0; s < nslot; ++s) {
+          const int h0 = s ? un.z : un.x;
+          const int h1r = s ? un.w : un.y;
+          const int h1 = h1r >= 0 ? h1r : h0;  // a lone head fills both halves (rows inactive)
 #pragma unroll
-            for (int dh = 0; dh < 2; ++dh) {
-              tma_load_3d(q + dh * 32768 + s * 16384, &a.tmap_q, &bars[V_QF + qb], 64 * dh, a.qrow0, h0);
-              tma_load_3d(q + dh * 32768 + s * 16384 + 8192, &a.tmap_q, &bars[V_QF + qb], 64 * dh, a.qrow0, h1);
-            }
+          for (int dh = 0; dh < 2; ++dh) {
+            tma_load_3d(sQ + dh * 32768 + s * 16384, &a.tmap_q, &bars[V_QF], 64 * dh, a.qrow0, h0);
+            tma_load_3d(sQ + dh * 32768 + s * 16384 + 8192, &a.tmap_q, &bars[V_QF], 64 * dh, a.qrow0, h1);
           }
-          cur_unit = w.unit;
         }
         const int hkv = (un.x / a.heads) * a.kv_heads + (un.x % a.heads) / (a.heads / a.kv_heads);
-        for (int kt = w.t_lo; kt < w.t_hi; ++kt, ++kj) {
-          const int ks = kj & 1;
-          if (kj >= kVsKSlots) mbar_wait_backoff<32>(&bars[V_KE + ks], ((kj >> 1) - 1) & 1);
-          uint8_t* dst = sK + ks * 32768;
-          mbar_arrive_expect_tx(&bars[V_KF + ks], 32768);
-          tma_load_3d(dst, &a.tmap_k, &bars[V_KF + ks], 0, kt * kTile, hkv);
-          tma_load_3d(dst + 16384, &a.tmap_k, &bars[V_KF + ks], 64, kt * kTile, hkv);
-        }
+        for (int pass = 0; pass < 2; ++pass)
+          for (int kt = pl.t_lo; kt < pl.t_hi; ++kt, ++kj) {
+            const int ks = kj % kVsKSlots;
+            if (kj >= kVsKSlots) mbar_wait_backoff<32>(&bars[V_KE + ks], ((kj / kVsKSlots) - 1) & 1);
+            uint8_t* dst = sK + ks * 32768;
+            mbar_arrive_expect_tx(&bars[V_KF + ks], 32768);
+            tma_load_3d(dst, &a.tmap_k, &bars[V_KF + ks], 0, kt * kTile, hkv);
+            tma_load_3d(dst + 16384, &a.tmap_k, &bars[V_KF + ks], 64, kt * kTile, hkv);
+          }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kVsSoftWarps + 1) {
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
       constexpr uint32_t idesc1 = idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t idesc2a = idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t idesc2b = idesc_bf16_f32(128, 256, 0, 0);
-      int cur_unit = -1, qb = -1, kj = 0, jt = 0;
-      int qfn0 = 0, qfn1 = 0;  // uses of each Q buffer
-      for (int it = 0;; ++it) {
-        const int rs = it & (kVsRing - 1);
-        mbar_wait(&bars[V_IF + rs], (it / kVsRing) & 1);
-        const int item = ring[rs];
-        if (item < 0) break;
-        const VsItem w = vs_item(item, U, a);
-        const bool sb = a.units[w.unit].z >= 0;
-        if (w.unit != cur_unit) {
-          qb = qb < 0 ? 0 : qb ^ 1;
-          mbar_wait(&bars[V_QF + qb], (qb ? qfn1 : qfn0) & 1);
-          if (qb) ++qfn1;
-          else ++qfn0;
-          cur_unit = w.unit;
-        }
-        const uint32_t q_addr = smem_u32(sQ + qb * 65536);
+      const uint32_t q_addr = smem_u32(sQ);
+      int kj = 0, jt = 0;
+      for (int v = 0; v < pl.nwaves; ++v) {
+        const int u = v * pl.W + pl.ws;
+        if (u >= pl.U) break;
+        const bool sb = a.units[u].z >= 0;
+        mbar_wait(&bars[V_QF], v & 1);
         tc_fence_after();
-        for (int kt = w.t_lo; kt < w.t_hi; ++kt, ++kj, ++jt) {
-          const int ks = kj & 1, b = jt & 1;
-          mbar_wait(&bars[V_KF + ks], (kj >> 1) & 1);
-          if (jt >= 2) {
-            mbar_wait(&bars[V_SE + b], ((jt >> 1) - 1) & 1);
-            mbar_wait(&bars[V_SE + 2 + b], ((jt >> 1) - 1) & 1);
-          }
-          tc_fence_after();
-          const uint32_t k_addr = smem_u32(sK + ks * 32768);
-          const uint32_t d0 = tbase + b * 256;
-          if (w.pass == 1) {
-            // S[slot] = Q_slot K^T: rows on lanes, keys on columns
+        for (int pass = 1; pass <= 2; ++pass)
+          for (int kt = pl.t_lo; kt < pl.t_hi; ++kt, ++kj, ++jt) {
+            const int ks = kj % kVsKSlots, b = jt & 1;
+            mbar_wait(&bars[V_KF + ks], (kj / kVsKSlots) & 1);
+            if (jt >= 2) {
+              mbar_wait(&bars[V_SE + b], ((jt >> 1) - 1) & 1);
+              mbar_wait(&bars[V_SE + 2 + b], ((jt >> 1) - 1) & 1);
+            }
+            tc_fence_after();
+            const uint32_t k_addr = smem_u32(sK + ks * 32768);
+            const uint32_t d0 = tbase + b * 256;
+            if (pass == 1) {
+              // S[slot] = Q_slot K^T: rows on lanes, keys on columns
 #pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              if (s == 1 && !sb) break;
+              for (int s = 0; s < 2; ++s) {
+                if (s == 1 && !sb) break;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                  mma_ss(d0 + s * 128,
+                         sdesc_sw128(q_addr + (kk >> 2) * 32768 + s * 16384 + (kk & 3) * 32, 16, 1024),
+                         sdesc_sw128(k_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), idesc1, kk > 0);
+              }
+            } else {
+              // S^T = K Q^T over both slots' rows (N = 256): keys on lanes
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk)
-                mma_ss(d0 + s * 128,
-                       sdesc_sw128(q_addr + (kk >> 2) * 32768 + s * 16384 + (kk & 3) * 32, 16, 1024),
-                       sdesc_sw128(k_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), idesc1, kk > 0);
+                mma_ss(d0, sdesc_sw128(k_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                       sdesc_sw128(q_addr + (kk >> 2) * 32768 + (kk & 3) * 32, 16, 1024), sb ? idesc2b : idesc2a,
+                       kk > 0);
             }
-          } else {
-            // S^T = K Q^T over both slots' rows (N = 256): keys on lanes
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              mma_ss(d0, sdesc_sw128(k_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                     sdesc_sw128(q_addr + (kk >> 2) * 32768 + (kk & 3) * 32, 16, 1024), sb ? idesc2b : idesc2a,
-                     kk > 0);
+            mma_commit(&bars[V_KE + ks]);
+            mma_commit(&bars[V_SF + b]);
+            mma_commit(&bars[V_SF + 2 + b]);
           }
-          mma_commit(&bars[V_KE + ks]);
-          mma_commit(&bars[V_SF + b]);
-          mma_commit(&bars[V_SF + 2 + b]);
-        }
-        // hand the Q buffer back when the next item belongs to another unit
-        const int rn = (it + 1) & (kVsRing - 1);
-        mbar_wait(&bars[V_IF + rn], ((it + 1) / kVsRing) & 1);
-        const int nxt = ring[rn];
-        if (nxt >= 0 && vs_item(nxt, U, a).unit != cur_unit) mma_commit(&bars[V_QE + qb]);
-        mbar_arrive(&bars[V_IE + rs]);
+        mma_commit(&bars[V_QE]);
       }
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    const int grp = warp >> 2;  // slot
+    const int grp = warp >> 2;      // 0..3
+    const int slot = grp >> 1;      // 128-row slot
+    const int sub = grp & 1;        // pass 1: key half of the tile; pass 2: head of the slot
+    const int q4 = warp & 3;        // TMEM lane quarter
     const int t = threadIdx.x & 127;
     const int lane = threadIdx.x & 31;
-    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const float sl2 = a.scale_log2;
-    const int pw = warp & 3;                                  // this warp's 32 keys of the tile
-    float* Dw = sD + warp * 512;                              // [16 rows][32 keys] per warp
-    float* sC = reinterpret_cast<float*>(smem + kVsOffC) + grp * 1536;  // [2][4 warps][6][32]
-    int cbuf = 0;
-    float* nl = reinterpret_cast<float*>(smem + kVsOffNl) + grp * 128;  // pass 2: -lse2 (-inf: no weight)
-    int jt = 0;
-    int nl_unit = -1;
-    for (int it = 0;; ++it) {
-      const int rs = it & (kVsRing - 1);
-      mbar_wait(&bars[V_IF + rs], (it / kVsRing) & 1);
-      const int item = ring[rs];
-      if (item < 0) break;
-      const VsItem w = vs_item(item, U, a);
-      const int4 un = a.units[w.unit];
-      const int ha = grp ? un.z : un.x, hb = grp ? un.w : un.y;
+    float* Dw = reinterpret_cast<float*>(smem + kVsOffD) + warp * 512;              // [16 rows][32 keys]
+    float* sC = reinterpret_cast<float*>(smem + kVsOffC) + grp * 1536;              // [2][4 warps][6][32]
+    float* nl = reinterpret_cast<float*>(smem + kVsOffNl) + grp * 64;               // -lse2 of the group's rows
+    float2* xch = reinterpret_cast<float2*>(smem + kVsOffX);
+    const int ng = (pl.cpu + kVsGroup - 1) / kVsGroup;
+    int jt = 0, cbuf = 0;
+    for (int v = 0; v < pl.nwaves; ++v) {
+      const int u = v * pl.W + pl.ws;
+      if (u >= pl.U) break;
+      const int4 un = a.units[u];
+      const int ha = slot ? un.z : un.x, hb = slot ? un.w : un.y;
       const bool on = ha >= 0;
-      if (w.pass == 1) {
-        // ---------------------------------------------------- pass 1 (thread = row)
+      // ---------------------------------------------------- pass 1 (thread = row, half the keys)
+      {
         const int hrow = (t < 64) ? ha : hb;
         const int i = a.qrow0 + (t & 63);
         const bool active = on && hrow >= 0 && i >= a.r_lo && i < a.r_hi;
         float m = -INFINITY, ssum = 0.f;
-        for (int kt = w.t_lo; kt < w.t_hi; ++kt, ++jt) {
+        for (int kt = pl.t_lo; kt < pl.t_hi; ++kt, ++jt) {
           const int b = jt & 1;
-          mbar_wait(&bars[V_SF + grp * 2 + b], (jt >> 1) & 1);
+          mbar_wait(&bars[V_SF + slot * 2 + b], (jt >> 1) & 1);
           if (on) {
             tc_fence_after();
-#pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2) {
-              uint32_t s[64];
-              tmem_ld32(tbase + lane_off + b * 256 + grp * 128 + 64 * c2, *reinterpret_cast<uint32_t(*)[32]>(s));
-              tmem_ld32(tbase + lane_off + b * 256 + grp * 128 + 64 * c2 + 32,
-                        *reinterpret_cast<uint32_t(*)[32]>(s + 32));
-              tmem_ld_wait();
-              if (!active) continue;
-              const int lim = i - (kt * kTile + 64 * c2);  // keep columns c <= lim
+            uint32_t s[64];
+            tmem_ld32(tbase + lane_off + b * 256 + slot * 128 + 64 * sub, *reinterpret_cast<uint32_t(*)[32]>(s));
+            tmem_ld32(tbase + lane_off + b * 256 + slot * 128 + 64 * sub + 32,
+                      *reinterpret_cast<uint32_t(*)[32]>(s + 32));
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&bars[V_SE + slot * 2 + b]);
+            if (active) {
+              const int lim = i - (kt * kTile + 64 * sub);  // keep columns c <= lim
               if (lim < 63) {
 #pragma unroll
-                for (int u = 0; u < 64; ++u)
-                  if (u > lim) s[u] = __float_as_uint(-INFINITY);
+                for (int c = 0; c < 64; ++c)
+                  if (c > lim) s[c] = __float_as_uint(-INFINITY);
               }
               float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-              for (int u = 0; u < 64; u += 8) {
-                m4[0] = fmax3(m4[0], __uint_as_float(s[u]), __uint_as_float(s[u + 1]));
-                m4[1] = fmax3(m4[1], __uint_as_float(s[u + 2]), __uint_as_float(s[u + 3]));
-                m4[2] = fmax3(m4[2], __uint_as_float(s[u + 4]), __uint_as_float(s[u + 5]));
-                m4[3] = fmax3(m4[3], __uint_as_float(s[u + 6]), __uint_as_float(s[u + 7]));
+              for (int c = 0; c < 64; c += 8) {
+                m4[0] = fmax3(m4[0], __uint_as_float(s[c]), __uint_as_float(s[c + 1]));
+                m4[1] = fmax3(m4[1], __uint_as_float(s[c + 2]), __uint_as_float(s[c + 3]));
+                m4[2] = fmax3(m4[2], __uint_as_float(s[c + 4]), __uint_as_float(s[c + 5]));
+                m4[3] = fmax3(m4[3], __uint_as_float(s[c + 6]), __uint_as_float(s[c + 7]));
               }
               const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-              if (mx == -INFINITY) continue;
-              const float mn = fmaxf(m, mx * sl2);
-              const float2 sc2 = make_float2(sl2, sl2), mo2 = make_float2(-mn, -mn);
-              float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                               make_float2(0.f, 0.f)};
+              if (mx != -INFINITY) {
+                const float mn = fmaxf(m, mx * sl2);
+                const float2 sc2 = make_float2(sl2, sl2), mo2 = make_float2(-mn, -mn);
+                float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                 make_float2(0.f, 0.f)};
 #pragma unroll
-              for (int u = 0; u < 64; u += 2) {
-                const float2 x = ffma2(make_float2(__uint_as_float(s[u]), __uint_as_float(s[u + 1])), sc2, mo2);
-                acc[(u >> 1) & 3] = fadd2(acc[(u >> 1) & 3], exp2_mix<3>(x, u >> 1));
+                for (int c = 0; c < 64; c += 2) {
+                  const float2 x = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2, mo2);
+                  acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], exp2_mix<3>(x, c >> 1));
+                }
+                const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+                ssum = ssum * fast_exp2(m - mn) + ((a01.x + a01.y) + (a23.x + a23.y));
+                m = mn;
               }
-              const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
-              ssum = ssum * fast_exp2(m - mn) + ((a01.x + a01.y) + (a23.x + a23.y));
-              m = mn;
             }
+          } else {
+            mbar_arrive(&bars[V_SE + slot * 2 + b]);
           }
-          tc_fence_before();
-          mbar_arrive(&bars[V_SE + grp * 2 + b]);
         }
-        // per-(chunk, row) statistics; both slots always write (unscored rows: (-inf, 0))
-        a.stats[((size_t)w.unit * a.c1 + w.chunk) * 256 + grp * 128 + t] = make_float2(m, ssum);
+        // per-(chunk, key half, row) statistics (unscored rows: (-inf, 0))
+        a.stats[(((size_t)u * kVsMaxCta + pl.rank) * 2 + sub) * 256 + slot * 128 + t] = make_float2(m, ssum);
         // zero this chunk's range of the diagonal output (and the column tail
         // beyond the scored keys) for the unit's heads: pass 2 adds into them
         {
-          const int o_lo = w.t_lo * kTile;
-          int o_hi = min(a.n, w.t_hi * kTile);
-          if (w.t_hi == a.nkt) o_hi = a.n;
+          const int o_lo = pl.t_lo * kTile;
+          const int o_hi = pl.t_hi == a.nkt ? a.n : min(a.n, pl.t_hi * kTile);
           const int tid = threadIdx.x;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int h = q == 0 ? un.x : (q == 1 ? un.y : (q == 2 ? un.z : un.w));
+          for (int qq = 0; qq < 4; ++qq) {
+            const int h = qq == 0 ? un.x : (qq == 1 ? un.y : (qq == 2 ? un.z : un.w));
             if (h < 0) continue;
             float* dd = a.diag_dst + (size_t)h * a.n;
             for (int o = o_lo + tid; o < o_hi; o += kVsSoft) dd[o] = 0.f;
-            if (!a.accumulate && w.t_hi == a.nkt) {
+            if (!a.accumulate && pl.t_hi == a.nkt) {
               float* cc = a.col_out + (size_t)h * a.n;
               for (int j = a.nkt * kTile + tid; j < a.n; j += kVsSoft) cc[j] = 0.f;
             }
           }
         }
         named_bar_sync(1, kVsSoft);
-        const int g1 = w.chunk / kVsGroup;
-        const int ngrp = (a.c1 + kVsGroup - 1) / kVsGroup;
+        const int g1 = pl.rank / kVsGroup;
         if (threadIdx.x == 0) {  // barrier, then one gpu-scope fence + atomic (release pattern)
           __threadfence();
-          const int gsz = min(kVsGroup, a.c1 - g1 * kVsGroup);
-          flag[0] = atomicAdd(&a.grp_done[w.unit * kVsGroup + g1], 1) == gsz - 1;
+          const int gsz = min(kVsGroup, pl.cpu - g1 * kVsGroup);
+          flag[0] = atomicAdd(&a.grp_done[u * kVsGroup + g1], 1) == gsz - 1;
         }
         named_bar_sync(1, kVsSoft);
         if (flag[0]) {
-          // first-level merge of the group's chunks (fixed order), thread = row
-          const int tid = threadIdx.x;
-          // (all loads in flight at once, then the fixed-order merge)
-          const int c0 = g1 * kVsGroup, cn = min(a.c1, c0 + kVsGroup) - c0;
-          float2 v[kVsGroup];
+          // first-level merge of the group's chunks (fixed order): thread = (row, key half)
+          const int row = threadIdx.x & 255, half = threadIdx.x >> 8;
+          const int c0 = g1 * kVsGroup, cn = min(pl.cpu, c0 + kVsGroup) - c0;
+          float2 vv[kVsGroup];
 #pragma unroll
           for (int c = 0; c < kVsGroup; ++c)
-            v[c] = c < cn ? __ldcg(&a.stats[((size_t)w.unit * a.c1 + c0 + c) * 256 + tid])
-                          : make_float2(-INFINITY, 0.f);
+            vv[c] = c < cn ? __ldcg(&a.stats[(((size_t)u * kVsMaxCta + c0 + c) * 2 + half) * 256 + row])
+                           : make_float2(-INFINITY, 0.f);
           float2 acc = make_float2(-INFINITY, 0.f);
 #pragma unroll
-          for (int c = 0; c < kVsGroup; ++c) acc = merge_stat(acc, v[c]);
-          a.stats2[((size_t)w.unit * kVsGroup + g1) * 256 + tid] = acc;
+          for (int c = 0; c < kVsGroup; ++c) acc = merge_stat(acc, vv[c]);
+          if (half) xch[row] = acc;
+          named_bar_sync(1, kVsSoft);
+          if (!half) a.stats2[((size_t)u * kVsGroup + g1) * 256 + row] = merge_stat(acc, xch[row]);
           named_bar_sync(1, kVsSoft);
           if (threadIdx.x == 0) {
             __threadfence();
-            flag[1] = atomicAdd(&a.unit_done[w.unit], 1) == ngrp - 1;
+            flag[1] = atomicAdd(&a.unit_done[u], 1) == ng - 1;
           }
           named_bar_sync(1, kVsSoft);
           if (flag[1]) {
-            float2 v2[kVsGroup];
+            if (!half) {
+              float2 v2[kVsGroup];
 #pragma unroll
-            for (int g = 0; g < kVsGroup; ++g)
-              v2[g] = g < ngrp ? __ldcg(&a.stats2[((size_t)w.unit * kVsGroup + g) * 256 + tid])
+              for (int g = 0; g < kVsGroup; ++g)
+                v2[g] = g < ng ? __ldcg(&a.stats2[((size_t)u * kVsGroup + g) * 256 + row])
                                : make_float2(-INFINITY, 0.f);
-            float2 r = make_float2(-INFINITY, 0.f);
+              float2 r = make_float2(-INFINITY, 0.f);
 #pragma unroll
-            for (int g = 0; g < kVsGroup; ++g) r = merge_stat(r, v2[g]);
-            a.lse2[(size_t)w.unit * 256 + tid] = r.y > 0.f ? r.x + log2f(r.y) : INFINITY;
+              for (int g = 0; g < kVsGroup; ++g) r = merge_stat(r, v2[g]);
+              a.lse2[(size_t)u * 256 + row] = r.y > 0.f ? r.x + log2f(r.y) : INFINITY;
+            }
             named_bar_sync(1, kVsSoft);
             if (threadIdx.x == 0) {
               __threadfence();
-              st_release(&a.ready[w.unit], 1);
+              st_release(&a.ready[u], 1);
             }
           }
         }
-      } else {
-        // ---------------------------------------------------- pass 2 (thread = key)
-        if (on && nl_unit != w.unit) {
+      }
+      // ---------------------------------------------------- pass 2 (thread = key, one head's rows)
+      {
+        const int h = sub ? hb : ha;
+        const bool work = on && h >= 0;
+        if (work) {
           if (t == 0) {
-            while (ld_relaxed(&a.ready[w.unit]) == 0) __nanosleep(64);
+            while (ld_relaxed(&a.ready[u]) == 0) __nanosleep(64);
             __threadfence();  // acquire: the statistics written before the release
           }
           named_bar_sync(2 + grp, 128);
-          nl[t] = -__ldcg(a.lse2 + (size_t)w.unit * 256 + grp * 128 + t);
+          if (t < 64) nl[t] = -__ldcg(a.lse2 + (size_t)u * 256 + slot * 128 + sub * 64 + t);
           named_bar_sync(2 + grp, 128);
-          nl_unit = w.unit;
         }
-        for (int kt = w.t_lo; kt < w.t_hi; ++kt, ++jt) {
+        const float2 sc2 = make_float2(sl2, sl2);
+        for (int kt = pl.t_lo; kt < pl.t_hi; ++kt, ++jt) {
           const int b = jt & 1;
-          mbar_wait(&bars[V_SF + grp * 2 + b], (jt >> 1) & 1);
-          if (on) {
-            tc_fence_after();
-            const int j = kt * kTile + t;
-            const int obase = a.qrow0 - kt * kTile - 127;
-            const float2 sc2 = make_float2(sl2, sl2);
+          mbar_wait(&bars[V_SF + slot * 2 + b], (jt >> 1) & 1);
+          if (!work) {
+            mbar_arrive(&bars[V_SE + slot * 2 + b]);
+            continue;
+          }
+          tc_fence_after();
+          const int j = kt * kTile + t;
+          const int obase = a.qrow0 - kt * kTile - 127;
+          // R[jj]: this lane's partial of diagonal op = lane + 16 jj + 96 - 32 q4
+          float R[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          float2 cs = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int hi = 0; hi < 2; ++hi) {
-              const int h = hi ? hb : ha;
-              if (h < 0) continue;
-              // R[jj]: this lane's partial of diagonal op = lane + 16 jj + 96 - 32 p
-              float R[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-              float2 cs = make_float2(0.f, 0.f);
+          for (int qh = 0; qh < 2; ++qh) {
+            uint32_t s[32];
+            tmem_ld32(tbase + lane_off + b * 256 + slot * 128 + sub * 64 + qh * 32, s);
+            tmem_ld_wait();
+            if (qh == 1) {
+              tc_fence_before();
+              mbar_arrive(&bars[V_SE + slot * 2 + b]);
+            }
+            // rows of this quarter: frame rows 32 qh + c, global qrow0 + 32 qh + c; causal j <= i
+            const int cmin = j - (a.qrow0 + 32 * qh);  // rows c >= cmin see key j
+            const bool cut = __any_sync(0xffffffffu, cmin > 0);
 #pragma unroll
-              for (int qh = 0; qh < 2; ++qh) {
-                uint32_t s[32];
-                tmem_ld32(tbase + lane_off + b * 256 + grp * 128 + hi * 64 + qh * 32, s);
-                float nlq[32];  // broadcast reads of this quarter's -lse2
-#pragma unroll
-                for (int c = 0; c < 32; c += 4) {
-                  const float4 v = *reinterpret_cast<const float4*>(nl + hi * 64 + qh * 32 + c);
-                  nlq[c] = v.x;
-                  nlq[c + 1] = v.y;
-                  nlq[c + 2] = v.z;
-                  nlq[c + 3] = v.w;
-                }
-                tmem_ld_wait();
-                // rows of this quarter: frame rows 32 qh + c, global qrow0 + 32 qh + c; causal j <= i
-                const int cmin = j - (a.qrow0 + 32 * qh);  // rows c >= cmin see key j
-                const bool cut = __any_sync(0xffffffffu, cmin > 0);
-                float wv[32];
-#pragma unroll
-                for (int c = 0; c < 32; c += 2) {
-                  const float2 x = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2,
-                                         make_float2(nlq[c], nlq[c + 1]));
-                  float2 e = make_float2(fast_exp2(x.x), fast_exp2(x.y));
-                  if (cut) {
-                    e.x = c >= cmin ? e.x : 0.f;
-                    e.y = c + 1 >= cmin ? e.y : 0.f;
-                  }
-                  cs = fadd2(cs, e);
-                  wv[c] = e.x;
-                  wv[c + 1] = e.y;
-                }
-                // two 16-row blocks through this warp's 16 x 32 buffer: lane l
-                // writes key l of each row; the rotated read (row s, key
-                // (s + 31 - lane) & 31) gives diagonal lane (s <= lane) or
-                // lane + 32 (s > lane) of the block, bank-conflict free
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  __syncwarp();
-#pragma unroll
-                  for (int c = 0; c < 16; ++c) Dw[c * 32 + lane] = wv[16 * e + c];
-                  __syncwarp();
-                  float A = 0.f, B = 0.f;
-#pragma unroll
-                  for (int sr = 0; sr < 16; ++sr) {
-                    const float v = Dw[sr * 32 + ((sr + 31 - lane) & 31)];
-                    if (sr <= lane) A += v;
-                    else B += v;
-                  }
-                  R[2 * qh + e] += A;
-                  R[2 * qh + e + 2] += B;
-                }
+            for (int c = 0; c < 32; c += 4) {
+              const float4 nv = *reinterpret_cast<const float4*>(nl + qh * 32 + c);  // broadcast
+              float2 x0 = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2,
+                                make_float2(nv.x, nv.y));
+              float2 x1 = ffma2(make_float2(__uint_as_float(s[c + 2]), __uint_as_float(s[c + 3])), sc2,
+                                make_float2(nv.z, nv.w));
+              float2 e0 = make_float2(fast_exp2(x0.x), fast_exp2(x0.y));
+              float2 e1 = make_float2(fast_exp2(x1.x), fast_exp2(x1.y));
+              if (cut) {
+                e0.x = c >= cmin ? e0.x : 0.f;
+                e0.y = c + 1 >= cmin ? e0.y : 0.f;
+                e1.x = c + 2 >= cmin ? e1.x : 0.f;
+                e1.y = c + 3 >= cmin ? e1.y : 0.f;
               }
-              if (j < a.n) {
-                float* dst = a.col_out + (size_t)h * a.n + j;
-                const float tot = cs.x + cs.y;
-                *dst = a.accumulate ? (*dst + tot) : tot;
+              cs = fadd2(cs, fadd2(e0, e1));
+              s[c] = __float_as_uint(e0.x);
+              s[c + 1] = __float_as_uint(e0.y);
+              s[c + 2] = __float_as_uint(e1.x);
+              s[c + 3] = __float_as_uint(e1.y);
+            }
+            // two 16-row blocks through this warp's 16 x 32 buffer: lane l
+            // writes key l of each row; the rotated read (row r, key
+            // (r + 31 - lane) & 31) gives diagonal lane (r <= lane) or
+            // lane + 32 (r > lane) of the block, bank-conflict free
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              __syncwarp();
+#pragma unroll
+              for (int c = 0; c < 16; ++c) Dw[c * 32 + lane] = __uint_as_float(s[16 * e + c]);
+              __syncwarp();
+              float A = 0.f, B = 0.f;
+#pragma unroll
+              for (int r = 0; r < 16; ++r) {
+                const float x = Dw[r * 32 + ((r + 31 - lane) & 31)];
+                if (r <= lane) A += x;
+                else B += x;
               }
-              // the four warps' partials meet in C (double-buffered per head)
-              float* Cb = sC + (cbuf & 1) * 768;
-              ++cbuf;
-#pragma unroll
-              for (int jj = 0; jj < 6; ++jj) Cb[(pw * 6 + jj) * 32 + lane] = R[jj];
-              named_bar_sync(2 + grp, 128);
-              float* dd = a.diag_dst + (size_t)h * a.n;
-#pragma unroll
-              for (int k2 = 0; k2 < 2; ++k2) {
-                const int op = t + 128 * k2;
-                if (op > 190) break;
-                float v = 0.f;
-#pragma unroll
-                for (int p2 = 0; p2 < 4; ++p2) {
-                  const int x = op - 96 + 32 * p2;  // = lane' + 16 jj'
-                  if (x < 0) continue;
-                  const int j1 = x >> 4;
-                  if (j1 - 1 >= 0 && j1 - 1 < 6) v += Cb[(p2 * 6 + j1 - 1) * 32 + (x - 16 * (j1 - 1))];
-                  if (j1 < 6) v += Cb[(p2 * 6 + j1) * 32 + (x - 16 * j1)];
-                }
-                const int o = obase + op;
-                if (o >= 0 && o < a.n) red_add(dd + o, v);
-              }
+              R[2 * qh + e] += A;
+              R[2 * qh + e + 2] += B;
             }
           }
-          tc_fence_before();
-          mbar_arrive(&bars[V_SE + grp * 2 + b]);
+          if (j < a.n) {
+            float* dst = a.col_out + (size_t)h * a.n + j;
+            const float tot = cs.x + cs.y;
+            *dst = a.accumulate ? (*dst + tot) : tot;
+          }
+          // the four warps' partials meet in C (double-buffered per tile)
+          float* Cb = sC + (cbuf & 1) * 768;
+          ++cbuf;
+#pragma unroll
+          for (int jj = 0; jj < 6; ++jj) Cb[(q4 * 6 + jj) * 32 + lane] = R[jj];
+          named_bar_sync(2 + grp, 128);
+          float* dd = a.diag_dst + (size_t)h * a.n;
+#pragma unroll
+          for (int k2 = 0; k2 < 2; ++k2) {
+            const int op = t + 128 * k2;
+            if (op > 190) break;
+            float vsum = 0.f;
+#pragma unroll
+            for (int p2 = 0; p2 < 4; ++p2) {
+              const int x = op - 96 + 32 * p2;  // = lane' + 16 jj'
+              if (x < 0) continue;
+              const int j1 = x >> 4;
+              if (j1 >= 1 && j1 - 1 < 6) vsum += Cb[(p2 * 6 + j1 - 1) * 32 + (x - 16 * (j1 - 1))];
+              if (j1 < 6) vsum += Cb[(p2 * 6 + j1) * 32 + (x - 16 * j1)];
+            }
+            const int o = obase + op;
+            if (o >= 0 && o < a.n) red_add(dd + o, vsum);
+          }
         }
       }
-      // ring entry released only now: the producer claims at most one item ahead
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[V_IE + rs]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc(tbase, 512);
+  if (warp == kVsSoftWarps + 1) tmem_dealloc(tbase, 512);
 }
 
 // Units from the device-selected families (one CTA, a warp per kv group): up to
@@ -644,34 +591,24 @@ __global__ void diag_add_kernel(float* diag_out, const float* dtmp, int n, const
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-static void tail_chunking(int r_hi, int* nkt, int* t1, int* c1, int* t2, int* c2) {
-  *nkt = (r_hi + kTile - 1) / kTile;
-  *t1 = std::max(2, (*nkt + kVsMaxChunks - 1) / kVsMaxChunks);
-  *c1 = (*nkt + *t1 - 1) / *t1;
-  *t2 = 2;
-  *c2 = (*nkt + *t2 - 1) / *t2;
-}
+static int sched_ints(int hh_total) { return hh_total * (kVsGroup + 2); }
 
-// pass-1 blocks between a unit's pass 1 and its pass 2: enough that the grid's
-// claimed-but-unfinished window (~2 items per CTA) lies inside later units' pass 1
-static int tail_lookahead(int c1, int sms) {
+// units per wave: W units' K (256 n bytes each) stay L2-resident between the passes
+static int tail_wave_units(int n) {
   static const int env = [] {
-    const char* e = getenv("SA_VS_LOOK");  // A/B override
+    const char* e = getenv("SA_VS_WAVE");  // A/B override
     return e ? atoi(e) : 0;
   }();
   if (env > 0) return env;
-  return std::max(1, std::min(4, (2 * sms + c1 - 1) / c1));
+  return (int)std::max<size_t>(1, kVsWaveBytes / ((size_t)n * 256));
 }
 
-static int sched_ints(int hh_total) { return 1 + hh_total * (kVsGroup + 2); }
-
-// workspace of one estimator call: statistics, queue state, unit lists and
-// (when rows > 64 or accumulate is possible) the scratch diagonal
+// workspace of one estimator call: statistics, completion state, unit lists and
+// the scratch diagonal of accumulating launches
 size_t tail_workspace_bytes(int hh_total, int n, int r_hi) {
-  int nkt, t1, c1, t2, c2;
-  tail_chunking(r_hi, &nkt, &t1, &c1, &t2, &c2);
+  (void)r_hi;
   const size_t U = hh_total;
-  return align256(U * c1 * 256 * sizeof(float2)) + align256(U * kVsGroup * 256 * sizeof(float2)) +
+  return align256(U * kVsMaxCta * 2 * 256 * sizeof(float2)) + align256(U * kVsGroup * 256 * sizeof(float2)) +
          align256(U * 256 * 4) + align256((size_t)sched_ints(hh_total) * 4) +
          align256((size_t)(hh_total + 2) * 4) + align256(U * sizeof(int4)) + align256((size_t)hh_total * n * 4) +
          256;
@@ -693,15 +630,15 @@ static int launch_tail64(int batch, int heads, int kv_heads, int n, float scale,
   a.r_lo = r_lo;
   a.r_hi = r_hi;
   a.qrow0 = r_hi - 64;
-  tail_chunking(r_hi, &a.nkt, &a.t1, &a.c1, &a.t2, &a.c2);
-  a.look = tail_lookahead(a.c1, device_sm_count());
+  a.nkt = (r_hi + kTile - 1) / kTile;
+  a.wave_units = tail_wave_units(n);
   a.scale_log2 = scale * 1.4426950408889634f;
   if (ws_bytes < tail_workspace_bytes(a.hh_total, n, r_hi))
     return fail(SA_ERR_DIMENSION, "score_tail workspace too small");
   const size_t U = a.hh_total;
   char* w = reinterpret_cast<char*>(ws);
   a.stats = reinterpret_cast<float2*>(w);
-  w += align256(U * a.c1 * 256 * sizeof(float2));
+  w += align256(U * kVsMaxCta * 2 * 256 * sizeof(float2));
   a.stats2 = reinterpret_cast<float2*>(w);
   w += align256(U * kVsGroup * 256 * sizeof(float2));
   a.lse2 = reinterpret_cast<float*>(w);
@@ -713,9 +650,8 @@ static int launch_tail64(int batch, int heads, int kv_heads, int n, float scale,
   int4* units = reinterpret_cast<int4*>(w);
   w += align256(U * sizeof(int4));
   float* dtmp = reinterpret_cast<float*>(w);
-  a.next = sched;
-  a.grp_done = sched + 1;
-  a.unit_done = sched + 1 + a.hh_total * kVsGroup;
+  a.grp_done = sched;
+  a.unit_done = sched + a.hh_total * kVsGroup;
   a.ready = a.unit_done + a.hh_total;
   a.col_out = col_out;
   a.diag_dst = accumulate ? dtmp : diag_out;
@@ -729,8 +665,8 @@ static int launch_tail64(int batch, int heads, int kv_heads, int n, float scale,
   once_per_device(attr_done, [] {
     cudaFuncSetAttribute(vs_estimator_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kVsSmemBytes);
   });
-  const long long max_items = (long long)a.hh_total * (a.c1 + a.c2);
-  const int grid = (int)std::min<long long>(device_sm_count(), max_items);
+  // one CTA per SM: the waiting CTAs of a unit only wait for CTAs that are resident
+  const int grid = device_sm_count();
   vs_estimator_kernel<<<grid, kVsThreads, kVsSmemBytes, st>>>(a);
   if ((rc = check_launch("vs_estimator_kernel"))) return rc;
   if (accumulate) {
