@@ -38,6 +38,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -51,16 +52,18 @@ namespace sa {
 constexpr int kVsSoftWarps = 16;
 constexpr int kVsSoft = kVsSoftWarps * 32;       // 512 softmax threads
 constexpr int kVsThreads = kVsSoft + 64;         // + warp 16 TMA producer, warp 17 MMA issuer
-constexpr int kVsKSlots = 3;
+constexpr int kVsKSlots = 2;
 constexpr int kVsGroup = 16;                     // pass-1 chunks merged per first-level group
 constexpr int kVsMaxCta = 16 * kVsGroup;         // CTAs per unit (two-level merge)
 constexpr size_t kVsWaveBytes = 64ull << 20;     // K bytes of one wave (L2-resident between passes)
-// shared memory: Q [64 KB] | K [3 slots][32 KB] | D [16 warps][16 x 32] f32 |
-// C [4 groups][2 buffers][4 warps][6][32] f32 | misc (barriers, flags, -lse2, merge exchange)
+// shared memory: Q [64 KB] | K [2 slots][32 KB] | D [16 warps][16 rows][kDw] f32 (skewed
+// diagonal blocks) | C2 [4 groups][191 diagonals][9] f32 | misc (barriers, flags, -lse2, merge exchange)
+constexpr int kDw = 50;                          // D row stride: conflict-free skewed writes and half-column reads
+constexpr int kC2Floats = 191 * 9 + 1;
 constexpr int kVsOffK = 65536;
 constexpr int kVsOffD = kVsOffK + kVsKSlots * 32768;
-constexpr int kVsOffC = kVsOffD + kVsSoftWarps * 2048;
-constexpr int kVsOffMisc = kVsOffC + 4 * 2 * 768 * 4;
+constexpr int kVsOffC = kVsOffD + kVsSoftWarps * 16 * kDw * 4;
+constexpr int kVsOffMisc = kVsOffC + ((4 * kC2Floats * 4 + 1023) & ~1023);
 constexpr int kVsOffNl = kVsOffMisc + 256;       // [4 groups][64] -lse2 of the group's rows
 constexpr int kVsOffX = kVsOffNl + 1024;         // [256] float2 merge exchange
 constexpr int kVsSmemBytes = kVsOffX + 2048 + 1024;
@@ -95,7 +98,21 @@ struct TailArgs {
   int accumulate;      // col_out += (diag goes to a scratch buffer, added afterwards)
   const int4* units;
   const int32_t* unit_count;
+  unsigned long long* trace;  // optional [grid, 64] globaltimer stamps (tools/vs_trace.py)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void vs_stamp(const TailArgs& a, int v, int e) {
+  if (a.trace && v < 8) a.trace[blockIdx.x * 64 + v * 8 + e] = gtimer();
+}
+// per-tile clock stamps of CTA 0, wave 0 (tools/vs_trace.py): [gridDim.x * 64 + tile * 8 + e]
+__device__ __forceinline__ void vs_tstamp(const TailArgs& a, int v, int tile, int e) {
+  if (a.trace && v == 0 && blockIdx.x == 0 && tile < 32) a.trace[gridDim.x * 64 + tile * 8 + e] = clock64();
+}
 
 // 2^x for a pair on the FMA pipe: x = j + f (j = rint x by the 1.5*2^23 magic
 // add), 2^f by a degree-5 fit on [-0.5, 0.5] (max relative error 2.4e-7 in
@@ -122,6 +139,27 @@ __device__ __forceinline__ float2 exp2_poly5(float2 x) {
 template <int POLY8>
 __device__ __forceinline__ float2 exp2_mix(float2 x, int p) {
   if ((p & 7) < POLY8) return exp2_poly5(x);
+  return make_float2(fast_exp2(x.x), fast_exp2(x.y));
+}
+
+// for sums only: x < -125 (masked) contributes 2^-125 instead of 0, which no
+// row sum (>= 1, the maximum's own term) can notice
+__device__ __forceinline__ float2 exp2_poly5_sum(float2 x) {
+  const float2 xc = make_float2(fmaxf(x.x, -125.f), fmaxf(x.y, -125.f));
+  const float2 t = fadd2(xc, make_float2(12582912.f, 12582912.f));
+  const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(j, make_float2(-1.f, -1.f), xc);
+  float2 p = ffma2(make_float2(0.0013277214f, 0.0013277214f), f, make_float2(0.0096755475f, 0.0096755475f));
+  p = ffma2(p, f, make_float2(0.0555071086f, 0.0555071086f));
+  p = ffma2(p, f, make_float2(0.2402212024f, 0.2402212024f));
+  p = ffma2(p, f, make_float2(0.6931469440f, 0.6931469440f));
+  p = ffma2(p, f, make_float2(1.0000001192f, 1.0000001192f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+template <int POLY8>
+__device__ __forceinline__ float2 exp2_mix_sum(float2 x, int p) {
+  if ((p & 7) < POLY8) return exp2_poly5_sum(x);
   return make_float2(fast_exp2(x.x), fast_exp2(x.y));
 }
 
@@ -160,6 +198,8 @@ __device__ __forceinline__ VsPlace vs_place(const TailArgs& a) {
   return p;
 }
 
+// P1POLY / P2POLY: pairs (of every 8) whose exp runs on the FMA pipe in pass 1 / 2
+template <int P1POLY, int P2POLY>
 __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __grid_constant__ TailArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -213,6 +253,12 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
           }
         }
         const int hkv = (un.x / a.heads) * a.kv_heads + (un.x % a.heads) / (a.heads / a.kv_heads);
+        // the whole K range of this CTA into L2 first: the two-slot ring then
+        // waits for L2 latency instead of DRAM latency (pass 2 re-reads it from L2)
+        for (int kt = pl.t_lo; kt < pl.t_hi; ++kt) {
+          tma_prefetch_l2_3d(&a.tmap_k, 0, kt * kTile, hkv);
+          tma_prefetch_l2_3d(&a.tmap_k, 64, kt * kTile, hkv);
+        }
         for (int pass = 0; pass < 2; ++pass)
           for (int kt = pl.t_lo; kt < pl.t_hi; ++kt, ++kj) {
             const int ks = kj % kVsKSlots;
@@ -242,10 +288,12 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
           for (int kt = pl.t_lo; kt < pl.t_hi; ++kt, ++kj, ++jt) {
             const int ks = kj % kVsKSlots, b = jt & 1;
             mbar_wait(&bars[V_KF + ks], (kj / kVsKSlots) & 1);
+            if (pass == 1) vs_tstamp(a, v, kt - pl.t_lo, 4);
             if (jt >= 2) {
               mbar_wait(&bars[V_SE + b], ((jt >> 1) - 1) & 1);
               mbar_wait(&bars[V_SE + 2 + b], ((jt >> 1) - 1) & 1);
             }
+            if (pass == 1) vs_tstamp(a, v, kt - pl.t_lo, 3);
             tc_fence_after();
             const uint32_t k_addr = smem_u32(sK + ks * 32768);
             const uint32_t d0 = tbase + b * 256;
@@ -285,12 +333,17 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
     const int lane = threadIdx.x & 31;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const float sl2 = a.scale_log2;
-    float* Dw = reinterpret_cast<float*>(smem + kVsOffD) + warp * 512;              // [16 rows][32 keys]
-    float* sC = reinterpret_cast<float*>(smem + kVsOffC) + grp * 1536;              // [2][4 warps][6][32]
+    float* Dw = reinterpret_cast<float*>(smem + kVsOffD) + warp * (16 * kDw);      // [16 rows][kDw] skewed
+    float* C2 = reinterpret_cast<float*>(smem + kVsOffC) + grp * kC2Floats;         // [191 ops][9]
     float* nl = reinterpret_cast<float*>(smem + kVsOffNl) + grp * 64;               // -lse2 of the group's rows
     float2* xch = reinterpret_cast<float2*>(smem + kVsOffX);
     const int ng = (pl.cpu + kVsGroup - 1) / kVsGroup;
-    int jt = 0, cbuf = 0;
+    int jt = 0;
+    // zero the never-written parts of this warp's skewed buffer and of the
+    // group's C2 (the written positions are the same for every tile)
+    for (int x = lane; x < 16 * kDw; x += 32) Dw[x] = 0.f;
+    for (int x = t; x < kC2Floats; x += 128) C2[x] = 0.f;
+    named_bar_sync(2 + grp, 128);
     for (int v = 0; v < pl.nwaves; ++v) {
       const int u = v * pl.W + pl.ws;
       if (u >= pl.U) break;
@@ -298,6 +351,7 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
       const int ha = slot ? un.z : un.x, hb = slot ? un.w : un.y;
       const bool on = ha >= 0;
       // ---------------------------------------------------- pass 1 (thread = row, half the keys)
+      if (threadIdx.x == 0) vs_stamp(a, v, 0);
       {
         const int hrow = (t < 64) ? ha : hb;
         const int i = a.qrow0 + (t & 63);
@@ -306,6 +360,7 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
         for (int kt = pl.t_lo; kt < pl.t_hi; ++kt, ++jt) {
           const int b = jt & 1;
           mbar_wait(&bars[V_SF + slot * 2 + b], (jt >> 1) & 1);
+          if (threadIdx.x == 0) vs_tstamp(a, v, kt - pl.t_lo, 0);
           if (on) {
             tc_fence_after();
             uint32_t s[64];
@@ -315,9 +370,11 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(&bars[V_SE + slot * 2 + b]);
+            if (threadIdx.x == 0) vs_tstamp(a, v, kt - pl.t_lo, 1);
+            const int lim = i - (kt * kTile + 64 * sub);  // keep columns c <= lim
+            const bool diag_tile = __any_sync(0xffffffffu, active && lim < 63);  // warp-uniform
             if (active) {
-              const int lim = i - (kt * kTile + 64 * sub);  // keep columns c <= lim
-              if (lim < 63) {
+              if (diag_tile) {
 #pragma unroll
                 for (int c = 0; c < 64; ++c)
                   if (c > lim) s[c] = __float_as_uint(-INFINITY);
@@ -339,13 +396,14 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
 #pragma unroll
                 for (int c = 0; c < 64; c += 2) {
                   const float2 x = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2, mo2);
-                  acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], exp2_mix<3>(x, c >> 1));
+                  acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], exp2_mix_sum<P1POLY>(x, c >> 1));
                 }
                 const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
                 ssum = ssum * fast_exp2(m - mn) + ((a01.x + a01.y) + (a23.x + a23.y));
                 m = mn;
               }
             }
+            if (threadIdx.x == 0) vs_tstamp(a, v, kt - pl.t_lo, 2);
           } else {
             mbar_arrive(&bars[V_SE + slot * 2 + b]);
           }
@@ -371,6 +429,7 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
           }
         }
         named_bar_sync(1, kVsSoft);
+        if (threadIdx.x == 0) vs_stamp(a, v, 1);
         const int g1 = pl.rank / kVsGroup;
         if (threadIdx.x == 0) {  // barrier, then one gpu-scope fence + atomic (release pattern)
           __threadfence();
@@ -415,6 +474,7 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
             if (threadIdx.x == 0) {
               __threadfence();
               st_release(&a.ready[u], 1);
+              vs_stamp(a, v, 2);
             }
           }
         }
@@ -427,12 +487,19 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
           if (t == 0) {
             while (ld_relaxed(&a.ready[u]) == 0) __nanosleep(64);
             __threadfence();  // acquire: the statistics written before the release
+            if (threadIdx.x == 0) vs_stamp(a, v, 3);
           }
           named_bar_sync(2 + grp, 128);
           if (t < 64) nl[t] = -__ldcg(a.lse2 + (size_t)u * 256 + slot * 128 + sub * 64 + t);
           named_bar_sync(2 + grp, 128);
         }
         const float2 sc2 = make_float2(sl2, sl2);
+        const int kslot = 4 * (q4 & 1);  // C2 slot of this warp's blocks: m + 4 (q4 & 1)
+        // diagonal op of block m, main column lane: 16 m + 96 - 32 q4 + 46 - lane;
+        // second column 32 + (lane >> 1): 16 m + 96 - 32 q4 + 14 - (lane >> 1)
+        const int op_main = 142 - 32 * q4 - lane;
+        const int op_sec = 110 - 32 * q4 - (lane >> 1);
+        const bool sec_on = (lane & 1) == 0 && lane < 30;
         for (int kt = pl.t_lo; kt < pl.t_hi; ++kt, ++jt) {
           const int b = jt & 1;
           mbar_wait(&bars[V_SF + slot * 2 + b], (jt >> 1) & 1);
@@ -443,8 +510,7 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
           tc_fence_after();
           const int j = kt * kTile + t;
           const int obase = a.qrow0 - kt * kTile - 127;
-          // R[jj]: this lane's partial of diagonal op = lane + 16 jj + 96 - 32 q4
-          float R[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          float Pm[4], Ps[4];  // per 16-row block: main / second column sums
           float2 cs = make_float2(0.f, 0.f);
 #pragma unroll
           for (int qh = 0; qh < 2; ++qh) {
@@ -465,8 +531,8 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
                                 make_float2(nv.x, nv.y));
               float2 x1 = ffma2(make_float2(__uint_as_float(s[c + 2]), __uint_as_float(s[c + 3])), sc2,
                                 make_float2(nv.z, nv.w));
-              float2 e0 = make_float2(fast_exp2(x0.x), fast_exp2(x0.y));
-              float2 e1 = make_float2(fast_exp2(x1.x), fast_exp2(x1.y));
+              float2 e0 = exp2_mix<P2POLY>(x0, c >> 1);
+              float2 e1 = exp2_mix<P2POLY>(x1, (c >> 1) + 1);
               if (cut) {
                 e0.x = c >= cmin ? e0.x : 0.f;
                 e0.y = c + 1 >= cmin ? e0.y : 0.f;
@@ -479,25 +545,26 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
               s[c + 2] = __float_as_uint(e1.x);
               s[c + 3] = __float_as_uint(e1.y);
             }
-            // two 16-row blocks through this warp's 16 x 32 buffer: lane l
-            // writes key l of each row; the rotated read (row r, key
-            // (r + 31 - lane) & 31) gives diagonal lane (r <= lane) or
-            // lane + 32 (r > lane) of the block, bank-conflict free
+            // two 16-row blocks through this warp's skewed buffer: lane l writes
+            // row c at column l - c + 15, so column x holds one diagonal
+            // (c + 31 - l = 46 - x) with zeros elsewhere: lane x sums column x,
+            // lanes 2k, 2k+1 sum half of column 32 + k each; no selects, and
+            // every address is the lane base plus an immediate
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               __syncwarp();
 #pragma unroll
-              for (int c = 0; c < 16; ++c) Dw[c * 32 + lane] = __uint_as_float(s[16 * e + c]);
+              for (int c = 0; c < 16; ++c) Dw[c * kDw - c + 15 + lane] = __uint_as_float(s[16 * e + c]);
               __syncwarp();
-              float A = 0.f, B = 0.f;
+              float v1 = 0.f, v2 = 0.f;
 #pragma unroll
-              for (int r = 0; r < 16; ++r) {
-                const float x = Dw[r * 32 + ((r + 31 - lane) & 31)];
-                if (r <= lane) A += x;
-                else B += x;
-              }
-              R[2 * qh + e] += A;
-              R[2 * qh + e + 2] += B;
+              for (int c = 0; c < 16; ++c) v1 += Dw[c * kDw + lane];
+              const float* col2 = Dw + 8 * (lane & 1) * kDw + 32 + (lane >> 1);  // lanes 30, 31: zero column 47
+#pragma unroll
+              for (int c = 0; c < 8; ++c) v2 += col2[c * kDw];
+              v2 += __shfl_xor_sync(0xffffffffu, v2, 1);
+              Pm[2 * qh + e] = v1;
+              Ps[2 * qh + e] = v2;
             }
           }
           if (j < a.n) {
@@ -505,30 +572,27 @@ __global__ void __launch_bounds__(kVsThreads, 1) vs_estimator_kernel(const __gri
             const float tot = cs.x + cs.y;
             *dst = a.accumulate ? (*dst + tot) : tot;
           }
-          // the four warps' partials meet in C (double-buffered per tile)
-          float* Cb = sC + (cbuf & 1) * 768;
-          ++cbuf;
+          // partials -> C2[op][slot] (one writer per entry), then each thread sums
+          // the 8 slots of diagonals t and t + 128 in slot order
+          named_bar_sync(2 + grp, 128);  // the previous tile's readers are done
 #pragma unroll
-          for (int jj = 0; jj < 6; ++jj) Cb[(q4 * 6 + jj) * 32 + lane] = R[jj];
+          for (int m = 0; m < 4; ++m) {
+            C2[(op_main + 16 * m) * 9 + kslot + m] = Pm[m];
+            if (sec_on) C2[(op_sec + 16 * m) * 9 + kslot + m] = Ps[m];
+          }
           named_bar_sync(2 + grp, 128);
           float* dd = a.diag_dst + (size_t)h * a.n;
 #pragma unroll
           for (int k2 = 0; k2 < 2; ++k2) {
             const int op = t + 128 * k2;
             if (op > 190) break;
-            float vsum = 0.f;
-#pragma unroll
-            for (int p2 = 0; p2 < 4; ++p2) {
-              const int x = op - 96 + 32 * p2;  // = lane' + 16 jj'
-              if (x < 0) continue;
-              const int j1 = x >> 4;
-              if (j1 >= 1 && j1 - 1 < 6) vsum += Cb[(p2 * 6 + j1 - 1) * 32 + (x - 16 * (j1 - 1))];
-              if (j1 < 6) vsum += Cb[(p2 * 6 + j1) * 32 + (x - 16 * j1)];
-            }
+            const float* cr = C2 + op * 9;
+            const float vsum = ((cr[0] + cr[1]) + (cr[2] + cr[3])) + ((cr[4] + cr[5]) + (cr[6] + cr[7]));
             const int o = obase + op;
             if (o >= 0 && o < a.n) red_add(dd + o, vsum);
           }
         }
+        if (threadIdx.x == 0) vs_stamp(a, v, 4);
       }
     }
   }
@@ -590,6 +654,8 @@ __global__ void diag_add_kernel(float* diag_out, const float* dtmp, int n, const
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static unsigned long long* g_vs_trace = nullptr;  // set by sa_vs_trace_buffer (profiling only)
 
 static int sched_ints(int hh_total) { return hh_total * (kVsGroup + 2); }
 
@@ -658,16 +724,36 @@ static int launch_tail64(int batch, int heads, int kv_heads, int n, float scale,
   a.accumulate = accumulate;
   a.units = units;
   a.unit_count = list + 1;
+  a.trace = g_vs_trace;
   build_units_kernel<<<1, 1024, 0, st>>>(gate, gate_val, a.hh_total, heads, kv_heads, units, list + 1, list + 2,
                                           list, sched, sched_ints(a.hh_total));
   if ((rc = check_launch("build_units_kernel"))) return rc;
+  // exp split between MUFU and the FMA pipe per pass (SA_VS_POLY="p1,p2" for A/B)
+  static const int poly = [] {
+    const char* e = getenv("SA_VS_POLY");
+    int p1 = 3, p2 = 0;
+    if (e) sscanf(e, "%d,%d", &p1, &p2);
+    return p1 * 10 + p2;
+  }();
+  void (*kern)(TailArgs);
+  switch (poly) {
+    case 0: kern = vs_estimator_kernel<0, 0>; break;
+    case 20: kern = vs_estimator_kernel<2, 0>; break;
+    case 40: kern = vs_estimator_kernel<4, 0>; break;
+    case 32: kern = vs_estimator_kernel<3, 2>; break;
+    default: kern = vs_estimator_kernel<3, 0>; break;
+  }
   static std::atomic<uint64_t> attr_done{0};
   once_per_device(attr_done, [] {
-    cudaFuncSetAttribute(vs_estimator_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kVsSmemBytes);
+    cudaFuncSetAttribute(vs_estimator_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kVsSmemBytes);
+    cudaFuncSetAttribute(vs_estimator_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kVsSmemBytes);
+    cudaFuncSetAttribute(vs_estimator_kernel<3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kVsSmemBytes);
+    cudaFuncSetAttribute(vs_estimator_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kVsSmemBytes);
+    cudaFuncSetAttribute(vs_estimator_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kVsSmemBytes);
   });
   // one CTA per SM: the waiting CTAs of a unit only wait for CTAs that are resident
   const int grid = device_sm_count();
-  vs_estimator_kernel<<<grid, kVsThreads, kVsSmemBytes, st>>>(a);
+  kern<<<grid, kVsThreads, kVsSmemBytes, st>>>(a);
   if ((rc = check_launch("vs_estimator_kernel"))) return rc;
   if (accumulate) {
     dim3 g2((n + 1023) / 1024, a.hh_total);
@@ -699,6 +785,13 @@ int launch_score_tail(int batch, int heads, int kv_heads, int n, float scale, co
 }
 
 }  // namespace sa
+
+// Profiling hook: a device buffer of [grid, 64] u64 globaltimer stamps per
+// estimator launch (nullptr disables).  Not part of the reference interface.
+extern "C" int sa_vs_trace_buffer(void* p) {
+  sa::g_vs_trace = reinterpret_cast<unsigned long long*>(p);
+  return 0;
+}
 
 extern "C" size_t sa_score_tail_workspace(int batch, int heads, int n, int r_hi) {
   return sa::tail_workspace_bytes(batch * heads, n, r_hi);
