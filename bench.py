@@ -53,7 +53,38 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-128k", action="store_true", help="skip the 131072-token sub-record")
+    ap.add_argument("--no-est", action="store_true", help="skip the all-VS estimator roofline block")
     return ap.parse_args()
+
+
+def maybe_relaunch(args) -> int | None:
+    """--gpus N without a torchrun environment: re-run this command under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous) and return its
+    exit code; with WORLD_SIZE set it must equal --gpus."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus:
+            raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; they must match")
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd[1:6])} ...", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def common_config(args, world: int) -> dict:
+    """The workload description both arms report (identical keys and values)."""
+    return {"workload": f"llama3-8b-attn-layer-{args.ctx // 1024}k-{args.mode}", "heads": H, "kv_heads": HK,
+            "head_dim": D, "seq_len": args.ctx, "batch": 1, "mode": args.mode,
+            "pattern": args.pattern, "seed": args.seed, "n_gpus": world}
 
 
 def synth_inputs(seed: int, ctx: int):
@@ -182,70 +213,142 @@ def cpu_cores():
 
 
 def stratified_cpu_ms(q, k, v, ctx, budget_steps=None):
-    """Time one head per family present in the oracle plan; extrapolate the layer."""
-    from oracle import sparse_oracle as O
+    """The CPU baseline of our arm's line: one head per family of the
+    reference's own auto plan through the reference package's per-head
+    prefill body (the oracle port when the package is absent), extrapolated
+    to the layer by the family counts."""
+    ref = _reference_module()
+    g = H // HK
+    cal = min(64, ctx)
+    if ref is not None:
+        space = ref.default_search_space(cal, D)
+        mats = lambda h: ref.AttnMatrices(q[h], k[h // g], v[h // g], causal=True)  # noqa: E731
+        pats = [ref.select_pattern_windowed(mats(h), space, cal).chosen for h in range(H)]
 
-    pats = oracle_plan(q, k, v, ctx)
+        def head_s(h):
+            t = time.perf_counter()
+            m = mats(h)
+            pat = ref.select_pattern_windowed(m, space, cal).chosen
+            ref.sparse_attention(m, ref.build_index(m, pat, mode="estimated", q_est=min(64, ctx)),
+                                 need_weights=False)
+            return time.perf_counter() - t
+        kind, what = "reference", "the reference package (baseline/_ref)"
+    else:
+        pats = oracle_plan(q, k, v, ctx)
+        head_s = lambda h: oracle_head_seconds(q, k, v, h, ctx)[0]  # noqa: E731
+        kind, what = "port", "the oracle port of the reference algorithm"
     fam_of = lambda p: type(p).__name__  # noqa: E731
-    counts = {}
-    first = {}
+    counts, first = {}, {}
     for h, p in enumerate(pats):
         counts[fam_of(p)] = counts.get(fam_of(p), 0) + 1
         first.setdefault(fam_of(p), h)
-    per = {}
-    for f, h in first.items():
-        per[f] = oracle_head_seconds(q, k, v, h, ctx)[0]
+    per = {f: head_s(h) for f, h in first.items()}
     ms = 1e3 * sum(counts[f] * per[f] for f in counts)
-    sample = (f"one full {ctx}-token head per family of the oracle's own auto plan "
-              f"({', '.join(f'{f}x{counts[f]}: {per[f]:.2f}s' for f in counts)}), "
-              f"layer = sum(count * per-head seconds); oracle port of the reference algorithm")
-    del O
-    return ms, sample
+    sample = (f"one full {ctx}-token head per family of the reference's own auto plan through {what}'s per-head "
+              f"prefill body ({', '.join(f'{f}x{counts[f]}: {per[f]:.2f}s' for f in counts)}), "
+              f"layer = sum(count * per-head seconds)")
+    return ms, sample, kind
+
+
+def _reference_module():
+    """The unmodified reference package installed into baseline/_ref (pip
+    --target), or None."""
+    ref_dir = os.path.join(HERE, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "sparseattn")):
+        return None
+    sys.path.insert(0, ref_dir)
+    try:
+        import sparseattn
+    except Exception:
+        return None
+    finally:
+        sys.path.remove(ref_dir)
+    return sparseattn
 
 
 def run_reference(args):
+    """Reference arm: the reference's own CPU path (runtime.prefill's per-head
+    body, runtime.py:174-193: AttnMatrices -> select_pattern_windowed ->
+    build_index(estimated) -> sparse_attention) on the box's host cores, one
+    head per step; the layer time is the per-family mean times the family
+    counts of the reference's own selection over all heads."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    ref = _reference_module()
     q, k, v = synth_inputs(args.seed, args.ctx)
-    pats = oracle_plan(q, k, v, args.ctx)
+    g = H // HK
+    cal = min(64, args.ctx)
+    q_est = min(64, args.ctx)
+    if ref is not None:
+        kind = "reference"
+        space = ref.default_search_space(cal, D)
+
+        def mats(h):
+            return ref.AttnMatrices(q[h], k[h // g], v[h // g], causal=True)
+
+        def select(h):
+            return ref.select_pattern_windowed(mats(h), space, cal).chosen
+
+        def head(h):
+            m = mats(h)
+            pat = ref.select_pattern_windowed(m, space, cal).chosen
+            idx = ref.build_index(m, pat, mode="estimated", q_est=q_est)
+            ref.sparse_attention(m, idx, need_weights=False)
+    else:  # no installed reference: the oracle port of the same algorithm
+        from oracle import sparse_oracle as O
+
+        kind = "port"
+        ospace = O.default_space(cal, D)
+
+        def select(h):
+            return O.select_windowed(q[h], k[h // g], v[h // g], ospace, cal)[0]
+
+        def head(h):
+            oracle_head_seconds(q, k, v, h, args.ctx)
+    pats = [select(h) for h in range(H)]
     fam_of = lambda p: type(p).__name__  # noqa: E731
     counts, heads = {}, {}
     for h, p in enumerate(pats):
         counts[fam_of(p)] = counts.get(fam_of(p), 0) + 1
         heads.setdefault(fam_of(p), []).append(h)
     fams = sorted(counts)
-    cheapest = "Blk" if "Blk" in heads else fams[0]
+    cheapest = min(fams, key=lambda f: {"BlockSparse": 0, "Blk": 0}.get(f, 1))
     for _ in range(args.warmup):
-        oracle_head_seconds(q, k, v, heads[cheapest][0], args.ctx)
+        head(heads[cheapest][0])
     samples = {f: [] for f in fams}
-    step_ms = []
+    step_s = []
     t0 = time.perf_counter()
-    for s in range(args.steps):
-        f = fams[s % len(fams)]
-        hsel = heads[f][(s // len(fams)) % len(heads[f])]
-        sec, _ = oracle_head_seconds(q, k, v, hsel, args.ctx)
+    for s_ in range(args.steps):
+        f = fams[s_ % len(fams)]
+        hsel = heads[f][(s_ // len(fams)) % len(heads[f])]
+        ts = time.perf_counter()
+        head(hsel)
+        sec = time.perf_counter() - ts
         samples[f].append(sec)
-        known = {g: statistics.mean(x) for g, x in samples.items() if x}
-        # extrapolate with the families measured so far (missing ones at the mean)
-        avg = statistics.mean(known.values())
-        step_ms.append(1e3 * sum(counts[g] * known.get(g, avg) for g in fams))
+        step_s.append(sec)
     wall = time.perf_counter() - t0
-    value = step_ms[-1]
+    known = {f: statistics.mean(x) for f, x in samples.items() if x}
+    avg = statistics.mean(known.values())
+    value = 1e3 * sum(counts[f] * known.get(f, avg) for f in fams)
     cores = cpu_cores()
-    sample = (f"each step = one full {args.ctx}-token head of the oracle's own auto plan, families round-robin "
-              f"({', '.join(f'{g}x{counts[g]}' for g in fams)}); layer ms = sum(count * mean per-head ms)")
+    sample = (f"each step = one full {args.ctx}-token head through the {'reference package' if ref else 'oracle port'}'s "
+              f"per-head prefill body (runtime.py:174-193), families round-robin "
+              f"({', '.join(f'{f}x{counts[f]}: {known.get(f, avg):.2f}s' for f in fams)}); value = layer ms = "
+              f"sum(count * mean per-head ms); ms_per_step = mean wall ms of one sampled head")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "ms/layer",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value, 3),
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * statistics.mean(step_s), 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (uniform [-1,1], rng([seed, ctx]), bf16-rounded)",
-        "config": {"workload": f"llama3-8b-attn-layer-{args.ctx // 1024}k-auto", "heads": H, "kv_heads": HK,
-                   "head_dim": D, "seq_len": args.ctx, "mode": "auto", "parallelism": "none (CPU)"},
-        "cpu_baseline": {"value": round(value, 3), "unit": "ms/layer", "cores": cores, "kind": "port",
+        "data": "synthetic (uniform [-1,1], rng([seed, ctx]) GQA draw, bf16-rounded)",
+        "config": common_config(args, world),
+        "cpu_baseline": {"value": round(value, 3), "unit": "ms/layer", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "ms/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": round(wall, 1),
+        "families": counts,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -271,6 +374,187 @@ def count_step_kernels(step):
     return sum(names.values()), names
 
 
+def layer_graph(plan, qd, kd, vd, out, ws, flag, cache_k, cache_v):
+    """CUDA graph of the whole layer step: selection + sa_prefill, which also
+    runs AttnMatrices' finiteness scan (core.py:72-74) and the KvCache fill
+    (runtime.py:197) on a side stream beside the estimators."""
+    plan.desc.check_flag = flag.data_ptr()
+    plan.desc.cache_k, plan.desc.cache_v = cache_k.data_ptr(), cache_v.data_ptr()
+    plan.desc.cache_capacity = cache_k.shape[1]
+    return plan.graph(qd, kd, vd, out, ws)
+
+
+def time_graph(graph, steps, dev_index, world=1, clocks=True):
+    import torch
+    import torch.distributed as dist
+
+    for _ in range(2):
+        graph.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev_index) if clocks else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if sampler:
+        sampler.__enter__()
+    e0.record()
+    for _ in range(steps):
+        graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
+    if world > 1:
+        dist.barrier()
+    return e0.elapsed_time(e1) / steps, sampler
+
+
+def stage_breakdown(plan, qd, kd, vd, out, ws, steps):
+    """Per-stage ms from eager steps with stage events (after the timed region)."""
+    import torch
+
+    evsets = []
+    for _ in range(steps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        for e in evs:
+            e.record()
+        evsets.append(evs)
+    torch.cuda.synchronize()
+    for evs in evsets:
+        evs[0].record()
+        if plan.mode == "auto":
+            plan.select(qd, kd, ws)
+        for i in range(5):
+            plan.desc.stage_events[i] = evs[1 + i].cuda_event
+        plan.run(qd, kd, vd, out, ws)
+        for i in range(5):
+            plan.desc.stage_events[i] = None
+        evs[6].record()
+    torch.cuda.synchronize()
+    stage = np.array([[evs[i].elapsed_time(evs[i + 1]) for i in range(6)] for evs in evsets])
+    return stage.mean(axis=0)  # select, vs-est, block-est, tiles, attention, (gather)
+
+
+def attn_roofline(plan, ws, attn_ms, n):
+    from paper_2412_06198_b200 import runtime as R
+    import torch
+
+    view = plan.views(ws)
+    cnt = R._wrap(view.tile_cnt, plan.hh * view.nqt, torch.int32).cpu().numpy()
+    exec_tiles = int(cnt.sum())
+    exec_flops = exec_tiles * 4.0 * 128 ** 3
+    peak, peak_sus, _, peak_kind = measured_peaks()
+    achieved = exec_flops / (attn_ms * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(HERE, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"attn_{n}_{plan.mode}")
+    return {"bound": "tensor", "kernel": "attn_fwd_kernel", "achieved": round(achieved, 1), "peak": peak,
+            "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "frac_sustained": round(achieved / peak_sus, 4),
+            "peak_kind": peak_kind, "traffic": traffic, "exec_tiles": exec_tiles, "attn_ms": round(attn_ms, 4),
+            "flops_per_launch": exec_flops,
+            "flops_note": "executed (q-tile, k-tile) pairs x 4*128^3 (QK^T and PV of a 128x128 tile, d=128)"}
+
+
+def e2e_host(R, q_h, k_h, v_h, cfg, mode, fixed, reps, world=1, dev=None):
+    """prefill() on HOST tensors (the public API): H2D of q/k/v, the layer,
+    D2H of the (1, n, H*d) output, all inside the wall-clock region."""
+    import torch
+    import torch.distributed as dist
+
+    kw = {"fixed_pattern": fixed} if fixed is not None else {}
+    res = None
+    for _ in range(2):
+        res = R.prefill(q_h, k_h, v_h, cfg, mode=mode, **kw)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    walls = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        res = R.prefill(q_h, k_h, v_h, cfg, mode=mode, **kw)
+        walls.append((time.perf_counter() - t0) * 1e3)
+    ms = statistics.median(walls)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    out = res.outputs
+    nbytes = lambda x: int(x.numel() * x.element_size()) if hasattr(x, "element_size") else int(x.nbytes)  # noqa
+    return ms, nbytes(q_h) + nbytes(k_h) + nbytes(v_h), nbytes(out), reps
+
+
+def estimator_roofline(n, dev, reps=5):
+    """The VS estimator chain of an all-VS layer (32 q / 8 kv heads, q_est = 64):
+    sa_score_tail (both passes, one kernel) + the stable top-k of the 32 column
+    and 32 diagonal rows (k = 3n/64, the auto VS pattern), timed with CUDA
+    events.  Algorithmic bytes: K read once (2 * n * 128 * 8) +
+    the Q tails (2 * 64 * 128 * 32) + fp32 column / diagonal scores written
+    (8 * n * 32) = 2304 n + 0.5 MB."""
+    import torch
+
+    from paper_2412_06198_b200 import _lib
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    q = (torch.rand((H, n, D), generator=g, device=dev) * 2 - 1).bfloat16()
+    k = (torch.rand((HK, n, D), generator=g, device=dev) * 2 - 1).bfloat16()
+    col = torch.empty((H, n), dtype=torch.float32, device=dev)
+    diag = torch.empty((H, n), dtype=torch.float32, device=dev)
+    kk = 3 * n // 64
+    ci = torch.empty((H, kk), dtype=torch.int32, device=dev)
+    di = torch.empty((H, kk), dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    wsb = int(lib.sa_score_tail_workspace(1, H, n, n))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    scale = 1 / math.sqrt(D)
+
+    def est():
+        _lib.call("sa_score_tail", 1, H, HK, n, scale, q.data_ptr(), k.data_ptr(), n - 64, n, col.data_ptr(),
+                  diag.data_ptr(), 0, None, 0, ws.data_ptr(), wsb, st)
+
+    def topk():
+        _lib.call("sa_topk_stable_f32", col.data_ptr(), H, n, n, kk, ci.data_ptr(), kk, st)
+        _lib.call("sa_topk_stable_f32", diag.data_ptr(), H, n, n, kk, di.data_ptr(), kk, st)
+
+    for _ in range(2):
+        est()
+        topk()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    t_est, t_topk = [], []
+    for _ in range(reps):
+        ev[0].record()
+        est()
+        ev[1].record()
+        topk()
+        ev[2].record()
+        torch.cuda.synchronize()
+        t_est.append(ev[0].elapsed_time(ev[1]) * 1e3)
+        t_topk.append(ev[1].elapsed_time(ev[2]) * 1e3)
+    est_us, topk_us = statistics.median(t_est), statistics.median(t_topk)
+    _, _, hbm, peak_kind = measured_peaks()
+    alg = 2304 * n + 2 * 64 * D * H
+    traffic = None
+    tp = os.path.join(HERE, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"vs_est_{n}")
+    chain = est_us + topk_us
+    return {"n": n, "heads": H, "kv_heads": HK, "q_est": 64, "topk_k": kk, "algorithmic_bytes": alg,
+            "estimator_us": round(est_us, 1), "topk_us": round(topk_us, 1), "chain_us": round(chain, 1),
+            "achieved_gbs": round(alg / (chain * 1e-6) / 1e9, 1),
+            "estimator_achieved_gbs": round(alg / (est_us * 1e-6) / 1e9, 1),
+            "peak_gbs": hbm, "peak_kind": peak_kind, "frac": round(alg / (chain * 1e-6) / 1e9 / hbm, 4),
+            "estimator_frac": round(alg / (est_us * 1e-6) / 1e9 / hbm, 4), "traffic": traffic,
+            "traffic_note": "ncu dram__bytes_read+write of vs_estimator_kernel (profiles/traffic.json)",
+            "floor_note": "two exact passes: 2 x 2*64*128*32*n bf16 MMA FLOP and 2 x 64*32*n exps; "
+                          "DESIGN.md 'VS estimator roofline'"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -278,22 +562,41 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: world size {world} != --gpus {args.gpus}")
     if world > 1:
         # SA_DIST_BACKEND=gloo lets ranks share one GPU (a dry run of the N > 1 path)
         backend = os.environ.get("SA_DIST_BACKEND", "nccl")
         torch.cuda.set_device(local % torch.cuda.device_count())
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
         else:
             dist.init_process_group(backend)
+        if dist.get_world_size() != args.gpus:
+            raise SystemExit(f"bench.py: communicator has {dist.get_world_size()} ranks, --gpus {args.gpus}")
+        print(f"bench.py: rank {rank}/{world} backend {dist.get_backend()} on cuda:{torch.cuda.current_device()}",
+              file=sys.stderr, flush=True)
     dev = torch.device("cuda", torch.cuda.current_device())
     if HK % world != 0:
         raise SystemExit(f"--gpus {world} must divide the {HK} kv heads")
 
-    from paper_2412_06198_b200 import _lib, runtime as R
+    from paper_2412_06198_b200 import runtime as R
+    from paper_2412_06198_b200.multigpu import gather_heads, shard_heads
     from paper_2412_06198_b200.patterns import BlockSparse, Triangular, VerticalSlash
 
-    from paper_2412_06198_b200.multigpu import gather_heads, shard_heads
+    def make_fixed(n):
+        mode = args.mode
+        fixed = None
+        if args.pattern:
+            fam, p1, p2 = args.pattern.split(":")
+            fixed = {"tri": Triangular, "vs": VerticalSlash, "block": BlockSparse}[fam](int(p1), int(p2))
+            mode = "fixed"
+        elif mode not in ("auto", "dense"):
+            from paper_2412_06198_b200.harness import fixed_pattern_for
+
+            fixed = fixed_pattern_for(mode, n)
+            mode = "fixed"
+        return mode, fixed
 
     n = args.ctx
     hk_l = HK // world
@@ -306,224 +609,191 @@ def run_ours(args):
     k_h = torch.from_numpy(np.ascontiguousarray(ks)).bfloat16().pin_memory()
     v_h = torch.from_numpy(np.ascontiguousarray(vs)).bfloat16().pin_memory()
     qd, kd, vd = q_h.to(dev), k_h.to(dev), v_h.to(dev)
-
-    mode = args.mode
-    fixed = None
-    if args.pattern:
-        fam, p1, p2 = args.pattern.split(":")
-        fixed = {"tri": Triangular, "vs": VerticalSlash, "block": BlockSparse}[fam](int(p1), int(p2))
-        mode = "fixed"
-    elif mode != "auto" and mode != "dense":
-        from paper_2412_06198_b200.harness import fixed_pattern_for
-
-        fixed = fixed_pattern_for(mode, n)
-        mode = "fixed"
+    mode, fixed = make_fixed(n)
     plan = R.PrefillPlan(1, h_l, hk_l, n, D, mode, fixed_pattern=fixed)
     ws = R._workspace(plan.ws_bytes, dev)
     out = torch.empty((1, n, h_l * D), dtype=torch.bfloat16, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    cache_k = torch.empty((hk_l, n, D), dtype=torch.bfloat16, device=dev)
+    cache_v = torch.empty((hk_l, n, D), dtype=torch.bfloat16, device=dev)
     final = torch.empty((n, H * D), dtype=torch.bfloat16, device=dev) if world > 1 else None
     # N > 1: the load-balanced layer (multigpu.BalancedLayer) is the timed step;
     # SA_MG_BALANCED=0 times the plain GQA-group sharding + output all-gather
     balanced = world > 1 and os.environ.get("SA_MG_BALANCED", "1") != "0"
-    layer = None
+    layer = peer = None
     if balanced:
         from paper_2412_06198_b200.multigpu import BalancedLayer
 
         qf, kf, vf = (torch.from_numpy(np.ascontiguousarray(x)).bfloat16().to(dev) for x in (q, k, v))
         layer = BalancedLayer(rank, world, H, HK, n, D, mode, fixed_pattern=fixed, device=dev)
-    # SA_MG_EXCHANGE=peer: the output all-gather fused into the attention epilogue
-    # (stores into every rank's CUDA-IPC-mapped output; multigpu.PeerOutputs)
-    peer = None
-    if balanced and os.environ.get("SA_MG_EXCHANGE", "nccl") == "peer":
-        from paper_2412_06198_b200.multigpu import PeerOutputs
+        layer.enable_checks(flag, cache_k, cache_v)
+        if os.environ.get("SA_MG_EXCHANGE", "nccl") == "peer":
+            from paper_2412_06198_b200.multigpu import PeerOutputs
 
-        peer = PeerOutputs(rank, world, n, H * D)
+            peer = PeerOutputs(rank, world, n, H * D)
 
-    def step(events=None):
-        if events is not None:
-            events[0].record()
+    # warm-up steps (eager), then the timed step
+    for _ in range(max(3, args.warmup)):
         if plan.mode == "auto":
             plan.select(qd, kd, ws)
-        if events is not None:
-            for i in range(5):
-                plan.desc.stage_events[i] = events[1 + i].cuda_event
         plan.run(qd, kd, vd, out, ws)
-        if events is not None:
-            for i in range(5):
-                plan.desc.stage_events[i] = None
-        if world > 1 and not balanced:
-            gather_heads(out[0], world, out=final)
-        if events is not None:
-            events[6].record()
-
-    for _ in range(max(3, args.warmup)):
-        step()
     torch.cuda.synchronize()
-    if balanced and peer is not None:
+    if balanced:
         def gstep():
-            layer.step_peers(qf, kf, vf, peer)
-    elif balanced:
-        def gstep():
-            layer.step(qf, kf, vf)
-    else:
-        # the timed steps replay a CUDA graph of selection + layer (PrefillPlan.graph)
-        graph = plan.graph(qd, kd, vd, out, ws)
-
-        def gstep():
-            graph.replay()
-            if world > 1:
-                gather_heads(out[0], world, out=final)
-
-    for _ in range(2):
-        gstep()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(torch.cuda.current_device())
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    with clocks:
-        t_start.record()
-        for s in range(args.steps):
+            if peer is not None:
+                layer.step_peers(qf, kf, vf, peer)
+            else:
+                layer.step(qf, kf, vf)
+        for _ in range(2):
             gstep()
-        t_end.record()
         torch.cuda.synchronize()
-    if world > 1:
         dist.barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(torch.cuda.current_device())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with clocks:
+            e0.record()
+            for _ in range(args.steps):
+                gstep()
+            e1.record()
+            torch.cuda.synchronize()
+        dist.barrier()
+        ms = e0.elapsed_time(e1) / args.steps
+    else:
+        graph = layer_graph(plan, qd, kd, vd, out, ws, flag, cache_k, cache_v)
+        if world > 1:
+            def gstep():
+                graph.replay()
+                gather_heads(out[0], world, out=final)
+        else:
+            gstep = graph.replay
+        for _ in range(2):
+            gstep()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(torch.cuda.current_device())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with clocks:
+            e0.record()
+            for _ in range(args.steps):
+                gstep()
+            e1.record()
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1) / args.steps
     torch.cuda.synchronize()
-    total_ms = t_start.elapsed_time(t_end)
-    ms = total_ms / args.steps
-    # per-stage breakdown (and the attention kernel time for the roofline) from
-    # eager steps with stage events, after the timed region
-    evsets = []
-    for _ in range(args.steps):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
-        for e in evs:
-            e.record()
-        evsets.append(evs)
-    torch.cuda.synchronize()
-    for s in range(args.steps):
-        step(evsets[s])
-    torch.cuda.synchronize()
-    stage = np.array([[evs[i].elapsed_time(evs[i + 1]) for i in range(6)] for evs in evsets])
-    stage_ms = stage.mean(axis=0)  # select, vs-est, block-est, tiles, attention, gather
+    if int(flag.item()):
+        raise SystemExit("bench.py: the synthetic inputs tripped the finiteness check")
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    # cache fill check: the cache holds the layer's k / v rows
+    if os.environ.get("SA_CHECK_MODE", "0") in ("0", "1"):
+        assert torch.equal(cache_k[:, :64], kd[:, :64]) and torch.equal(cache_v[:, -64:], vd[:, -64:])
+    plan.desc.check_flag = None
+    plan.desc.cache_k = plan.desc.cache_v = None
+    plan.desc.cache_capacity = 0
 
-    # executed-tile and realised FLOPs of this rank's attention launch
-    view = plan.views(ws)
-    nqt = view.nqt
-    cnt = R._wrap(view.tile_cnt, plan.hh * nqt, torch.int32).cpu().numpy()
-    exec_tiles = int(cnt.sum())
-    if balanced:  # this rank's attention launch covers its dealt items of every head
-        from paper_2412_06198_b200.multigpu import _view
-
-        cf = _view(layer.ws_full, layer.vf.tile_cnt, layer.items, torch.int32)
-        exec_tiles = int(cf[layer.mine.long()].sum().item())
-    exec_flops = exec_tiles * 4.0 * 128 ** 3
-    plans = plan.plans(ws, with_search=False)
-    fams = [type(hp.pattern).__name__ if hp.pattern is not None else "dense" for hp in plans[0]]
+    stage_ms = stage_breakdown(plan, qd, kd, vd, out, ws, args.steps)
     attn_ms = float(stage_ms[4])
     if balanced:  # the attention launch of this rank's dealt items, CUDA events on its stream
         ts = []
         for _ in range(args.steps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
             if peer is not None:
                 layer.attend_peers(qf, kf, vf, peer)
             else:
                 layer.attend(qf, kf, vf)
-            e1.record()
+            a1.record()
             torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1))
+            ts.append(a0.elapsed_time(a1))
         attn_ms = float(np.mean(ts))
-    peak, peak_sus, hbm, peak_kind = measured_peaks()
-    achieved = exec_flops / (attn_ms * 1e-3) / 1e12
-    if world > 1:
-        t = torch.tensor([exec_flops, attn_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    roof = attn_roofline(plan, ws, attn_ms, n)
+    if balanced:  # this rank's attention launch covers its dealt items of every head
+        from paper_2412_06198_b200.multigpu import _view
+
+        cf = _view(layer.ws_full, layer.vf.tile_cnt, layer.items, torch.int32)
+        roof["exec_tiles"] = int(cf[layer.mine.long()].sum().item())
+        roof["flops_per_launch"] = roof["exec_tiles"] * 4.0 * 128 ** 3
+        roof["achieved"] = round(roof["flops_per_launch"] / (attn_ms * 1e-3) / 1e12, 1)
+        roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    plans = plan.plans(ws, with_search=False)
+    fams = [type(hp.pattern).__name__ if hp.pattern is not None else "dense" for hp in plans[0]]
     # kernels per step, counted by CUPTI (torch.profiler) on one extra untimed step
     launches_per_step, kernel_names = count_step_kernels(gstep)
 
-    e2e = None
+    cfg = R.ModelConfig(n_heads=h_l, d_model=h_l * D, d_head=D, max_context=n)
+    e2e = e2e_np = None
     if not args.no_e2e:
-        # the public API on HOST tensors: prefill streams the layer through the GPU
-        # (H2D of q/k/v, kernels, D2H of the (1, n, H*d) output) and returns host outputs
-        cfg = R.ModelConfig(n_heads=h_l, d_model=h_l * D, d_head=D, max_context=n)
-        qh4, kh4, vh4 = q_h[None], k_h[None], v_h[None]
-        kw = {"fixed_pattern": fixed} if fixed is not None else {}
-        for _ in range(2):
-            res = R.prefill(qh4, kh4, vh4, cfg, mode=plan.mode, **kw)
-        assert not res.outputs.is_cuda
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
         reps = max(3, min(args.steps, 5))
-        walls = []
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            res = R.prefill(qh4, kh4, vh4, cfg, mode=plan.mode, **kw)
-            walls.append((time.perf_counter() - t0) * 1e3)
-        e2e_ms = statistics.median(walls)
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"value": round(e2e_ms, 3), "unit": "ms/layer",
-               "h2d_bytes_per_step": int(q_h.numel() * 2 + k_h.numel() * 2 + v_h.numel() * 2),
-               "d2h_bytes_per_step": int(res.outputs.numel() * 2), "reps": reps, "timer": "wall, median",
+        ems, bi, bo, reps = e2e_host(R, q_h[None], k_h[None], v_h[None], cfg, plan.mode, fixed, reps, world, dev)
+        e2e = {"value": round(ems, 3), "unit": "ms/layer", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+               "reps": reps, "timer": "wall, median",
                "path": "paper_2412_06198_b200.prefill(pinned host bf16 torch tensors) -> host outputs "
                        "(per-kv-group H2D / kernels / D2H streams overlapped)"}
+        if world == 1:
+            # the reference's own input type: numpy float32 (pageable), numpy float32 out
+            qn, kn, vn = (np.ascontiguousarray(x)[None] for x in (qs, ks, vs))
+            nms, bi2, bo2, r2 = e2e_host(R, qn, kn, vn, cfg, plan.mode, fixed, 3)
+            e2e_np = {"value": round(nms, 3), "unit": "ms/layer", "h2d_bytes_per_step": bi2,
+                      "d2h_bytes_per_step": bo2, "reps": r2, "timer": "wall, median",
+                      "path": "paper_2412_06198_b200.prefill(numpy float32 (1, H|HK, n, 128)) -> numpy float32 "
+                              "outputs (the reference's own call and types)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cms, sample = stratified_cpu_ms(q, k, v, n)
-        cpu = {"value": round(cms, 1), "unit": "ms/layer", "cores": cpu_cores(), "kind": "port", "sample": sample}
+        cms, sample, ckind = stratified_cpu_ms(q, k, v, n)
+        cpu = {"value": round(cms, 1), "unit": "ms/layer", "cores": cpu_cores(), "kind": ckind, "sample": sample}
+
+    # north-star sub-records (single GPU): the 128K layer and the all-VS estimator chain
+    sub128 = None
+    est = None
+    if world == 1 and n != 131072 and not args.no_128k:
+        del qd, kd, vd, out, cache_k, cache_v, q_h, k_h, v_h
+        torch.cuda.empty_cache()
+        sub128 = run_sub_layer(args, R, make_fixed, 131072, dev)
+    if world == 1 and not args.no_est:
+        est = [estimator_roofline(nn, dev) for nn in sorted({n, 131072})]
 
     if rank == 0:
-        traffic = None
-        tp = os.path.join(HERE, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            with open(tp) as f:
-                tj = json.load(f)
-            traffic = tj.get(f"attn_{n}_{plan.mode}")
         fam_counts = {f: fams.count(f) for f in sorted(set(fams))}
         line = {
             "metric": METRIC, "value": round(ms, 4), "unit": "ms/layer", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (uniform [-1,1], rng([seed, ctx]) GQA draw, bf16)",
-            "config": {"workload": f"llama3-8b-attn-layer-{n // 1024}k-{args.mode}", "heads": H, "kv_heads": HK,
-                       "head_dim": D, "seq_len": n, "batch": 1, "mode": args.mode,
-                       "parallelism": (f"balanced head-parallel x{world}: per-group estimation, index all-gather, "
-                                       f"heaviest-first (head, q-tile) deal, " +
-                                       ("output rows stored into every rank's IPC-mapped buffer by the attention "
-                                        "epilogue (fused all-gather)" if peer is not None else
-                                        "output-block all-gather")) if balanced else
-                                      (f"head-parallel x{world} + NCCL all-gather" if world > 1 else "single GPU"),
-                       "l2": l2_note(n),
-                       "launch": ("eager balanced steps (BalancedLayer.step); stage_ms from eager steps of this "
-                                  "rank's GQA-group plan with stage events") if balanced else
-                                 ("timed steps replay a CUDA graph of selection + layer (PrefillPlan.graph); "
-                                  "stage_ms from eager steps with stage events"),
-                       "families_rank0": fam_counts,
-                       "stage_note": "the VS and block estimator chains overlap on two streams: vs_estimator = "
-                                     "selection end -> VS chain end, block_estimator = the rest of the block chain"},
-            "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel", "achieved": round(achieved, 1),
-                         "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                         "frac_sustained": round(achieved / peak_sus, 4), "peak_kind": peak_kind,
-                         "traffic": traffic, "exec_tiles": exec_tiles, "attn_ms": round(attn_ms, 4),
-                         "flops_per_launch": exec_flops},
+            "config": common_config(args, world),
+            "details": {
+                "parallelism": (f"balanced head-parallel x{world}: per-group estimation, index all-gather, "
+                                f"heaviest-first (head, q-tile) deal, " +
+                                ("output rows stored into every rank's IPC-mapped buffer by the attention "
+                                 "epilogue (fused all-gather)" if peer is not None else "output-block all-gather"))
+                if balanced else (f"head-parallel x{world} + NCCL all-gather" if world > 1 else "single GPU"),
+                "l2": l2_note(n),
+                "step": ("eager balanced steps (BalancedLayer.step)" if balanced else
+                         "CUDA graph of selection + sa_prefill; the step includes AttnMatrices' finiteness scan of "
+                         "q/k/v (core.py:72-74) and the KvCache fill (runtime.py:197), both on a side stream beside "
+                         "the estimators"),
+                "families_rank0": fam_counts,
+                "stage_note": "stage_ms from eager steps with stage events; the VS and block estimator chains "
+                              "overlap on two streams: vs_estimator = selection end -> VS chain end, "
+                              "block_estimator = the rest of the block chain"},
+            "roofline": roof,
             "stage_ms": {k2: round(float(x), 4) for k2, x in zip(
                 ["select", "vs_estimator", "block_estimator", "tile_lists", "attention", "all_gather"], stage_ms)},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_numpy_f32": e2e_np,
             "gpu_launches": int(launches_per_step * args.steps),
             "kernels_per_step": kernel_names,
             "clocks": clocks.summary(),
+            "ctx_131072": sub128,
+            "estimator_roofline": est,
         }
         print(json.dumps(line), flush=True)
     if peer is not None:
@@ -533,8 +803,61 @@ def run_ours(args):
     return 0
 
 
+def run_sub_layer(args, R, make_fixed, n, dev):
+    """The north-star config on the same run: one 128K layer (BASELINE configs[2]
+    shape, auto mode unless --mode/--pattern), graph-timed like the headline,
+    with its stage breakdown, attention roofline and host e2e."""
+    import torch
+
+    mode, fixed = make_fixed(n)
+    q, k, v = synth_inputs(args.seed, n)
+    q_h = torch.from_numpy(q).bfloat16().pin_memory()
+    k_h = torch.from_numpy(k).bfloat16().pin_memory()
+    v_h = torch.from_numpy(v).bfloat16().pin_memory()
+    del q, k, v
+    qd, kd, vd = q_h.to(dev), k_h.to(dev), v_h.to(dev)
+    plan = R.PrefillPlan(1, H, HK, n, D, mode, fixed_pattern=fixed)
+    ws = R._workspace(plan.ws_bytes, dev)
+    out = torch.empty((1, n, H * D), dtype=torch.bfloat16, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    cache_k = torch.empty((HK, n, D), dtype=torch.bfloat16, device=dev)
+    cache_v = torch.empty((HK, n, D), dtype=torch.bfloat16, device=dev)
+    for _ in range(2):
+        if plan.mode == "auto":
+            plan.select(qd, kd, ws)
+        plan.run(qd, kd, vd, out, ws)
+    graph = layer_graph(plan, qd, kd, vd, out, ws, flag, cache_k, cache_v)
+    steps = max(3, min(args.steps, 5))
+    ms, sampler = time_graph(graph, steps, torch.cuda.current_device())
+    assert not int(flag.item())
+    plan.desc.check_flag = None
+    plan.desc.cache_k = plan.desc.cache_v = None
+    plan.desc.cache_capacity = 0
+    stage_ms = stage_breakdown(plan, qd, kd, vd, out, ws, 2)
+    roof = attn_roofline(plan, ws, float(stage_ms[4]), n)
+    plans = plan.plans(ws, with_search=False)
+    fams = [type(hp.pattern).__name__ if hp.pattern is not None else "dense" for hp in plans[0]]
+    del graph, qd, kd, vd, out, cache_k, cache_v
+    torch.cuda.empty_cache()
+    e2e = None
+    if not args.no_e2e:
+        cfg = R.ModelConfig(n_heads=H, d_model=H * D, d_head=D, max_context=n)
+        ems, bi, bo, reps = e2e_host(R, q_h[None], k_h[None], v_h[None], cfg, plan.mode, fixed, 3)
+        e2e = {"value": round(ems, 3), "unit": "ms/layer", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+               "reps": reps, "timer": "wall, median"}
+    return {"seq_len": n, "workload": f"llama3-8b-attn-layer-{n // 1024}k-{args.mode}", "value": round(ms, 4),
+            "unit": "ms/layer", "steps": steps, "families": {f: fams.count(f) for f in sorted(set(fams))},
+            "roofline": roof,
+            "stage_ms": {k2: round(float(x), 4) for k2, x in zip(
+                ["select", "vs_estimator", "block_estimator", "tile_lists", "attention"], stage_ms[:5])},
+            "e2e": e2e, "clocks": sampler.summary() if sampler else None, "l2": l2_note(n)}
+
+
 def main():
     args = parse()
+    rc = maybe_relaunch(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

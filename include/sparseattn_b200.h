@@ -96,6 +96,14 @@ typedef struct {
   int32_t stop_after_tiles; /* 1 = selection, estimators and tile lists only (no
                                attention): the realised index of these heads,
                                e.g. for exchange between ranks (multigpu.py) */
+  int32_t* check_flag;      /* optional device int: cleared, then set to 1 when q, k
+                               or v holds a NaN / Inf (AttnMatrices, core.py:72-74).
+                               The scan runs on a side stream beside the layer and
+                               is joined before sa_prefill's work completes; the
+                               caller reads the flag before using the outputs. */
+  void* cache_k;            /* optional bf16 KvCache storage [B, HK, cache_capacity, 128]: */
+  void* cache_v;            /* k / v rows 0..n-1 are copied in (runtime.py:197 cache.append) */
+  int32_t cache_capacity;   /* on the same side stream as the scan (0 = no cache fill)    */
 } sa_prefill_desc;
 
 /* Device views into a prefill workspace (valid after sa_prefill). */

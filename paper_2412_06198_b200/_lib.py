@@ -69,6 +69,10 @@ class sa_prefill_desc(ctypes.Structure):
         ("stage_events", ctypes.c_void_p * 6),
         ("out_ld", ctypes.c_int64),
         ("stop_after_tiles", ctypes.c_int32),
+        ("check_flag", ctypes.c_void_p),
+        ("cache_k", ctypes.c_void_p),
+        ("cache_v", ctypes.c_void_p),
+        ("cache_capacity", ctypes.c_int32),
     ]
 
 

@@ -70,6 +70,14 @@ struct TopkArgs {
 
 int launch_topk(const TopkArgs& a, cudaStream_t st);
 
+// util.cu: *flag |= any non-finite bf16 among count values at x (flag not cleared)
+int launch_check_finite(const void* x, long long count, int32_t* flag, cudaStream_t st);
+// util.cu: finiteness scan of q (nq values), k and v (nkv values each, rows of
+// `row` values) fused with the copy of k / v into cache rows of `cap` values
+// per head (cache_k / cache_v may be null); flag as above
+int launch_scan_fill(const void* q, long long nq, const void* k, const void* v, long long nkv, long long row,
+                     void* cache_k, void* cache_v, long long cap, int32_t* flag, cudaStream_t st);
+
 int launch_score_tail(int batch, int heads, int kv_heads, int n, float scale, const void* q,
                       const void* k, int r_lo, int r_hi, float* col_out, float* diag_out,
                       int accumulate, const int32_t* gate, int gate_val, void* ws, size_t ws_bytes,

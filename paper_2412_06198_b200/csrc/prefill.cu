@@ -34,8 +34,8 @@ static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 // Per-thread, per-device side stream and fork / join events (created on the
 // first call that needs them; the warm-up run before a graph capture does).
 struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork0 = nullptr, kdone = nullptr, fork = nullptr, join = nullptr;
+  cudaStream_t s = nullptr, s2 = nullptr;
+  cudaEvent_t fork0 = nullptr, kdone = nullptr, fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr;
 };
 static SideStream* side_stream() {
   static thread_local SideStream tab[16];
@@ -44,6 +44,9 @@ static SideStream* side_stream() {
   SideStream& x = tab[dev & 15];
   if (!x.s) {
     cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&x.s2, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&x.fork2, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.join2, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&x.fork0, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&x.kdone, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
@@ -286,6 +289,31 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   const int n = p.n;
   const int B = desc->batch, H = desc->heads, HK = desc->kv_heads;
 
+  // AttnMatrices' finiteness scan (core.py:72-74) of q, k, v: HBM-bound, on a
+  // second side stream beside the (compute-bound) selection and estimators,
+  // joined before this call's work completes
+  // The KvCache fill (runtime.py:197) rides on the same stream.
+  const bool fill = desc->cache_capacity > 0 && desc->cache_k && desc->cache_v;
+  if (fill && desc->cache_capacity < n)
+    return fail(SA_ERR_CACHE_OVERFLOW, "cache of capacity %d cannot hold %d rows", desc->cache_capacity, n);
+  static const int chk_mode = [] {
+    const char* e = getenv("SA_CHECK_MODE");  // A/B: 0 both, 1 no scan, 2 no fill, 3 neither
+    return e ? atoi(e) : 0;
+  }();
+  SideStream* chk = (desc->check_flag || fill) ? side_stream() : nullptr;
+  if (chk) {
+    cudaEventRecord(chk->fork2, st);
+    cudaStreamWaitEvent(chk->s2, chk->fork2, 0);
+    if (desc->check_flag) cudaMemsetAsync(desc->check_flag, 0, sizeof(int32_t), chk->s2);
+    const long long nq = (long long)p.hh * n * kHeadDim, nkv = (long long)p.hk * n * kHeadDim;
+    if ((rc = launch_scan_fill(q, (chk_mode & 1) ? 0 : nq, k, v, nkv, (long long)n * kHeadDim,
+                               (fill && !(chk_mode & 2)) ? desc->cache_k : nullptr,
+                               (fill && !(chk_mode & 2)) ? desc->cache_v : nullptr,
+                               (long long)std::max(desc->cache_capacity, 1) * kHeadDim, desc->check_flag,
+                               chk->s2)))
+      return rc;
+    cudaEventRecord(chk->join2, chk->s2);
+  }
   // The single Block-Cluster candidate's key pooling needs only K: it runs on
   // the side stream from the start, beside the selector.
   static const bool overlap = [] {
@@ -422,6 +450,7 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   // 4. executed tiles + attention
   if ((rc = sa_build_tiles(&V.index, p.hh, n, V.tile_off, V.tile_cnt, V.tiles, stream))) return rc;
   mark(3);
+  if (chk) cudaStreamWaitEvent(st, chk->join2, 0);
   if (desc->stop_after_tiles) return SA_OK;
   // longest-first CTA order over the non-empty items (SA_ATTN_ORDER=0 keeps
   // the kernel's kv-group-major default, for A/B)

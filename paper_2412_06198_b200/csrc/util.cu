@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "api_common.h"
 
@@ -16,8 +17,25 @@ __global__ void check_finite_kernel(const uint4* __restrict__ x, long long n16, 
                                     int ntail, int32_t* flag) {
   bool bad = false;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
-    const uint4 v = __ldg(x + i);
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // four independent 16-byte loads in flight per thread (a small grid still
+  // streams near HBM rate, leaving SMs to the kernels it runs beside)
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(x + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        bad |= (w[k] & 0x7f80u) == 0x7f80u;
+        bad |= (w[k] & 0x7f800000u) == 0x7f800000u;
+      }
+    }
+  }
+  for (; i < n16; i += stride) {
+    const uint4 v = __ldcs(x + i);
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -29,9 +47,71 @@ __global__ void check_finite_kernel(const uint4* __restrict__ x, long long n16, 
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1;
 }
 
+// AttnMatrices' finiteness scan of q, k, v fused with the KvCache fill
+// (runtime.py:197): one pass reads q, k and v once (16-byte streaming loads,
+// four in flight per thread) and writes k / v into the cache rows
+// [hk, 0..rows) of a cache with `cap` rows per head.  A grid-stride loop over
+// a small grid, so it streams beside the compute-bound estimator kernels.
+__device__ __forceinline__ bool bf16x8_bad(const uint4& v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) bad |= ((w[k] & 0x7f80u) == 0x7f80u) | ((w[k] & 0x7f800000u) == 0x7f800000u);
+  return bad;
+}
+__global__ void scan_fill_kernel(const uint4* __restrict__ q, long long nq16, const uint4* __restrict__ k,
+                                 const uint4* __restrict__ v, long long nkv16, long long row16, uint4* ck,
+                                 uint4* cv, long long cap16, int32_t* flag) {
+  bool bad = false;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // k / v: rows of (head, n * 8 uint4); cache rows of cap16 uint4 per head
+  for (long long i = t0; i < nkv16; i += stride) {
+    const uint4 a = __ldcs(k + i), b = __ldcs(v + i);
+    bad |= bf16x8_bad(a) | bf16x8_bad(b);
+    if (ck) {
+      const long long h = i / row16, r = i - h * row16, o = h * cap16 + r;
+      ck[o] = a;
+      cv[o] = b;
+    }
+  }
+  long long i = t0;
+  for (; i + 3 * stride < nq16; i += 4 * stride) {
+    uint4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = __ldcs(q + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bad |= bf16x8_bad(x[u]);
+  }
+  for (; i < nq16; i += stride) bad |= bf16x8_bad(__ldcs(q + i));
+  if (flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
+int launch_scan_fill(const void* q, long long nq, const void* k, const void* v, long long nkv, long long row,
+                     void* cache_k, void* cache_v, long long cap, int32_t* flag, cudaStream_t st) {
+  if ((nq | nkv | row | cap) % 8 != 0) return fail(SA_ERR_DIMENSION, "scan/fill needs 16-byte rows");
+  static const int cap_blocks = [] {
+    const char* e = getenv("SA_SCAN_BLOCKS");  // A/B: grid of the fused scan / cache fill
+    return e ? atoi(e) : 296;
+  }();
+  scan_fill_kernel<<<cap_blocks, 256, 0, st>>>(
+      reinterpret_cast<const uint4*>(q), nq / 8, reinterpret_cast<const uint4*>(k),
+      reinterpret_cast<const uint4*>(v), nkv / 8, row / 8, reinterpret_cast<uint4*>(cache_k),
+      reinterpret_cast<uint4*>(cache_v), cap / 8, flag);
+  return check_launch("scan_fill_kernel");
+}
+
 }  // namespace sa
 
+namespace sa {
+int launch_check_finite(const void* x, long long count, int32_t* flag, cudaStream_t st);
+}
+
 extern "C" int sa_check_finite_bf16(const void* x, long long count, int32_t* flag, void* stream) {
+  return sa::launch_check_finite(x, count, flag, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sa::launch_check_finite(const void* x, long long count, int32_t* flag, cudaStream_t st) {
   using namespace sa;
   if (count < 0 || !flag || (count > 0 && !x)) return fail(SA_ERR_DIMENSION, "bad finiteness-check arguments");
   if (count == 0) return SA_OK;
@@ -41,9 +121,13 @@ extern "C" int sa_check_finite_bf16(const void* x, long long count, int32_t* fla
   const int ntail = (int)(count % 8);
   const int threads = 256;
   long long blocks = (n16 + threads - 1) / threads;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  static const int cap = [] {
+    const char* e = getenv("SA_CHECK_BLOCKS");  // A/B: grid cap of the scan
+    return e ? atoi(e) : 148;
+  }();
+  if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  check_finite_kernel<<<(int)blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  check_finite_kernel<<<(int)blocks, threads, 0, st>>>(
       reinterpret_cast<const uint4*>(x), n16, reinterpret_cast<const uint16_t*>(x) + n16 * 8, ntail, flag);
   return check_launch("check_finite_kernel");
 }

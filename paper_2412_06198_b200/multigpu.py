@@ -161,6 +161,16 @@ class BalancedLayer:
         self.n_mine = torch.tensor([len(self.positions[rank])], dtype=torch.int32, device=dev)
         self.out = torch.zeros((self.nqt * 128, heads * d), dtype=torch.bfloat16, device=dev)
 
+    def enable_checks(self, flag: torch.Tensor, cache_k: torch.Tensor, cache_v: torch.Tensor) -> None:
+        """Run AttnMatrices' finiteness scan (core.py:72-74) of this rank's
+        q / k / v and the KvCache fill of its kv heads (runtime.py:197) inside
+        the estimation step (sa_prefill's side stream); `flag` is a device int,
+        cache_k / cache_v are (kv_heads / world, capacity, 128) bf16."""
+        d = self.local.desc
+        d.check_flag = flag.data_ptr()
+        d.cache_k, d.cache_v = cache_k.data_ptr(), cache_v.data_ptr()
+        d.cache_capacity = cache_k.shape[1]
+
     # -- index fields of `nh` heads starting at head `h0` of a plan's views
     def _fields(self, ws, view, h0: int, nh: int):
         idx = view.index

@@ -71,10 +71,17 @@ class KvCache:
     ``values()`` return numpy when the appended rows were numpy, else tensors."""
 
     def __init__(self, batch: int, n_heads: int, d_head: int, capacity: int, dtype=np.float32,
-                 kv_heads: int | None = None):
+                 kv_heads: int | None = None, _rows=None):
         dev = D.require_cuda()
         tdt = dtype if isinstance(dtype, torch.dtype) else torch.from_numpy(np.zeros(0, dtype)).dtype
         h = n_heads if kv_heads is None else kv_heads
+        if _rows is not None:  # full-capacity device rows held in place (see adopt)
+            self._k, self._v = _rows
+            if tuple(self._k.shape) != (batch, h, capacity, d_head) or self._k.dtype != tdt:
+                raise DimensionError("adopted cache rows do not match the cache shape")
+            self._np = not isinstance(dtype, torch.dtype)
+            self.length = capacity
+            return
         # rows past `length` are never read (keys()/values() slice), so no zero fill
         self._k = torch.empty((batch, h, capacity, d_head), dtype=tdt, device=dev)
         self._v = torch.empty((batch, h, capacity, d_head), dtype=tdt, device=dev)
@@ -303,14 +310,24 @@ class PrefillPlan:
         torch.cuda.current_stream().wait_stream(side)
         return g
 
-    def plans(self, ws: torch.Tensor, with_search: bool = True):
-        """Per (batch, head) HeadPlan list from the device choice (one small D2H)."""
+    def plans(self, ws: torch.Tensor, with_search: bool = True, flag: torch.Tensor | None = None):
+        """Per (batch, head) HeadPlan list from the device choice (one small D2H).
+        With `flag` (the device finiteness flag of desc.check_flag) the same
+        readback carries it and NonFiniteError is raised when it is set."""
         v = self.views(ws)
         hh = self.hh
+        parts = [] if flag is None else [flag.double()]
+        if self.mode == "auto":
+            parts += [_wrap(v.choice, hh, torch.int32).double(), _wrap(v.errors, hh * _lib.MAX_CAND, torch.float64)]
+        small = torch.cat(parts).cpu().numpy() if parts else None
+        if flag is not None:
+            if int(small[0]):
+                raise NonFiniteError("q, k or v contains NaN or Inf")
+            small = small[1:]
         if self.mode != "auto":
             return self.plans_from(None, None, self.batch, self.heads, with_search)
-        choice = _read_i32(v.choice, hh)
-        errs = _read_f64(v.errors, hh * _lib.MAX_CAND).reshape(hh, _lib.MAX_CAND)
+        choice = small[:hh].astype(np.int64)
+        errs = small[hh:].reshape(hh, _lib.MAX_CAND)
         return self.plans_from(choice, errs, self.batch, self.heads, with_search)
 
     def plans_from(self, choice, errs, batch: int, heads: int, with_search: bool = True):
@@ -427,34 +444,45 @@ def prefill(q, k, v, cfg: ModelConfig, search: SearchSpace | None = None, mode: 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     ev[0].record()
     qd, kd, vd = stage_layer(q, k, v)
-    for name, x in (("q", qd), ("k", kd), ("v", vd)):
-        if not bool(torch.isfinite(x).all().item()):
-            raise NonFiniteError(f"{name} contains NaN or Inf")
     plan = PrefillPlan(batch, cfg.n_heads, kv_heads, length, cfg.d_head, mode, search=search,
                        fixed_pattern=fixed_pattern, cal_window=cal_window, q_est=q_est)
     ws = _workspace(plan.ws_bytes, dev)
+    # AttnMatrices' finiteness scan (core.py:72-74) runs inside sa_prefill on a
+    # side stream; its flag comes back with the plans (one readback) and raises
+    # before any output is returned
+    flag = torch.empty(1, dtype=torch.int32, device=dev)
+    plan.desc.check_flag = flag.data_ptr()
+    cdt = k.dtype if D.is_torch(k) else np.asarray(k).dtype
+    cache = KvCache(batch, cfg.n_heads, cfg.d_head, cfg.max_context, dtype=cdt, kv_heads=kv_heads)
+    dev_fill = D.is_torch(k) and k.dtype == torch.bfloat16 and cfg.d_head == D.HEAD_DIM
+    if dev_fill:  # cache.append (runtime.py:197) inside sa_prefill, beside the estimators
+        plan.desc.cache_k, plan.desc.cache_v = cache._k.data_ptr(), cache._v.data_ptr()
+        plan.desc.cache_capacity = cfg.max_context
     out = torch.empty((batch, length, cfg.n_heads * D.HEAD_DIM), dtype=torch.bfloat16, device=dev)
     ev[1].record()
     if mode == "auto":
         plan.select(qd, kd, ws)
     ev[2].record()
     plan.run(qd, kd, vd, out, ws)
+    plan.desc.check_flag = None
+    plan.desc.cache_k = plan.desc.cache_v = None
+    plan.desc.cache_capacity = 0
+    try:
+        plans = plan.plans(ws, flag=flag)
+    except NonFiniteError:
+        names = [nm for nm, x in (("q", qd), ("k", kd), ("v", vd)) if not bool(torch.isfinite(x).all())]
+        raise NonFiniteError(f"{names[0] if names else 'input'} contains NaN or Inf") from None
     y = out
     if cfg.d_head < D.HEAD_DIM:
         y = out.view(batch, length, cfg.n_heads, D.HEAD_DIM)[..., : cfg.d_head].reshape(batch, length, cfg.d_model)
     outputs = D.to_host_or_keep(y, q)
-    cache = KvCache(batch, cfg.n_heads, cfg.d_head, cfg.max_context,
-                    dtype=(k.dtype if D.is_torch(k) else np.asarray(k).dtype), kv_heads=kv_heads)
-    if D.is_torch(k) and k.dtype == torch.bfloat16:
-        # fill from the staged device copies (no second host->device transfer)
-        cache.append(kd.view(batch, kv_heads, length, D.HEAD_DIM)[..., : cfg.d_head],
-                     vd.view(batch, kv_heads, length, D.HEAD_DIM)[..., : cfg.d_head])
+    if dev_fill:
+        cache.length = length
     else:  # the reference caches the rows as given (runtime.py:197), not their bf16 rounding
         cache.append(k, v)
     cache._np = not D.is_torch(k)
     ev_end = torch.cuda.Event(enable_timing=True)
     ev_end.record()
-    plans = plan.plans(ws)
     torch.cuda.synchronize()
     elapsed = time.perf_counter() - t0
     select_s = ev[1].elapsed_time(ev[2]) / 1e3
