@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-128k", action="store_true", help="skip the 131072-token sub-record")
     ap.add_argument("--no-est", action="store_true", help="skip the all-VS estimator roofline block")
+    ap.add_argument("--no-ttft", action="store_true", help="skip the 32-layer 64K TTFT sub-record")
+    ap.add_argument("--ttft-layers", type=int, default=32)
+    ap.add_argument("--ttft-ctx", type=int, default=65536)
     return ap.parse_args()
 
 
@@ -759,6 +762,9 @@ def run_ours(args):
         sub128 = run_sub_layer(args, R, make_fixed, 131072, dev)
     if world == 1 and not args.no_est:
         est = [estimator_roofline(nn, dev) for nn in sorted({n, 131072})]
+    ttft = None
+    if not args.no_ttft:
+        ttft = run_ttft(args, world, rank, dev)
 
     if rank == 0:
         fam_counts = {f: fams.count(f) for f in sorted(set(fams))}
@@ -794,6 +800,7 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "ctx_131072": sub128,
             "estimator_roofline": est,
+            "ttft_c4": ttft,
         }
         print(json.dumps(line), flush=True)
     if peer is not None:
@@ -801,6 +808,70 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_ttft(args, world, rank, dev):
+    """BASELINE configs[3]: a 32-layer Llama-3-8B-shape sparse prefill at 64K
+    (attention path only, like runtime.py:1-10), head-parallel over the ranks:
+    layers.LayerStack runs every layer's selection, estimators, attention,
+    finiteness scan and KvCache fill back to back (one CUDA graph on one GPU;
+    with N > 1 each layer's output all-gather overlaps the next layer).  TTFT =
+    device time of the stack, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_06198_b200.layers import LayerStack
+    from paper_2412_06198_b200.runtime import ModelConfig
+
+    L, n = args.ttft_layers, args.ttft_ctx
+    cfg = ModelConfig(n_heads=H, d_model=H * D, d_head=D, max_context=n)
+    h_l, hk_l = H // world, HK // world
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 * args.seed + rank)
+
+    def draw(heads):
+        return (torch.rand((1, heads, n, D), generator=g, device=dev) * 2 - 1).bfloat16()
+
+    qs = [draw(h_l) for _ in range(L)]
+    ks = [draw(hk_l) for _ in range(L)]
+    vs = [draw(hk_l) for _ in range(L)]
+    stack = LayerStack(L, cfg, HK, n, mode="auto", world=world, device=dev)
+    if world == 1:
+        graph = stack.graph(qs, ks, vs)
+        step = graph.replay
+    else:
+        def step():
+            stack.run(qs, ks, vs)
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    reps = 3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    plans = stack.finish()
+    fams = {}
+    for p in plans:
+        for hp in p[0]:
+            f = type(hp.pattern).__name__
+            fams[f] = fams.get(f, 0) + 1
+    del stack, qs, ks, vs
+    torch.cuda.empty_cache()
+    return {"layers": L, "seq_len": n, "ttft_ms": round(ms, 2), "ms_per_layer": round(ms / L, 4), "reps": reps,
+            "n_gpus": world, "families_rank0_all_layers": fams,
+            "data": "synthetic uniform [-1,1] per layer (device RNG), bf16",
+            "step": ("one CUDA graph of the 32-layer stack" if world == 1 else
+                     "eager layers; layer l's NCCL output all-gather overlaps layer l+1") +
+                    "; every layer includes the finiteness scan and its KvCache fill"}
 
 
 def run_sub_layer(args, R, make_fixed, n, dev):

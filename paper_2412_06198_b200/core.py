@@ -106,9 +106,6 @@ def dense_attention(m: AttnMatrices, *, need_weights: bool = True):
     """Causal (or full) softmax(q k^T / sqrt(d)) v on the B200 kernel (core.py:138-154)."""
     from .patterns import SparseIndex, _run_index
 
-    if not m.causal:
-        # the tile kernels are causal; a non-causal head is outside the hot path
-        raise DimensionError("non-causal dense attention is not supported by the B200 kernels")
     w, y = _run_index(m, SparseIndex(n=m.n), dense=True, need_weights=need_weights)
     return (w if need_weights else None), y
 

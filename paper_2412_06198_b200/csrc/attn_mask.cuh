@@ -81,6 +81,8 @@ __device__ __forceinline__ void mask_make(const Args& a, const RowConst& c, int 
       const int s = gq - qt * (kTile / c.b);
       mask_set_range(m, s * c.b, s * c.b + c.b);
     }
+  } else if (kind == TK_LIMIT) {
+    mask_set_range(m, 0, a.n - j0);
   } else if (kind == TK_BLOCKDIAG) {
     mask_set_range(m, (i / c.b) * c.b - j0, diag_c + 1);
   } else if (kind == TK_BAND) {

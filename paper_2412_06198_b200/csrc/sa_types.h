@@ -10,7 +10,8 @@ namespace sa {
 // Pattern families, in the reference's DEFAULT_FAMILIES order
 // (search.py:322): the selector's argmin index is the family id.
 enum Family : int32_t { FAM_TRI = 0, FAM_VS = 1, FAM_BLOCK = 2, FAM_DENSE = 3,
-                        FAM_VS_NOEYE = 5 /* VS index with always_diagonal=False */ };
+                        FAM_VS_NOEYE = 5 /* VS index with always_diagonal=False */,
+                        FAM_DENSE_NC = 6 /* non-causal dense (core.py:138-154, causal=False) */ };
 
 // Per-tile mask kinds (bits 28..31 of a tile-list entry).
 enum TileKind : uint32_t {
@@ -23,6 +24,7 @@ enum TileKind : uint32_t {
   // blocks each contribute one b-key slot to a gathered 128-key tile.
   TK_GATHER = 5,     // ktile field = rank g: slot s holds the g-th off-diagonal block of query block s
   TK_BLOCKDIAG = 6,  // kt == qt: only the row's own (diagonal) block, j <= i
+  TK_LIMIT = 7,      // non-causal dense, last key tile: every key j < n
 };
 
 // Gather mode applies to block sides whose blocks are whole 8-row swizzle atoms

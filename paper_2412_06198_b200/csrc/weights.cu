@@ -18,8 +18,9 @@
 namespace sa {
 
 __device__ __forceinline__ bool index_allows(const sa_head_index& ix, int hh, int n, int i, int j) {
-  if (j > i) return false;
   const int fam = ix.family[hh];
+  if (fam == FAM_DENSE_NC) return true;
+  if (j > i) return false;
   if (fam == FAM_DENSE) return true;
   if (fam == FAM_TRI) return (i - j < ix.tri_window[hh]) || (j < ix.tri_sinks[hh]) || i == j;
   if (fam == FAM_VS || fam == FAM_VS_NOEYE) {

@@ -21,7 +21,8 @@ import torch
 
 from . import _lib
 
-FAM_TRI, FAM_VS, FAM_BLOCK, FAM_DENSE, FAM_VS_NOEYE = 0, 1, 2, 3, 5
+FAM_TRI, FAM_VS, FAM_BLOCK, FAM_DENSE, FAM_VS_NOEYE, FAM_DENSE_NC = 0, 1, 2, 3, 5, 6
+TK_FULL, TK_LIMIT = 0, 7  # tile kinds (sa_types.h)
 HEAD_DIM = 128
 
 
@@ -73,8 +74,8 @@ class HostIndexBuilder:
         self.blk_b = np.ones(hh, np.int32)
         self._blk_rows: dict[int, list[np.ndarray]] = {}
 
-    def set_dense(self, h: int) -> None:
-        self.family[h] = FAM_DENSE
+    def set_dense(self, h: int, causal: bool = True) -> None:
+        self.family[h] = FAM_DENSE if causal else FAM_DENSE_NC
 
     def set_triangular(self, h: int, window: int, sinks: int) -> None:
         self.family[h] = FAM_TRI
@@ -141,6 +142,19 @@ def num_qtiles(n: int) -> int:
 def tile_capacity(n: int, hh: int) -> int:
     t = num_qtiles(n)
     return hh * t * (t + 1) // 2
+
+
+def noncausal_dense_tiles(n: int, hh: int, dev):
+    """Tile lists of non-causal dense heads (core.py:138-154 with causal=False):
+    every query tile lists every key tile, the last one limited to keys < n."""
+    nqt = num_qtiles(n)
+    row = np.full(nqt, TK_FULL << 28, np.int64) | np.arange(nqt)
+    if n % 128:
+        row[-1] = (TK_LIMIT << 28) | (nqt - 1)
+    tiles = np.tile(row, hh * nqt).astype(np.uint32).view(np.int32)
+    off = (np.arange(hh * nqt, dtype=np.int64) * nqt).astype(np.int32)
+    cnt = np.full(hh * nqt, nqt, np.int32)
+    return tuple(torch.from_numpy(x).to(dev) for x in (off, cnt, tiles))
 
 
 def build_tiles(index: DeviceIndex, stream=None):

@@ -36,10 +36,11 @@ def gather_heads(local: torch.Tensor, world: int, group=None, out: torch.Tensor 
         buf = torch.empty((world, n, w), dtype=local.dtype, device=local.device)
         dist.all_gather_into_tensor(buf, local.contiguous(), group=group)
         out.view(n, world, w).copy_(buf.permute(1, 0, 2))
-    else:  # gloo (CPU tests)
-        parts = [torch.empty_like(local) for _ in range(world)]
-        dist.all_gather(parts, local.contiguous(), group=group)
-        out.view(n, world, w).copy_(torch.stack(parts, 1))
+    else:  # gloo (CPU tests; CUDA tensors hop through the host)
+        src = local.contiguous().cpu()
+        parts = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(parts, src, group=group)
+        out.view(n, world, w).copy_(torch.stack(parts, 1).to(out.device))
     return out
 
 

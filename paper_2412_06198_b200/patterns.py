@@ -180,12 +180,16 @@ def _check_nonempty(idx: SparseIndex) -> None:
 
 
 def _run_index(m: AttnMatrices, idx: SparseIndex, *, dense: bool = False, need_weights: bool = False):
-    """Attention of one head under `idx` on the tcgen05 kernel -> (weights|None, y)."""
+    """Attention of one head under `idx` on the tcgen05 kernel -> (weights|None, y).
+    dense with m.causal False: every key of every row (core.py:150)."""
     n = m.n
     q, k, v = m.staged()
+    noncausal = dense and not m.causal
     builder = _index_builder(idx, n, dense=dense)
+    if noncausal:
+        builder.set_dense(0, causal=False)
     dix = builder.upload(q.device)
-    off, cnt, tiles = DI.build_tiles(dix)
+    off, cnt, tiles = DI.noncausal_dense_tiles(n, 1, q.device) if noncausal else DI.build_tiles(dix)
     out = torch.empty((n, DI.HEAD_DIM), dtype=torch.bfloat16, device=q.device)
     lse = torch.empty((1, n), dtype=torch.float32, device=q.device) if need_weights else None
     view = dix.view()

@@ -585,3 +585,36 @@ def test_prefill_many_candidates(sa):
         assert (type(hp.pattern).__name__[0], *hp.pattern.__dict__.values()) == \
             (type(want).__name__[0], *want.__dict__.values()), h
         assert abs(hp.search.error - err) <= 1e-4 * max(1.0, err)
+
+
+# ---- non-causal dense attention (core.py:138-154; test_core.py:55-61) ------------
+
+def _naive_attention(q, k, v, causal):
+    """float64 three-loop restatement (reference tests/oracles.py:12-30)."""
+    n, d = q.shape
+    s = (q.astype(np.float64) @ k.astype(np.float64).T) / np.sqrt(d)
+    if causal:
+        s = np.where(np.tri(n, dtype=bool), s, -np.inf)
+    w = np.exp(s - s.max(axis=1, keepdims=True))
+    w /= w.sum(axis=1, keepdims=True)
+    return w, w @ v.astype(np.float64)
+
+
+@pytest.mark.parametrize("n,d", [(5, 3), (128, 128), (300, 64), (1000, 128)])
+def test_dense_non_causal(sa, n, d):
+    m, (q, k, v) = mats(sa, 70 + n, n, d)
+    m = sa.AttnMatrices(m.q, m.k, m.v, causal=False)
+    w, y = sa.dense_attention(m)
+    ow, oy = _naive_attention(q, k, v, causal=False)
+    close(y, oy)
+    np.testing.assert_allclose(w, ow, atol=2e-3)
+    np.testing.assert_allclose(np.asarray(w).sum(axis=1), 1.0, atol=1e-5)
+    assert (np.asarray(w)[np.triu_indices(n, 1)] > 0).all()  # keys after the row do count
+
+
+def test_sparse_rejects_non_causal(sa):
+    """test_patterns.py:168-172: the sparse kernels stay causal-only."""
+    m, _ = mats(sa, 18, 4, 2)
+    m = sa.AttnMatrices(m.q, m.k, m.v, causal=False)
+    with pytest.raises(sa.PatternParamError):
+        sa.vertical_slash_attention(m, sa.SparseIndex(n=4))

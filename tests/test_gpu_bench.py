@@ -25,7 +25,7 @@ def _run(args, env=None, timeout=600):
 def test_bench_self_launches_ranks():
     """`bench.py --gpus 2` without torchrun spawns two ranks itself (here both
     on the one GPU over gloo) and reports n_gpus = 2."""
-    line, err = _run(["--gpus", "2", "--ctx", "4096", "--steps", "2", "--warmup", "3", "--no-e2e",
+    line, err = _run(["--gpus", "2", "--ctx", "4096", "--steps", "2", "--warmup", "3", "--no-e2e", "--ttft-layers", "2", "--ttft-ctx", "2048",
                       "--no-cpu-baseline", "--no-128k", "--no-est"], env={"SA_DIST_BACKEND": "gloo"})
     assert line["n_gpus"] == 2 and line["config"]["n_gpus"] == 2
     assert "rank 1/2" in err and "rank 0/2" in err
@@ -43,7 +43,7 @@ def test_bench_line_fields_small():
     """One small run: the step includes the finiteness scan and the cache fill,
     the line carries the roofline / e2e / clocks keys and the same config keys
     as the reference arm."""
-    line, _ = _run(["--ctx", "4096", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-128k"])
+    line, _ = _run(["--ctx", "4096", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-128k", "--ttft-layers", "3", "--ttft-ctx", "4096"])
     for key in ("roofline", "e2e", "e2e_numpy_f32", "clocks", "gpu_launches", "estimator_roofline"):
         assert line.get(key) is not None, key
     ref, _ = _run(["--impl", "reference", "--ctx", "1024", "--steps", "2", "--warmup", "1"])
