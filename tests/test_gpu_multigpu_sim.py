@@ -75,7 +75,7 @@ def test_bench_two_ranks_share_one_gpu(exchange):
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2
-    assert lines[0]["config"]["parallelism"].startswith("balanced head-parallel x2")
+    assert lines[0]["details"]["parallelism"].startswith("balanced head-parallel x2")
     assert ("fused all-gather" in lines[0]["config"]["parallelism"]) == (exchange == "peer")
 
 
