@@ -70,13 +70,13 @@ def test_bench_two_ranks_share_one_gpu(exchange):
     env = dict(os.environ, SA_DIST_BACKEND="gloo", SA_MG_EXCHANGE=exchange)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--ctx", "8192", "--steps", "3",
-           "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
+           "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-ttft"]
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2
     assert lines[0]["details"]["parallelism"].startswith("balanced head-parallel x2")
-    assert ("fused all-gather" in lines[0]["config"]["parallelism"]) == (exchange == "peer")
+    assert ("fused all-gather" in lines[0]["details"]["parallelism"]) == (exchange == "peer")
 
 
 @pytest.mark.parametrize("world,n,mode", [(2, 4096, "auto"), (4, 2500, "fixed")])
