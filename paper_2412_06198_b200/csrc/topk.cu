@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "api_common.h"
 #include "internal.h"
@@ -532,12 +533,20 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
         if (key >= lo && (uint64_t)(key - lo) < span) atomicAdd(&hist[key_bin(key, bm)], 1);
       }
       cl.sync();
-      if (cr == 0) {
-        for (int q = 1; q < kClusterC; ++q) {
-          const int* rh = cl.map_shared_rank(hist, q);
-          for (int t = tid; t < kBins; t += blockDim.x) hist[t] += rh[t];
+      {
+        // distributed merge: CTA cr sums bin slice cr of every CTA's histogram
+        // into the leader's copy of that slice (the only reader / writer of it)
+        constexpr int kSlice = kBins / kClusterC;
+        int* lh = cl.map_shared_rank(hist, 0);
+        for (int t = cr * kSlice + tid; t < (cr + 1) * kSlice; t += blockDim.x) {
+          int acc = 0;
+#pragma unroll
+          for (int q = 0; q < kClusterC; ++q) acc += cl.map_shared_rank(hist, q)[t];
+          lh[t] = acc;
         }
-        __syncthreads();
+      }
+      cl.sync();
+      if (cr == 0) {
         const int pb = kBins / blockDim.x;
         const int b_hi = kBins - tid * pb;
         int mine = 0;
@@ -583,13 +592,18 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
         }
       }
       cl.sync();
-      // 4. exact ranks in the leader
-      if (cr == 0) {
-        for (int c = tid; c < m; c += blockDim.x) {
+      // 4. exact ranks: every CTA copies the leader's candidates and ranks
+      // its share of them; the one of rank want - 1 goes to the leader
+      {
+        const uint64_t* rc = cl.map_shared_rank(cand, 0);
+        if (cr != 0)
+          for (int c = tid; c < m; c += blockDim.x) cand[c] = rc[c];
+        __syncthreads();
+        for (int c = cr * blockDim.x + tid; c < m; c += kClusterC * blockDim.x) {
           const uint64_t me = cand[c];
           int rank = 0;
           for (int o = 0; o < m; ++o) rank += cand[o] > me;
-          if (rank == want - 1) sh_T = me;
+          if (rank == want - 1) *cl.map_shared_rank(&sh_T, 0) = me;
         }
       }
       cl.sync();
@@ -663,7 +677,12 @@ int launch_topk(const TopkArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kTopkSmem + ((262144 / kClusterC) + 4) * 4);
   });
-  if (a.lens == nullptr && a.ks == nullptr && a.n >= kClusterMin && a.n <= 262144 && threads == kTopkThreads) {
+  static const int use_cluster = [] {
+    const char* e = getenv("SA_TOPK_CLUSTER");  // A/B: cluster-of-8 kernel for long rows
+    return e ? atoi(e) : 1;
+  }();
+  if (use_cluster && a.lens == nullptr && a.ks == nullptr && a.n >= kClusterMin && a.n <= 262144 &&
+      threads == kTopkThreads) {
     topk_cluster_kernel<<<rows * kClusterC, kTopkThreads, kTopkSmem + cl_per * 4, st>>>(a);
     return check_launch("topk_cluster_kernel");
   }
