@@ -64,6 +64,7 @@ struct AttnArgs {
   int* counter;              // optional work-item counter (zeroed before launch): dynamic fetch
   const int32_t* n_work;     // optional device count of `work` entries (default hh_total * nqt)
   int st256;                 // output rows 32-byte aligned: 256-bit stores
+  int skip_dead;             // warps whose 32 rows are all masked out of a sub-tile write P = 0 only
   int n_peers;               // > 0: every output row is also stored into these buffers (same layout),
   __nv_bfloat16* peer_out[kMaxPeers];  // other ranks' outputs mapped over NVLink (fused all-gather)
 };
@@ -239,9 +240,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         if (g >= kRing) mbar_wait_backoff<kProducerSleepNs>(&bars[B_EMPTY0 + slot], ((g / kRing) - 1) & 1);
         PT(1);
         uint8_t* dst = sRing + slot * kSlotBytes;
-        if (kind != TK_GATHER) {
+        // b = 64: a gathered sub-tile is one whole key block, loaded like a contiguous one
+        const int gk64 = (kind == TK_GATHER && bsz == kSub) ? __shfl_sync(0xffffffffu, slot_gk, u & 1) : -1;
+        if (kind != TK_GATHER || gk64 >= 0) {
           if (lane == 0) {
-            const int row = (int)tile_ktile(e) * kTile + (u & 1) * kSub;
+            const int row = gk64 >= 0 ? gk64 * kSub : (int)tile_ktile(e) * kTile + (u & 1) * kSub;
             const CUtensorMap* map = (i & 1) ? &a.tmap_v : &a.tmap_k;
             sLay[slot] = 0;
             mbar_arrive_expect_tx(&bars[B_FULL0 + slot], kSlotBytes);
@@ -401,8 +404,23 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
         mbar_wait(&bars[B_SF0 + half], (sb + (u >> 1)) & 1);
         PT(2);
         tc_fence_after();
-        uint32_t s[2][32];
         const uint32_t s_col = tbase + lane_off + kColS + half * kSub;
+        // Gathered / block-diagonal / causal-diagonal tiles leave half the rows
+        // of a sub-tile with no visible key: such a warp skips the softmax and
+        // only zeroes its P rows (the PV MMA still reads all 128), keeping m, l, O.
+        if (kind != TK_FULL && a.skip_dead &&
+            __all_sync(0xffffffffu, ((half ? msk[2] : msk[0]) | (half ? msk[3] : msk[1])) == 0u)) {
+          uint32_t z[32];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) z[t] = 0u;
+          tmem_st32(s_col, z);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&bars[B_PF0 + half]);
+          PT(7);
+          continue;
+        }
+        uint32_t s[2][32];
         tmem_ld32(s_col, s[0]);
         tmem_ld32(s_col + 32, s[1]);
         tmem_ld_wait();
@@ -593,6 +611,11 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   if (a.out_row_stride % 8 != 0 || (reinterpret_cast<uintptr_t>(out) & 15) != 0)
     return fail(SA_ERR_DIMENSION, "output rows must be 16-byte aligned (out_ld %% 8 == 0)");
   a.st256 = (a.out_row_stride % 16 == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0) ? 1 : 0;
+  static const int skip_dead = [] {
+    const char* e = getenv("SA_ATTN_SKIP");  // A/B: 0 = every warp runs the softmax of every sub-tile
+    return e ? atoi(e) : 1;
+  }();
+  a.skip_dead = skip_dead;
   if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && !peer_out))
     return fail(SA_ERR_DIMENSION, "n_peers must be in [0, %d]", kMaxPeers);
   a.n_peers = n_peers;
