@@ -246,7 +246,7 @@ int sa_attn_sparse_work(int batch, int heads, int kv_heads, int n, float scale, 
  * stored, from the epilogue, at the same offset into each of the `n_peers`
  * (<= 7) buffers in `peer_out` — other ranks' output buffers mapped with
  * sa_ipc_open — so no separate all-gather follows.  The caller orders the
- * peers' reads after this kernel (stream sync + a host barrier). */
+ * peers' reads after this kernel with sa_peer_barrier on the same stream. */
 int sa_attn_sparse_work_peers(int batch, int heads, int kv_heads, int n, float scale, const void* q,
                               const void* k, const void* v, void* out, void* const* peer_out, int n_peers,
                               const sa_head_index* index, const int32_t* tile_off, const int32_t* tile_cnt,
@@ -262,6 +262,20 @@ int sa_ipc_alloc(size_t bytes, void** ptr, void* handle);
 int sa_ipc_free(void* ptr);
 int sa_ipc_open(const void* handle, void** ptr);
 int sa_ipc_close(void* ptr);
+
+/* Device-side barrier of `world` ranks over IPC-mapped flag buffers (no host
+ * synchronisation; capturable in a CUDA graph).  `flags` is this rank's
+ * buffer of world + 1 zero-initialised int32 (slot r = rank r's last epoch,
+ * slot world = this rank's epoch counter); `peer_flags` are the other
+ * world - 1 ranks' buffers mapped with sa_ipc_open.  One thread bumps the
+ * epoch, fences (system scope: every earlier write on the stream, including
+ * sa_attn_sparse_work_peers' stores into peer outputs, is visible before the
+ * flag), writes the epoch into slot `rank` of every peer with a system-scope
+ * release and waits (acquire) until every other rank's slot of `flags` holds
+ * it.  Work queued after it on `stream` sees every rank's writes issued
+ * before their barrier.  A rank that does not arrive within `timeout_ms`
+ * traps the kernel (a CUDA error, not a hang). */
+int sa_peer_barrier(int32_t* flags, void* const* peer_flags, int rank, int world, int timeout_ms, void* stream);
 
 #ifdef __cplusplus
 }

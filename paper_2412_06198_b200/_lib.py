@@ -132,6 +132,7 @@ _SIGNATURES = {
     "sa_ipc_free": (ctypes.c_int, [_P]),
     "sa_ipc_open": (ctypes.c_int, [_P, _P]),
     "sa_ipc_close": (ctypes.c_int, [_P]),
+    "sa_peer_barrier": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
     "sa_decode_workspace": (_SZ, [_I, _I, _I, _I, _I]),
     "sa_decode_attn": (ctypes.c_int, [_I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _I, _P, _P, _SZ, _P]),
     "sa_order_work": (ctypes.c_int, [_P, _I, _I, _P, _P]),

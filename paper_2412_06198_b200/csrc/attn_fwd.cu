@@ -564,6 +564,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     }
     if (kProf) pc[11] += clock64() - t_entry;
     PT_FLUSH(0);
+    if (a.n_peers > 0) __threadfence_system();  // peer stores drained before the CTA retires
   }
   tc_fence_before();
   __syncthreads();

@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "api_common.h"
 
@@ -139,4 +140,54 @@ extern "C" int sa_memcpy2d_async(void* dst, size_t dpitch, const void* src, size
                                           reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(SA_ERR_CUDA, "cudaMemcpy2DAsync: %s", cudaGetErrorString(e));
   return SA_OK;
+}
+
+// ------------------------------------------------------------ peer barrier
+namespace sa {
+
+struct PeerFlags {
+  int32_t* peer[8];
+};
+
+__global__ void peer_barrier_kernel(int32_t* flags, PeerFlags pf, int rank, int world, long long timeout_ns) {
+  if (threadIdx.x != 0) return;
+  const int e = flags[world] + 1;
+  flags[world] = e;
+  // earlier work on this stream (the epilogue's peer stores) before the flags
+  asm volatile("fence.sc.sys;" ::: "memory");
+  for (int p = 0; p < world - 1; ++p)
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(pf.peer[p] + rank), "r"(e) : "memory");
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) continue;
+    for (;;) {
+      int v;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
+      if (v - e >= 0) break;
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if ((long long)(t - t0) > timeout_ns) __trap();
+      __nanosleep(200);
+    }
+  }
+}
+
+}  // namespace sa
+
+extern "C" int sa_peer_barrier(int32_t* flags, void* const* peer_flags, int rank, int world, int timeout_ms,
+                               void* stream) {
+  using namespace sa;
+  if (world < 1 || world > 8 || rank < 0 || rank >= world || !flags || (world > 1 && !peer_flags) ||
+      timeout_ms < 1)
+    return fail(SA_ERR_DIMENSION, "sa_peer_barrier: bad arguments (world must be in [1, 8])");
+  PeerFlags pf;
+  memset(&pf, 0, sizeof(pf));
+  for (int p = 0; p < world - 1; ++p) {
+    pf.peer[p] = reinterpret_cast<int32_t*>(peer_flags[p]);
+    if (!pf.peer[p]) return fail(SA_ERR_DIMENSION, "sa_peer_barrier: null peer flag buffer");
+  }
+  peer_barrier_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flags, pf, rank, world,
+                                                                           (long long)timeout_ms * 1000000ll);
+  return check_launch("peer_barrier_kernel");
 }

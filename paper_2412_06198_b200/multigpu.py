@@ -82,6 +82,30 @@ class PeerOutputs:
                 self.peer_ptrs.append(p.value)
         self.peers = (ctypes.c_void_p * max(1, len(self.peer_ptrs)))(*self.peer_ptrs)
         self.local = torch.as_tensor(_DeviceArray(self._ptr, (rows, cols)), device="cuda").view(torch.bfloat16)
+        # barrier flags: [world] last epoch written by each rank + this rank's epoch counter
+        fptr = ctypes.c_void_p()
+        fh = (ctypes.c_uint8 * 64)()
+        _lib.check(lib.sa_ipc_alloc(4 * (world + 1), ctypes.byref(fptr), fh))
+        self._fptr = fptr.value
+        torch.as_tensor(_DeviceArray(self._fptr, (2 * (world + 1),)), device="cuda").zero_()
+        torch.cuda.synchronize()
+        fhandles = [None] * world
+        dist.all_gather_object(fhandles, bytes(fh), group=group)  # every rank's flags zeroed before any use
+        self.peer_flag_ptrs = []
+        for r in range(world):
+            if r != rank:
+                p = ctypes.c_void_p()
+                _lib.check(lib.sa_ipc_open(ctypes.c_char_p(fhandles[r]), ctypes.byref(p)))
+                self.peer_flag_ptrs.append(p.value)
+        self.peer_flags = (ctypes.c_void_p * max(1, len(self.peer_flag_ptrs)))(*self.peer_flag_ptrs)
+
+    def barrier(self, timeout_ms: int = 60000) -> None:
+        """Device-side barrier of the ranks on the current stream (sa_peer_barrier):
+        later work on the stream sees every rank's peer stores issued before it."""
+        from . import _lib
+        from . import _device as Dv
+
+        _lib.call("sa_peer_barrier", self._fptr, self.peer_flags, self.rank, self.world, timeout_ms, Dv.stream())
 
     def close(self) -> None:
         """Unmap the peers and free this rank's buffer (collective)."""
@@ -90,11 +114,12 @@ class PeerOutputs:
         lib = _lib.load()
         torch.cuda.synchronize()
         dist.barrier(group=self._group)  # no rank still stores into a peer
-        for p in self.peer_ptrs:
+        for p in self.peer_ptrs + self.peer_flag_ptrs:
             _lib.check(lib.sa_ipc_close(ctypes.c_void_p(p)))
         dist.barrier(group=self._group)  # no rank still maps this buffer
         self.local = None
         _lib.check(lib.sa_ipc_free(ctypes.c_void_p(self._ptr)))
+        _lib.check(lib.sa_ipc_free(ctypes.c_void_p(self._fptr)))
 
 
 # ---------------------------------------------------------------- balanced layer
@@ -283,10 +308,12 @@ class BalancedLayer:
 
     def step_peers(self, q, k, v, peer: PeerOutputs, group=None) -> torch.Tensor:
         """One layer with the output all-gather fused into the attention
-        epilogue; the stream sync + barrier order every rank's peer stores
-        before any rank reads its output."""
+        epilogue.  Two device-side barriers (no host sync): before the
+        attention, every rank is done with the previous layer's output
+        (write-after-read on the peers' buffers); after it, every rank's peer
+        stores are visible to the work queued next on this stream."""
         self.load_index(self._all_gather(self.estimate(q, k, v), self.world, group))
+        peer.barrier()
         self.attend_peers(q, k, v, peer)
-        torch.cuda.current_stream().synchronize()
-        dist.barrier(group=group)
+        peer.barrier()
         return peer.local[: self.n]

@@ -1,8 +1,9 @@
 """Worker for tests/test_gpu_multigpu_sim.py::test_fused_peer_exchange: one
 rank of a torchrun job whose ranks all share cuda:0 (gloo for the small
 collectives).  It runs multigpu.BalancedLayer.step_peers (output all-gather
-fused into the attention epilogue over CUDA IPC mappings) and prints whether
-its output equals the single-GPU layer bit for bit."""
+fused into the attention epilogue over CUDA IPC mappings, ordered by the
+device-side peer barrier) and prints whether its output equals the
+single-GPU layer bit for bit."""
 import json
 import os
 import sys
@@ -37,9 +38,9 @@ def main():
     peer = PeerOutputs(rank, world, n, H * D)
     ok = []
     for _ in range(2):  # the mapped buffers are reused across layers
+        # no host barrier: step_peers' device-side entry barrier orders this
+        # clear before any peer stores into the buffer
         peer.local.fill_(float("nan"))
-        torch.cuda.synchronize()
-        dist.barrier()  # every buffer is cleared before any rank stores into it
         got = layer.step_peers(q, k, v, peer)
         ok.append(bool(torch.equal(got, want[0])))
     peer.close()

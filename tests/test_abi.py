@@ -92,3 +92,19 @@ def test_device_index_encoding():
     assert list(np.flatnonzero(bits)) == [0, 5, 299]
     rbits = np.unpackbits(b.diagrev[0].view(np.uint8), bitorder="little")
     assert sorted(300 + 127 - np.flatnonzero(rbits)) == [0, 3]
+
+
+def test_peer_barrier_argument_checks():
+    """sa_peer_barrier rejects bad rank / world / pointers before touching the
+    device (the barrier itself runs in tests/test_gpu_multigpu_sim.py)."""
+    from paper_2412_06198_b200 import _lib
+
+    lib = _lib.load()
+    buf = (ctypes.c_int32 * 16)()
+    peers = (ctypes.c_void_p * 1)(None)
+    assert lib.sa_peer_barrier(buf, peers, 0, 0, 1000, None) == 1  # world 0
+    assert lib.sa_peer_barrier(buf, peers, 2, 2, 1000, None) == 1  # rank >= world
+    assert lib.sa_peer_barrier(buf, peers, 0, 9, 1000, None) == 1  # more than 8 ranks
+    assert lib.sa_peer_barrier(buf, peers, 0, 2, 1000, None) == 1  # null peer buffer
+    assert lib.sa_peer_barrier(None, peers, 0, 2, 1000, None) == 1
+    assert lib.sa_peer_barrier(buf, peers, 0, 2, 0, None) == 1  # no timeout
