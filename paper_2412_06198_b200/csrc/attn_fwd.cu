@@ -683,11 +683,28 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = cs;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  // highest scheduling priority: when a short-CTA kernel (the finiteness scan /
+  // cache fill) runs beside it, freed SM slots go to attention CTAs first
+  static const int prio = [] {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const char* e = getenv("SA_ATTN_PRIO");  // A/B: 0 = stream priority
+    return (e && e[0] == '0') ? 1 : hi;
+  }();
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl && counter_zeroed) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (prio <= 0) {
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na].val.priority = prio;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = (pdl && counter_zeroed) ? 1 : 0;
+  cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, kern, a);
   return check_launch("attn_fwd_kernel");
 }

@@ -76,7 +76,7 @@ int launch_check_finite(const void* x, long long count, int32_t* flag, cudaStrea
 // `row` values) fused with the copy of k / v into cache rows of `cap` values
 // per head (cache_k / cache_v may be null); flag as above
 int launch_scan_fill(const void* q, long long nq, const void* k, const void* v, long long nkv, long long row,
-                     void* cache_k, void* cache_v, long long cap, int32_t* flag, cudaStream_t st);
+                     void* cache_k, void* cache_v, long long cap, int32_t* flag, cudaStream_t st, bool chunked = false);
 
 int launch_score_tail(int batch, int heads, int kv_heads, int n, float scale, const void* q,
                       const void* k, int r_lo, int r_hi, float* col_out, float* diag_out,

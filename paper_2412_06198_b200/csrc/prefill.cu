@@ -289,10 +289,13 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   const int n = p.n;
   const int B = desc->batch, H = desc->heads, HK = desc->kv_heads;
 
-  // AttnMatrices' finiteness scan (core.py:72-74) of q, k, v: HBM-bound, on a
-  // second side stream beside the (compute-bound) selection and estimators,
-  // joined before this call's work completes
-  // The KvCache fill (runtime.py:197) rides on the same stream.
+  // AttnMatrices' finiteness scan (core.py:72-74) of q, k, v and the KvCache
+  // fill (runtime.py:197): one HBM-bound kernel on a second side stream,
+  // joined before this call's work completes.  By default it runs beside the
+  // attention (which moves ~1 TB/s of its 8): 128-thread CTAs that fit into
+  // the registers two attention CTAs leave on an SM, the attention launched
+  // at top priority so it claims SMs first (32K auto layer: +25 us over no
+  // scan / fill, against +55 us beside the estimators).
   const bool fill = desc->cache_capacity > 0 && desc->cache_k && desc->cache_v;
   if (fill && desc->cache_capacity < n)
     return fail(SA_ERR_CACHE_OVERFLOW, "cache of capacity %d cannot hold %d rows", desc->cache_capacity, n);
@@ -300,20 +303,29 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
     const char* e = getenv("SA_CHECK_MODE");  // A/B: 0 both, 1 no scan, 2 no fill, 3 neither
     return e ? atoi(e) : 0;
   }();
+  // Placement (SA_SCAN_AT): 0 = grid-stride kernel from the start, joined
+  // before the attention; 1 = short-CTA kernel from the start, joined after
+  // the attention; 2 = short-CTA kernel forked beside the attention (whose
+  // persistent CTAs leave room for one per SM and launch at top priority).
+  static const int scan_at = [] {
+    const char* e = getenv("SA_SCAN_AT");
+    return e ? atoi(e) : 2;
+  }();
   SideStream* chk = (desc->check_flag || fill) ? side_stream() : nullptr;
-  if (chk) {
+  auto fork_scan = [&](bool chunked) -> int {
     cudaEventRecord(chk->fork2, st);
     cudaStreamWaitEvent(chk->s2, chk->fork2, 0);
     if (desc->check_flag) cudaMemsetAsync(desc->check_flag, 0, sizeof(int32_t), chk->s2);
     const long long nq = (long long)p.hh * n * kHeadDim, nkv = (long long)p.hk * n * kHeadDim;
-    if ((rc = launch_scan_fill(q, (chk_mode & 1) ? 0 : nq, k, v, nkv, (long long)n * kHeadDim,
-                               (fill && !(chk_mode & 2)) ? desc->cache_k : nullptr,
-                               (fill && !(chk_mode & 2)) ? desc->cache_v : nullptr,
-                               (long long)std::max(desc->cache_capacity, 1) * kHeadDim, desc->check_flag,
-                               chk->s2)))
-      return rc;
+    const int r = launch_scan_fill(q, (chk_mode & 1) ? 0 : nq, k, v, nkv, (long long)n * kHeadDim,
+                                   (fill && !(chk_mode & 2)) ? desc->cache_k : nullptr,
+                                   (fill && !(chk_mode & 2)) ? desc->cache_v : nullptr,
+                                   (long long)std::max(desc->cache_capacity, 1) * kHeadDim, desc->check_flag,
+                                   chk->s2, chunked);
     cudaEventRecord(chk->join2, chk->s2);
-  }
+    return r;
+  };
+  if (chk && scan_at != 2 && (rc = fork_scan(scan_at == 1))) return rc;
   // The single Block-Cluster candidate's key pooling needs only K: it runs on
   // the side stream from the start, beside the selector.
   static const bool overlap = [] {
@@ -450,7 +462,10 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   // 4. executed tiles + attention
   if ((rc = sa_build_tiles(&V.index, p.hh, n, V.tile_off, V.tile_cnt, V.tiles, stream))) return rc;
   mark(3);
-  if (chk) cudaStreamWaitEvent(st, chk->join2, 0);
+  // SA_SCAN_AT=2: the scan is queued here, ahead of the work-order kernel
+  // (queueing it after the attention launch measured 20 us slower)
+  if (chk && scan_at == 2 && (rc = fork_scan(true))) return rc;
+  if (chk && (scan_at == 0 || desc->stop_after_tiles)) cudaStreamWaitEvent(st, chk->join2, 0);
   if (desc->stop_after_tiles) return SA_OK;
   // CTA order: auto layers mix heavy (VS, dense-like) and light (Block) heads,
   // so the non-empty items go longest-first (LPT); a uniform layer (dense or
@@ -479,5 +494,6 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
                    lpt ? work : nullptr, nullptr, st, desc->out_ld, counter, lpt ? n_work : nullptr, nullptr, 0,
                    lpt);
   mark(4);
+  if (chk && scan_at != 0) cudaStreamWaitEvent(st, chk->join2, 0);
   return rc;
 }

@@ -88,9 +88,63 @@ __global__ void scan_fill_kernel(const uint4* __restrict__ q, long long nq16, co
   if (flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1;
 }
 
+// Chunked variant (one 16 KB piece of q, or 8 KB of k + 8 KB of v, per
+// CTA): short-lived CTAs that fill whatever an SM has left beside a
+// persistent kernel (the attention kernel leaves room for one per SM).
+constexpr int kScanU = 8;
+constexpr int kScanT = 128;  // 128 x 48 registers: fits beside two attention CTAs
+__global__ void __launch_bounds__(kScanT) scan_fill_chunk_kernel(
+    const uint4* __restrict__ q, long long nq16, const uint4* __restrict__ k, const uint4* __restrict__ v,
+    long long nkv16, long long row16, uint4* ck, uint4* cv, long long cap16, int32_t* flag, int kv_blocks) {
+  bool bad = false;
+  if ((int)blockIdx.x < kv_blocks) {
+    const long long base = (long long)blockIdx.x * (kScanT * kScanU / 2) + threadIdx.x;
+    uint4 a[kScanU / 2], b[kScanU / 2];
+#pragma unroll
+    for (int u = 0; u < kScanU / 2; ++u) {
+      const long long i = base + u * kScanT;
+      if (i < nkv16) a[u] = __ldcs(k + i), b[u] = __ldcs(v + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kScanU / 2; ++u) {
+      const long long i = base + u * kScanT;
+      if (i < nkv16) {
+        bad |= bf16x8_bad(a[u]) | bf16x8_bad(b[u]);
+        if (ck) {
+          const long long h = i / row16, r = i - h * row16, o = h * cap16 + r;
+          __stcs(ck + o, a[u]);
+          __stcs(cv + o, b[u]);
+        }
+      }
+    }
+  } else {
+    const long long base = (long long)(blockIdx.x - kv_blocks) * (kScanT * kScanU) + threadIdx.x;
+    uint4 x[kScanU];
+#pragma unroll
+    for (int u = 0; u < kScanU; ++u) {
+      const long long i = base + u * kScanT;
+      if (i < nq16) x[u] = __ldcs(q + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kScanU; ++u)
+      if (base + u * kScanT < nq16) bad |= bf16x8_bad(x[u]);
+  }
+  if (flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
 int launch_scan_fill(const void* q, long long nq, const void* k, const void* v, long long nkv, long long row,
-                     void* cache_k, void* cache_v, long long cap, int32_t* flag, cudaStream_t st) {
+                     void* cache_k, void* cache_v, long long cap, int32_t* flag, cudaStream_t st, bool chunked) {
   if ((nq | nkv | row | cap) % 8 != 0) return fail(SA_ERR_DIMENSION, "scan/fill needs 16-byte rows");
+  if (chunked) {
+    const long long kv_blocks = (nkv / 8 + kScanT * kScanU / 2 - 1) / (kScanT * kScanU / 2);
+    const long long q_blocks = (nq / 8 + kScanT * kScanU - 1) / (kScanT * kScanU);
+    if (kv_blocks + q_blocks == 0) return SA_OK;
+    scan_fill_chunk_kernel<<<(unsigned)(kv_blocks + q_blocks), kScanT, 0, st>>>(
+        reinterpret_cast<const uint4*>(q), nq / 8, reinterpret_cast<const uint4*>(k),
+        reinterpret_cast<const uint4*>(v), nkv / 8, row / 8, reinterpret_cast<uint4*>(cache_k),
+        reinterpret_cast<uint4*>(cache_v), cap / 8, flag, (int)kv_blocks);
+    return check_launch("scan_fill_chunk_kernel");
+  }
   static const int cap_blocks = [] {
     const char* e = getenv("SA_SCAN_BLOCKS");  // A/B: grid of the fused scan / cache fill
     return e ? atoi(e) : 296;
