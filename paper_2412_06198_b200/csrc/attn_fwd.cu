@@ -660,7 +660,12 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   });
   // persistent: two CTAs per SM (113 KB shared memory and 256 TMEM columns each)
   const int num_sms = device_sm_count();
-  const int grid = (int)std::min<long long>(2LL * num_sms, (long long)a.hh_total * a.nqt);
+  static const int per_sm = [] {
+    const char* e = getenv("SA_ATTN_CTAS");  // A/B: CTAs per SM (default 2)
+    const int v = e ? atoi(e) : 2;
+    return v == 1 ? 1 : 2;
+  }();
+  const int grid = (int)std::min<long long>((long long)per_sm * num_sms, (long long)a.hh_total * a.nqt);
   // the need_weights path derives weights from lse: keep exact MUFU exps there
   void (*kern)(AttnArgs);
   switch (lse != nullptr ? 0 : poly) {

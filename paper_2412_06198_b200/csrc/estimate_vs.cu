@@ -86,6 +86,7 @@ struct TailArgs {
   int qrow0;           // global row of Q box row 0 (r_hi - 64, may be negative)
   int nkt;             // key tiles with a causal key: ceil(r_hi / 128)
   int wave_units;      // most units per wave
+  int min_tiles;       // fewest key tiles per CTA (small launches leave SMs to the concurrent block chain)
   float scale_log2;
   float2* stats;       // [U, kVsMaxCta, 2 key halves, 256] per-(chunk, row) (max2, sum)
   float2* stats2;      // [U, 16, 256] per-(group, row)
@@ -189,7 +190,7 @@ __device__ __forceinline__ VsPlace vs_place(const TailArgs& a) {
   VsPlace p;
   p.U = *a.unit_count;
   p.W = min(p.U, a.wave_units);
-  p.cpu = p.W > 0 ? min((int)gridDim.x / p.W, min(a.nkt, kVsMaxCta)) : 0;
+  p.cpu = p.W > 0 ? min((int)gridDim.x / p.W, min((a.nkt + a.min_tiles - 1) / a.min_tiles, kVsMaxCta)) : 0;
   p.ws = p.cpu > 0 ? (int)blockIdx.x / p.cpu : 0;
   p.rank = p.cpu > 0 ? (int)blockIdx.x % p.cpu : 0;
   p.t_lo = p.cpu > 0 ? (int)(((long long)p.rank * a.nkt) / p.cpu) : 0;
@@ -698,6 +699,12 @@ static int launch_tail64(int batch, int heads, int kv_heads, int n, float scale,
   a.qrow0 = r_hi - 64;
   a.nkt = (r_hi + kTile - 1) / kTile;
   a.wave_units = tail_wave_units(n);
+  static const int min_tiles = [] {
+    const char* e = getenv("SA_VS_MIN_TILES");  // A/B
+    const int v = e ? atoi(e) : 1;
+    return v >= 1 ? v : 1;
+  }();
+  a.min_tiles = min_tiles;
   a.scale_log2 = scale * 1.4426950408889634f;
   if (ws_bytes < tail_workspace_bytes(a.hh_total, n, r_hi))
     return fail(SA_ERR_DIMENSION, "score_tail workspace too small");
