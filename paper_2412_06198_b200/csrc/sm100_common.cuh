@@ -263,17 +263,21 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 // via the 1.5*2^23 magic add, 2^f by a degree-3 fit on [-0.5, 0.5] (max rel
 // error 7.5e-5, below the bf16 rounding of P), 2^j added into the exponent
 // field.  x is clamped at -125 (result ~2e-38 instead of 0 for masked logits).
+// 2^j is built as a float scale (exponent field j + 127); x <= -127 (masked
+// logits, -inf) gives the field 0, i.e. a scale of +0 and an exact 0 result,
+// like ex2.approx.ftz (results below 2^-126 flush to 0 as well).
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -125.f);
-  x.y = fmaxf(x.y, -125.f);
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
   const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
   const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
   const float2 f = ffma2(j, make_float2(-1.f, -1.f), x);
   float2 p = ffma2(make_float2(0.0551716685f, 0.0551716685f), f, make_float2(0.242611155f, 0.242611155f));
   p = ffma2(p, f, make_float2(0.693260968f, 0.693260968f));
   p = ffma2(p, f, make_float2(0.999928057f, 0.999928057f));
-  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
-                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+  const float2 sc = make_float2(__uint_as_float((__float_as_uint(t.x) << 23) + 0x3f800000u),
+                                __uint_as_float((__float_as_uint(t.y) << 23) + 0x3f800000u));
+  return fmul2(p, sc);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {

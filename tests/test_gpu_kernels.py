@@ -133,7 +133,8 @@ def gather_tiles(rows, b, n):
 
 
 @pytest.mark.parametrize("n,b,k_b", [(1000, 8, 1), (4096, 8, 1), (4100, 8, 2), (2049, 16, 3), (3000, 32, 2),
-                                     (4096, 64, 4), (777, 8, 5), (300, 16, 1)])
+                                     (4096, 64, 4), (777, 8, 5), (300, 16, 1), (4100, 64, 3), (2000, 64, 1),
+                                     (8192, 64, 20)])
 def test_block_gather_vs_oracle(sa, n, b, k_b):
     """Block-Cluster heads through the gathered-tile path: outputs against the
     oracle's block kernel, and the tile counts the gather cost model implies."""
