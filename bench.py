@@ -504,11 +504,12 @@ def estimator_roofline(n, dev, reps=5):
     g.manual_seed(5)
     q = (torch.rand((H, n, D), generator=g, device=dev) * 2 - 1).bfloat16()
     k = (torch.rand((HK, n, D), generator=g, device=dev) * 2 - 1).bfloat16()
-    col = torch.empty((H, n), dtype=torch.float32, device=dev)
-    diag = torch.empty((H, n), dtype=torch.float32, device=dev)
+    # column rows then diagonal rows in one buffer: one top-k launch over all
+    # 2H rows, as sa_prefill's VS index step launches it
+    scores = torch.empty((2, H, n), dtype=torch.float32, device=dev)
+    col, diag = scores[0], scores[1]
     kk = 3 * n // 64
-    ci = torch.empty((H, kk), dtype=torch.int32, device=dev)
-    di = torch.empty((H, kk), dtype=torch.int32, device=dev)
+    idx = torch.empty((2 * H, kk), dtype=torch.int32, device=dev)
     lib = _lib.load()
     wsb = int(lib.sa_score_tail_workspace(1, H, n, n))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
@@ -520,8 +521,7 @@ def estimator_roofline(n, dev, reps=5):
                   diag.data_ptr(), 0, None, 0, ws.data_ptr(), wsb, st)
 
     def topk():
-        _lib.call("sa_topk_stable_f32", col.data_ptr(), H, n, n, kk, ci.data_ptr(), kk, st)
-        _lib.call("sa_topk_stable_f32", diag.data_ptr(), H, n, n, kk, di.data_ptr(), kk, st)
+        _lib.call("sa_topk_stable_f32", scores.data_ptr(), 2 * H, n, n, kk, idx.data_ptr(), kk, st)
 
     for _ in range(2):
         est()

@@ -55,6 +55,7 @@ struct TopkArgs {
   const int32_t* gate;   // optional: process row r only if gate[r / gate_div] == gate_val
   int gate_div;
   int gate_val;
+  int gate_sparse;       // the gate is expected to keep few rows (auto layers): size the launch for that
   // optional second row set: rows r >= split use (scores2, k2, idx_out2, bits2,
   // bit_base2, bit_neg2) with local row r - split (same ld / out_ld / bits_ld)
   int split;

@@ -419,6 +419,7 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
       t.bit_base = 0;
       t.bit_neg = 0;
       t.gate = choice ? choice : V.family;
+      t.gate_sparse = desc->mode == SA_MODE_AUTO;  // a fixed VS layer keeps every row
       t.gate_div = 1;
       t.gate_val = choice ? c : SA_VERTICAL_SLASH;
       // diagonal rows in the same launch (rows >= hh)

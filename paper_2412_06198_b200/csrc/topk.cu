@@ -27,6 +27,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -476,6 +477,7 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
   __shared__ int sh_rem;
   const int tid = threadIdx.x, lane = tid & 31;
 
+  auto key_of = [&](int j) -> uint32_t { return skey[j]; };
   // stage the slice as preference keys (16-byte loads when aligned)
   {
     const float* sp = s + j_lo;
@@ -501,8 +503,9 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
     __syncthreads();
     uint32_t mn = 0xffffffffu, mx = 0u;
     for (int j = tid; j < sl; j += blockDim.x) {
-      mn = min(mn, skey[j]);
-      mx = max(mx, skey[j]);
+      const uint32_t kj = key_of(j);
+      mn = min(mn, kj);
+      mx = max(mx, kj);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -529,7 +532,7 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
       __syncthreads();
       const BinMap bm = make_binmap(lo, span);
       for (int j = tid; j < sl; j += blockDim.x) {
-        const uint32_t key = skey[j];
+        const uint32_t key = key_of(j);
         if (key >= lo && (uint64_t)(key - lo) < span) atomicAdd(&hist[key_bin(key, bm)], 1);
       }
       cl.sync();
@@ -581,7 +584,7 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
       int* lm = cl.map_shared_rank(&sh_m, 0);
       uint64_t* lc = cl.map_shared_rank(cand, 0);
       for (int j0 = tid; (j0 & ~31) < sl; j0 += blockDim.x) {  // warp-uniform trip count
-        const uint32_t key = j0 < sl ? skey[j0] : 0u;
+        const uint32_t key = j0 < sl ? key_of(j0) : 0u;
         const bool hit = j0 < sl && key >= lo && (uint64_t)(key - lo) < span;
         const uint32_t bal = __ballot_sync(0xffffffffu, hit);
         if (bal) {
@@ -623,7 +626,7 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
   const int w0 = min(sl, w * wlen), w1 = min(sl, w0 + wlen);
   int mine = 0;
   for (int j = w0 + lane; (j - lane) < w1; j += 32) {
-    const bool keep = j < w1 && (take_all || (k > 0 && composite(skey[j], j_lo + j) >= T));
+    const bool keep = j < w1 && (take_all || (k > 0 && composite(key_of(j), j_lo + j) >= T));
     mine += __popc(__ballot_sync(0xffffffffu, keep));
   }
   int total;
@@ -644,7 +647,7 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
   int pos = sh_base + __shfl_sync(0xffffffffu, wbase, 0);
   if (mine > 0) {
     for (int j = w0 + lane; (j - lane) < w1; j += 32) {
-      const bool keep = j < w1 && (take_all || (k > 0 && composite(skey[j], j_lo + j) >= T));
+      const bool keep = j < w1 && (take_all || (k > 0 && composite(key_of(j), j_lo + j) >= T));
       const uint32_t bal = __ballot_sync(0xffffffffu, keep);
       if (keep) {
         const int p = pos + __popc(bal & ((1u << lane) - 1u));
@@ -681,10 +684,24 @@ int launch_topk(const TopkArgs& a, cudaStream_t st) {
     const char* e = getenv("SA_TOPK_CLUSTER");  // A/B: cluster-of-8 kernel for long rows
     return e ? atoi(e) : 1;
   }();
+  // Long plain rows: a cluster per row (keys staged in the CTAs' shared
+  // memory) while all clusters fit one wave — the lowest latency per row;
+  // beyond that, rows that fit one CTA's shared memory go one CTA per row
+  // (32K x 64 rows: 30 vs 48 us) and longer rows stay on clusters in two
+  // waves (clusters re-reading their slices from L2 fit one wave but doubled
+  // the per-row latency: 128K x 64 rows 104 vs 87 us).  SA_TOPK_CLUSTER=2
+  // forces clusters.
   if (use_cluster && a.lens == nullptr && a.ks == nullptr && a.n >= kClusterMin && a.n <= 262144 &&
       threads == kTopkThreads) {
-    topk_cluster_kernel<<<rows * kClusterC, kTopkThreads, kTopkSmem + cl_per * 4, st>>>(a);
-    return check_launch("topk_cluster_kernel");
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, topk_cluster_kernel, kTopkThreads,
+                                                  kTopkSmem + cl_per * 4);
+    const bool one_wave = (long long)rows * kClusterC <= (long long)std::max(per_sm, 1) * device_sm_count();
+    // (auto layers' gated VS rows: usually only a few are kept — clusters)
+    if (use_cluster == 2 || (use_cluster == 1 && (one_wave || a.gate_sparse || a.n > kCacheMax))) {
+      topk_cluster_kernel<<<rows * kClusterC, kTopkThreads, kTopkSmem + cl_per * 4, st>>>(a);
+      return check_launch("topk_cluster_kernel");
+    }
   }
   const int maxlen = a.n;  // a.n bounds every row length
   if (maxlen <= kCacheMax && a.lens == nullptr)

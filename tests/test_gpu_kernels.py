@@ -189,6 +189,29 @@ def test_topk_bit_exact(sa, n, k):
         np.testing.assert_array_equal(got[r], O.top_k_stable(rows[r], k))
 
 
+@pytest.mark.parametrize("n,k,nrows", [(32768, 1536, 48), (131072, 6144, 48), (20000, 777, 40)])
+def test_topk_many_rows_bit_exact(sa, n, k, nrows):
+    """More rows than one wave of clusters: rows that fit one CTA's shared
+    memory go one CTA per row, longer ones to clusters in two waves
+    (csrc/topk.cu launch_topk); both must stay bit-exact."""
+    rng = np.random.default_rng(n + nrows)
+    rows = []
+    for r in range(nrows):
+        kind = r % 4
+        if kind == 0:
+            rows.append(rng.random(n).astype(np.float32))
+        elif kind == 1:
+            rows.append((rng.integers(0, 6, n) * 0.25).astype(np.float32))
+        elif kind == 2:
+            rows.append((rng.random(n) ** 8 * 1e-3).astype(np.float32))
+        else:
+            rows.append(np.where(rng.random(n) < 0.5, np.float32(0.0), rng.standard_normal(n).astype(np.float32)))
+    rows = np.stack(rows)
+    got = device_topk(rows, k)
+    for r in range(nrows):
+        np.testing.assert_array_equal(got[r], O.top_k_stable(rows[r], k), err_msg=f"row {r}")
+
+
 def test_topk_golden_vectors(sa):
     from tests.golden_io import load
 
