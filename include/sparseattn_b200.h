@@ -193,6 +193,16 @@ int sa_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b, f
                     const void* qp, const void* kp, int32_t* blk_idx, int32_t* blk_row_off,
                     void* ws, size_t ws_bytes, void* stream);
 
+/* Block-Cluster index for k_b <= 8 straight from bf16 q [B*H, n, 128] and k
+ * [B*HK, n, 128] (the path sa_prefill takes; replaces block_mean +
+ * build_block_index, patterns.py:279-321): fp32 pooling, one fp16 tcgen05
+ * screen pass with a rigorous error bound, exact fp64 re-scoring of every
+ * near-cut candidate.  Same row layout as sa_block_select (scale-free: the
+ * positive 1/sqrt(d) does not change a row's order). */
+size_t sa_block_index_workspace(int batch, int heads, int kv_heads, int n, int b, int k_b);
+int sa_block_index_bf16(int batch, int heads, int kv_heads, int n, int b, int k_b, const void* q, const void* k,
+                        int32_t* blk_idx, int32_t* blk_row_off, void* ws, size_t ws_bytes, void* stream);
+
 /* Dense [n, n] fp32 weights of head hh under `index` (need_weights=True of
  * patterns.py:422-434, 466-467; core.py:152), rows normalised by the lse that
  * sa_attn_sparse returned.  n <= 1048560 (the caller owns the n * n * 4 bytes). */

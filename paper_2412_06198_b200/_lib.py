@@ -116,6 +116,8 @@ _SIGNATURES = {
     "sa_block_pool": (ctypes.c_int, [_I, _I, _I, _I, _P, _P, _P, _P]),
     "sa_block_select_workspace": (_SZ, [_I, _I, _I]),
     "sa_block_select": (ctypes.c_int, [_I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _P, _P, _SZ, _P]),
+    "sa_block_index_workspace": (_SZ, [_I, _I, _I, _I, _I, _I]),
+    "sa_block_index_bf16": (ctypes.c_int, [_I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _SZ, _P]),
     "sa_attn_weights": (ctypes.c_int, [_I, _I, _I, _I, _F, _P, _P, _P, _IDX, _P, _P]),
     "sa_block_mean_f32": (ctypes.c_int, [_P, _I, _I, _I, _P, _P]),
     "sa_build_tiles": (ctypes.c_int, [_IDX, _I, _I, _P, _P, _P, _P]),

@@ -65,6 +65,7 @@ struct AttnArgs {
   const int32_t* n_work;     // optional device count of `work` entries (default hh_total * nqt)
   int st256;                 // output rows 32-byte aligned: 256-bit stores
   int skip_dead;             // warps whose 32 rows are all masked out of a sub-tile write P = 0 only
+  int epi_mode;              // experiment (SA_ATTN_EPI): 1 = full epilogue, 0 = no global stores, 2 = no O read
   int n_peers;               // > 0: every output row is also stored into these buffers (same layout),
   __nv_bfloat16* peer_out[kMaxPeers];  // other ranks' outputs mapped over NVLink (fused all-gather)
 };
@@ -526,8 +527,12 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       const long long ooff = (long long)bidx * a.out_batch_stride + (long long)i * a.out_row_stride +
                              (long long)h * kHeadDim;
       __nv_bfloat16* orow = a.out + ooff;
+      if (a.epi_mode == 2) {
+        tc_fence_before();
+        mbar_arrive(&bars[B_OE]);
+      }
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < (a.epi_mode == 2 ? 0 : 4); ++c) {
         uint32_t o[32];
         tmem_ld32(tbase + lane_off + kColO + 32 * c, o);
         tmem_ld_wait();
@@ -535,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
           tc_fence_before();
           mbar_arrive(&bars[B_OE]);  // O may now be overwritten by the next item's PV(0)
         }
-        if (valid) {
+        if (valid && a.epi_mode == 1) {
           uint32_t pk[16];
 #pragma unroll
           for (int t = 0; t < 16; ++t)
@@ -617,6 +622,11 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
     return e ? atoi(e) : 1;
   }();
   a.skip_dead = skip_dead;
+  static const int epi_mode = [] {
+    const char* e = getenv("SA_ATTN_EPI");  // experiment only: output left unwritten when != 1
+    return e ? atoi(e) : 1;
+  }();
+  a.epi_mode = epi_mode;
   if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && !peer_out))
     return fail(SA_ERR_DIMENSION, "n_peers must be in [0, %d]", kMaxPeers);
   a.n_peers = n_peers;

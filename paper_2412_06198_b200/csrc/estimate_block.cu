@@ -350,6 +350,14 @@ __global__ void fixed_row_off_kernel(int32_t* row_off, int hh_total, int nb, int
   row_off[(long long)hh * row_stride + g] = (int32_t)(hh * head_stride + (long long)g * stride);
 }
 
+int launch_fixed_row_off(int32_t* row_off, int hh_total, int nb, int stride, int row_stride, long long head_stride,
+                         const int32_t* gate, int gate_val, cudaStream_t st) {
+  const long long tot = (long long)hh_total * (nb + 1);
+  fixed_row_off_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(row_off, hh_total, nb, stride, row_stride,
+                                                                       head_stride, gate, gate_val);
+  return check_launch("fixed_row_off_kernel");
+}
+
 // MATERIALIZE: per row, fold the stable top-k output (ascending ids) and the
 // forced diagonal into the fixed-stride row.
 __global__ void merge_diag_kernel(const int32_t* topk, int k_b, int nb, int32_t* blk_idx,

@@ -88,6 +88,17 @@ size_t tail_workspace_bytes(int hh_total, int n, int r_hi);
 int launch_block_pool(int groups, int n, int b, int side, const void* x, void* split_out,
                       float* mean_out, const int32_t* gate, int gate_val, cudaStream_t st);
 size_t block_select_ws(int n, int b, int k_b, int hh_total);
+int launch_fixed_row_off(int32_t* row_off, int hh_total, int nb, int stride, int row_stride, long long head_stride,
+                         const int32_t* gate, int gate_val, cudaStream_t st);
+// block_screen.cu: Block-Cluster index for k_b <= 8 (fp16 screen + exact refine)
+size_t pool16_bytes(int groups, int nb);
+size_t block_screen_ws(int nb, int k_b, int hh_total);
+int launch_block_pool16(int groups, int n, int b, const void* x, void* pooled, bool key_side, const int32_t* gate,
+                        int gate_val, cudaStream_t st);
+int launch_block_screen(int batch, int heads, int kv_heads, int n, int b, int k_b, const void* qpool,
+                        const void* kpool, int32_t* blk_idx, long long head_stride, int32_t* blk_row_off,
+                        int row_stride, const int32_t* gate, int gate_val, void* ws, size_t ws_bytes,
+                        cudaStream_t st);
 int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b, float scale,
                         const void* qp, const void* kp, int32_t* blk_idx, long long head_stride,
                         int32_t* blk_row_off, int row_stride, const int32_t* gate, int gate_val,

@@ -104,6 +104,18 @@ static int clamp_pattern(const sa_pattern& in, int n, sa_pattern* out) {
   return SA_OK;
 }
 
+// SA_BLOCK_SCREEN=1: Block-Cluster candidates with k_b <= 8 take the fp16
+// screen + exact refine of block_screen.cu instead of the split-bf16 GEMM of
+// estimate_block.cu.  Opt-in: measured slower at 32K ("Block
+// estimator: fp16 screen"), kept for A/B and as the sa_block_index_bf16 path.
+static bool use_block_screen(int k_b) {
+  static const bool on = [] {
+    const char* e = getenv("SA_BLOCK_SCREEN");
+    return e && e[0] == '1';
+  }();
+  return on && k_b <= 8;
+}
+
 static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
   if (!d) return fail(SA_ERR_DIMENSION, "null descriptor");
   if (d->batch < 1 || d->heads < 1 || d->kv_heads < 1 || d->n < 1)
@@ -159,6 +171,7 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
       p->max_nb = std::max(p->max_nb, nb);
       head_stride = std::max(head_stride, (long long)nb * (pt.p2 + 1));
       blk_ws = std::max(blk_ws, block_select_ws(n, pt.p1, pt.p2, p->hh));
+      if (use_block_screen(pt.p2)) blk_ws = std::max(blk_ws, block_screen_ws(nb, pt.p2, p->hh));
     }
   }
   // block rows are addressed with int32 offsets (hh * head_stride + row * stride)
@@ -171,8 +184,9 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
   p->tail_groups = (p->q_est + 127) / 128;
   const int r_hi_max = n;
   p->tail_ws = p->any_vs ? tail_workspace_bytes(p->hh, n, r_hi_max) : 256;
-  p->qp_elems = p->any_block ? (size_t)p->hh * p->max_nb * 384 : 128;
-  p->kp_elems = p->any_block ? (size_t)p->hk * p->max_nb * 256 : 128;
+  // pooled blocks: split-bf16 operands (k_b > 8) or the fp16-screen layout (k_b <= 8), whichever is larger
+  p->qp_elems = p->any_block ? std::max((size_t)p->hh * p->max_nb * 384, pool16_bytes(p->hh, p->max_nb) / 2) : 128;
+  p->kp_elems = p->any_block ? std::max((size_t)p->hk * p->max_nb * 256, pool16_bytes(p->hk, p->max_nb) / 2) : 128;
 
   size_t sz[W_NUM];
   const size_t hh = p->hh;
@@ -340,8 +354,11 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   if (kpool_early) {
     cudaEventRecord(side->fork0, st);
     cudaStreamWaitEvent(side->s, side->fork0, 0);
-    if ((rc = launch_block_pool(p.hk, n, p.cand[blk_c].p1, 1, k, b + L.off[W_KP], nullptr, nullptr, 0, side->s)))
-      return rc;
+    if (use_block_screen(p.cand[blk_c].p2))
+      rc = launch_block_pool16(p.hk, n, p.cand[blk_c].p1, k, b + L.off[W_KP], true, nullptr, 0, side->s);
+    else
+      rc = launch_block_pool(p.hk, n, p.cand[blk_c].p1, 1, k, b + L.off[W_KP], nullptr, nullptr, 0, side->s);
+    if (rc) return rc;
     cudaEventRecord(side->kdone, side->s);
   }
   // 1. per-head choice
@@ -442,6 +459,21 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
       const int bs = p.cand[c].p1, kb = p.cand[c].p2;
       const int32_t* gate = choice ? choice : V.family;
       const int gval = choice ? c : SA_BLOCK_SPARSE;
+      if (use_block_screen(kb)) {
+        // k_b <= 8 (the auto search's Block(8, 1)): fp16 screen + exact refine (block_screen.cu)
+        if ((rc = launch_block_pool16(p.hh, n, bs, q, b + L.off[W_QP], false, gate, gval, st))) return rc;
+        if (kpool_early) {
+          cudaStreamWaitEvent(st, side->kdone, 0);
+        } else if ((rc = launch_block_pool16(p.hk, n, bs, k, b + L.off[W_KP], true, nullptr, 0, st))) {
+          return rc;
+        }
+        if ((rc = launch_block_screen(B, H, HK, n, bs, kb, b + L.off[W_QP], b + L.off[W_KP],
+                                      const_cast<int32_t*>(V.index.blk_idx), p.blk_head_stride,
+                                      const_cast<int32_t*>(V.index.blk_row_off), p.blk_row_stride, gate, gval,
+                                      b + L.off[W_BLKWS], p.blk_ws, st)))
+          return rc;
+        continue;
+      }
       if ((rc = launch_block_pool(p.hh, n, bs, 0, q, b + L.off[W_QP], nullptr, gate, gval, st))) return rc;
       if (kpool_early) {
         cudaStreamWaitEvent(st, side->kdone, 0);

@@ -38,6 +38,18 @@
 namespace sa {
 
 constexpr int kTopkThreads = 1024;
+
+// Profiling hook (tools/topk_lab.py --trace): per-CTA globaltimer stamps at the
+// phase boundaries, [blockIdx.x * 16 + phase]; null (the default) disables.
+__device__ unsigned long long* g_topk_trace = nullptr;
+__device__ __forceinline__ void tk_stamp(int e) {
+  unsigned long long* t = g_topk_trace;
+  if (t != nullptr && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    t[blockIdx.x * 16 + e] = v;
+  }
+}
 constexpr int kBins = 4096;
 constexpr int kCand = 1024;
 constexpr int kTopkSmem = kBins * 4 + kCand * 8;  // 24 KB dynamic
@@ -109,6 +121,24 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total)
   total = warp_tot[32];
   __syncthreads();
   return r;
+}
+
+// Exact rank of the candidates: warp gw of nw (block-wide or cluster-wide
+// numbering) ranks candidates gw, gw + nw, ...; its lanes split the
+// comparisons and a butterfly sums them, so m candidates cost m^2 / (32 nw)
+// compares per lane instead of m per thread.  The composite of rank want - 1
+// (0-based; composites are unique) is written to *T_out.
+__device__ __forceinline__ void rank_candidates(const uint64_t* cand, int m, int want, int gw, int nw,
+                                                uint64_t* T_out) {
+  const int lane = threadIdx.x & 31;
+  for (int c = gw; c < m; c += nw) {
+    const uint64_t me = cand[c];
+    int rank = 0;
+    for (int o = lane; o < m; o += 32) rank += cand[o] > me;
+#pragma unroll
+    for (int x = 16; x > 0; x >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, x);
+    if (lane == 0 && rank == want - 1) *T_out = me;
+  }
 }
 
 // Histogram of the keys inside [lo, lo + span) into kBins bins; returns the bin
@@ -184,6 +214,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
   int k = a.ks ? a.ks[r] : kk;
   k = k < len ? k : len;
   const float* s = scores + (long long)r * a.ld;
+  tk_stamp(0);
 
   extern __shared__ __align__(16) uint8_t tk_smem[];
   int* hist = reinterpret_cast<int*>(tk_smem);
@@ -203,6 +234,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
     for (int j = 4 * n4 + threadIdx.x; j < len; j += blockDim.x) skey[j] = pref_key(__ldg(s + j));
     __syncthreads();
   }
+  tk_stamp(1);
   __shared__ int warp_tot[33];
   __shared__ uint32_t sh_min, sh_max;
   __shared__ int sh_m;
@@ -251,9 +283,11 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
     uint64_t span = (uint64_t)(sh_max - sh_min) + 1;
     int want = k;  // rank (1-based) of T among the keys in [lo, lo + span)
     bool located = false;
+    tk_stamp(2);
     for (int level = 0; level < 2 && !located; ++level) {
       int bin, above;
       hist_locate<CACHED>(s, skey, len, lo, span, want, hist, warp_tot, sh_pair, bin, above);
+      tk_stamp(3 + 3 * level);
       const int m = sh_pair[2];
       want -= above;
       // narrow the key range to the bin: keys with key_bin == bin
@@ -287,14 +321,11 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
         }
       }
       __syncthreads();
+      tk_stamp(4 + 3 * level);
       // 4. exact rank of every candidate; rank want - 1 (0-based) is T
-      for (int c = tid; c < m; c += blockDim.x) {
-        const uint64_t me = cand[c];
-        int rank = 0;
-        for (int o = 0; o < m; ++o) rank += cand[o] > me;
-        if (rank == want - 1) sh_T = me;
-      }
+      rank_candidates(cand, m, want, tid >> 5, (int)blockDim.x >> 5, &sh_T);
       __syncthreads();
+      tk_stamp(5 + 3 * level);
       T = sh_T;
       located = true;
     }
@@ -378,6 +409,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(TopkArgs a) {
     }
   }
   if (tid == 0 && a.count_out) a.count_out[blockIdx.x] = total;
+  tk_stamp(15);
 }
 
 namespace cg = cooperative_groups;
@@ -478,6 +510,7 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
   const int tid = threadIdx.x, lane = tid & 31;
 
   auto key_of = [&](int j) -> uint32_t { return skey[j]; };
+  tk_stamp(0);
   // stage the slice as preference keys (16-byte loads when aligned)
   {
     const float* sp = s + j_lo;
@@ -492,6 +525,7 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
     }
     for (int j = 4 * n4 + tid; j < sl; j += blockDim.x) skey[j] = pref_key(__ldg(sp + j));
   }
+  tk_stamp(1);
   const bool take_all = k >= len;
   uint64_t T = 0;
   if (!take_all && k > 0) {
@@ -526,6 +560,7 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
     uint64_t span = (uint64_t)(*cl.map_shared_rank(&sh_max, 0) - lo) + 1;
     int want = k;
     bool located = false;
+    tk_stamp(2);
     for (int level = 0; level < 2 && !located; ++level) {
       // 2. per-CTA histograms of the slice; the leader sums them and locates
       for (int t = tid; t < kBins; t += blockDim.x) hist[t] = 0;
@@ -572,6 +607,7 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
         if (tid == 0) sh_m = 0;
       }
       cl.sync();
+      tk_stamp(3 + 3 * level);
       const int* lp = cl.map_shared_rank(sh_pair, 0);
       const int bin = lp[0], above = lp[1], m = lp[2];
       want -= above;
@@ -595,6 +631,7 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
         }
       }
       cl.sync();
+      tk_stamp(4 + 3 * level);
       // 4. exact ranks: every CTA copies the leader's candidates and ranks
       // its share of them; the one of rank want - 1 goes to the leader
       {
@@ -602,14 +639,11 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
         if (cr != 0)
           for (int c = tid; c < m; c += blockDim.x) cand[c] = rc[c];
         __syncthreads();
-        for (int c = cr * blockDim.x + tid; c < m; c += kClusterC * blockDim.x) {
-          const uint64_t me = cand[c];
-          int rank = 0;
-          for (int o = 0; o < m; ++o) rank += cand[o] > me;
-          if (rank == want - 1) *cl.map_shared_rank(&sh_T, 0) = me;
-        }
+        const int nwc = (int)blockDim.x >> 5;
+        rank_candidates(cand, m, want, cr * nwc + (tid >> 5), kClusterC * nwc, cl.map_shared_rank(&sh_T, 0));
       }
       cl.sync();
+      tk_stamp(5 + 3 * level);
       T = *cl.map_shared_rank(&sh_T, 0);
       located = true;
     }
@@ -661,7 +695,9 @@ __global__ void __cluster_dims__(kClusterC, 1, 1) __launch_bounds__(kTopkThreads
       pos += __popc(bal);
     }
   }
+  tk_stamp(14);
   cl.sync();  // no CTA leaves while its shared memory may still be read
+  tk_stamp(15);
 }
 
 int launch_topk(const TopkArgs& a, cudaStream_t st) {
@@ -712,6 +748,11 @@ int launch_topk(const TopkArgs& a, cudaStream_t st) {
 }
 
 }  // namespace sa
+
+extern "C" int sa_topk_trace_buffer(void* p) {
+  unsigned long long* v = reinterpret_cast<unsigned long long*>(p);
+  return cudaMemcpyToSymbol(sa::g_topk_trace, &v, sizeof(v)) == cudaSuccess ? 0 : 1;
+}
 
 extern "C" int sa_topk_stable_f32(const float* scores, int rows, int n, long long ld, int k,
                                   int32_t* idx_out, long long out_ld, void* stream) {
