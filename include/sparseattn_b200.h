@@ -138,6 +138,11 @@ int sa_prefill(const sa_prefill_desc* desc, const void* q, const void* k, const 
 int sa_check_finite_bf16(const void* x, long long count, int32_t* flag, void* stream);
 /* cudaMemcpy2DAsync passthrough (kind = cudaMemcpyDefault) so host code can
  * move a head group's output columns without torch strided copies. */
+/* fp32 <-> bf16 staging of host-API (numpy float32) layers: count elements,
+ * round to nearest even; sa_f32_to_bf16 also sets *flag (nullable) to 1 if any
+ * input is NaN/Inf (AttnMatrices' check, core.py:72-74, on the rows as given). */
+int sa_f32_to_bf16(const float* x, void* y, long long count, int32_t* flag, void* stream);
+int sa_bf16_to_f32(const void* x, float* y, long long count, void* stream);
 int sa_memcpy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
                       size_t height, void* stream);
 

@@ -123,6 +123,8 @@ _SIGNATURES = {
     "sa_build_tiles": (ctypes.c_int, [_IDX, _I, _I, _P, _P, _P, _P]),
     "sa_check_finite_bf16": (ctypes.c_int, [_P, _LL, _P, _P]),
     "sa_memcpy2d_async": (ctypes.c_int, [_P, _SZ, _P, _SZ, _SZ, _SZ, _P]),
+    "sa_f32_to_bf16": (ctypes.c_int, [_P, _P, _LL, _P, _P]),
+    "sa_bf16_to_f32": (ctypes.c_int, [_P, _P, _LL, _P]),
     "sa_select_family": (ctypes.c_int, [_P, ctypes.c_int64, _I, _I, _P, _P]),
     "sa_block_topk_workspace": (_SZ, [_I, _I]),
     "sa_block_topk_f32": (ctypes.c_int, [_P, _I, ctypes.c_int64, _I, _P, _P, _SZ, _P]),

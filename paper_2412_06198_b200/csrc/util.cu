@@ -4,11 +4,13 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
 
 #include "api_common.h"
+#include "internal.h"
 
 namespace sa {
 
@@ -185,6 +187,71 @@ int sa::launch_check_finite(const void* x, long long count, int32_t* flag, cudaS
   check_finite_kernel<<<(int)blocks, threads, 0, st>>>(
       reinterpret_cast<const uint4*>(x), n16, reinterpret_cast<const uint16_t*>(x) + n16 * 8, ntail, flag);
   return check_launch("check_finite_kernel");
+}
+
+// ---------------------------------------------------- fp32 <-> bf16 staging
+namespace sa {
+// fp32 -> bf16 (round to nearest even) with the finiteness flag of the fp32
+// input (exponent all ones): the AttnMatrices check (core.py:72-74) on the
+// rows as given; 32-byte loads, grid-stride.
+__global__ void f32_to_bf16_kernel(const float4* __restrict__ x, uint2* __restrict__ y, long long n4,
+                                   const float* tail, __nv_bfloat16* ytail, int ntail, int32_t* flag) {
+  bool bad = false;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = __ldcs(x + i);
+    bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    y[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < ntail) {
+    bad |= !isfinite(tail[threadIdx.x]);
+    ytail[threadIdx.x] = __float2bfloat16_rn(tail[threadIdx.x]);
+  }
+  if (flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
+__global__ void bf16_to_f32_kernel(const uint2* __restrict__ x, float4* __restrict__ y, long long n4,
+                                   const __nv_bfloat16* tail, float* ytail, int ntail) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const uint2 v = __ldcs(x + i);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+    __stcs(y + i, make_float4(a.x, a.y, b.x, b.y));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < ntail) ytail[threadIdx.x] = __bfloat162float(tail[threadIdx.x]);
+}
+}  // namespace sa
+
+extern "C" int sa_f32_to_bf16(const float* x, void* y, long long count, int32_t* flag, void* stream) {
+  using namespace sa;
+  if (count < 0 || (count > 0 && (!x || !y))) return fail(SA_ERR_DIMENSION, "bad conversion arguments");
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 7))
+    return fail(SA_ERR_DIMENSION, "conversion buffers must be 16-byte (fp32) / 8-byte (bf16) aligned");
+  if (count == 0) return SA_OK;
+  const long long n4 = count / 4;
+  const int ntail = (int)(count - n4 * 4);
+  const int grid = (int)std::min<long long>(std::max<long long>((n4 + 255) / 256, 1), 4LL * device_sm_count());
+  f32_to_bf16_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float4*>(x), reinterpret_cast<uint2*>(y), n4, x + n4 * 4,
+      reinterpret_cast<__nv_bfloat16*>(y) + n4 * 4, ntail, flag);
+  return check_launch("f32_to_bf16_kernel");
+}
+
+extern "C" int sa_bf16_to_f32(const void* x, float* y, long long count, void* stream) {
+  using namespace sa;
+  if (count < 0 || (count > 0 && (!x || !y))) return fail(SA_ERR_DIMENSION, "bad conversion arguments");
+  if ((reinterpret_cast<uintptr_t>(x) & 7) || (reinterpret_cast<uintptr_t>(y) & 15))
+    return fail(SA_ERR_DIMENSION, "conversion buffers must be 8-byte (bf16) / 16-byte (fp32) aligned");
+  if (count == 0) return SA_OK;
+  const long long n4 = count / 4;
+  const int ntail = (int)(count - n4 * 4);
+  const int grid = (int)std::min<long long>(std::max<long long>((n4 + 255) / 256, 1), 4LL * device_sm_count());
+  bf16_to_f32_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint2*>(x), reinterpret_cast<float4*>(y), n4,
+      reinterpret_cast<const __nv_bfloat16*>(x) + n4 * 4, y + n4 * 4, ntail);
+  return check_launch("bf16_to_f32_kernel");
 }
 
 extern "C" int sa_memcpy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,

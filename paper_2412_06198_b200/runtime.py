@@ -440,6 +440,10 @@ def prefill(q, k, v, cfg: ModelConfig, search: SearchSpace | None = None, mode: 
             and not v.is_cuda and cfg.d_head == D.HEAD_DIM):
         return _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window, q_est,
                                       batch, length, kv_heads)
+    if (not D.is_torch(q) and not D.is_torch(k) and not D.is_torch(v) and cfg.d_head == D.HEAD_DIM
+            and all(np.asarray(x).dtype == np.float32 for x in (q, k, v))):
+        return _prefill_numpy_f32(q, k, v, cfg, search, mode, fixed_pattern, cal_window, q_est,
+                                  batch, length, kv_heads)
     t0 = time.perf_counter()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     ev[0].record()
@@ -489,6 +493,71 @@ def prefill(q, k, v, cfg: ModelConfig, search: SearchSpace | None = None, mode: 
     kernel_s = ev[2].elapsed_time(ev_end) / 1e3
     return PrefillResult(outputs=outputs, cache=cache, plans=plans, elapsed_s=elapsed,
                          select_s=select_s, kernel_s=kernel_s)
+
+
+def _prefill_numpy_f32(q, k, v, cfg, search, mode, fixed_pattern, cal_window, q_est, batch, length,
+                       kv_heads) -> PrefillResult:
+    """prefill for numpy float32 inputs (the reference's own call and types):
+    chunked pinned-staged H2D of the fp32 rows, one device pass converting them
+    to bf16 with AttnMatrices' finiteness check on the rows as given
+    (core.py:72-74), the layer, the KvCache kept in fp32 on the device (the
+    reference caches the rows as given, runtime.py:197) and a chunked D2H of
+    the fp32 output into a numpy array."""
+    dev = D.require_cuda()
+    t0 = time.perf_counter()
+    H, HK, n, d = cfg.n_heads, kv_heads, length, D.HEAD_DIM
+    st = D.stream()
+    qf = torch.empty((batch * H, n, d), dtype=torch.float32, device=dev)
+    cap = cfg.max_context
+    cache = KvCache(batch, H, d, cap, dtype=np.float32, kv_heads=HK)
+    if cap == n:  # the cache rows ARE the device copies of k / v
+        kf, vf = cache._k.view(batch * HK, n, d), cache._v.view(batch * HK, n, d)
+    else:
+        kf = torch.empty((batch * HK, n, d), dtype=torch.float32, device=dev)
+        vf = torch.empty((batch * HK, n, d), dtype=torch.float32, device=dev)
+    D.h2d_f32([(np.ascontiguousarray(k), kf), (np.ascontiguousarray(v), vf), (np.ascontiguousarray(q), qf)])
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    bf = torch.bfloat16
+    qd = torch.empty((batch * H, n, d), dtype=bf, device=dev)
+    kd = torch.empty((batch * HK, n, d), dtype=bf, device=dev)
+    vd = torch.empty((batch * HK, n, d), dtype=bf, device=dev)
+    for src, dst in ((qf, qd), (kf, kd), (vf, vd)):
+        _lib.call("sa_f32_to_bf16", src.data_ptr(), dst.data_ptr(), src.numel(), flag.data_ptr(), st)
+    if cap != n:  # rows [0, n) of each (batch, kv head) of the cache
+        for src, dst in ((kf, cache._k), (vf, cache._v)):
+            _lib.call("sa_memcpy2d_async", dst.data_ptr(), cap * d * 4, src.data_ptr(), n * d * 4, n * d * 4,
+                      batch * HK, st)
+    key = ("np", batch, H, HK, n, d, mode, repr(search), repr(fixed_pattern), cal_window, q_est)
+    plan = _PLAN_CACHE.get(key)
+    if plan is None:
+        plan = PrefillPlan(batch, H, HK, n, d, mode, search=search, fixed_pattern=fixed_pattern,
+                           cal_window=cal_window, q_est=q_est)
+        if len(_PLAN_CACHE) > 64:
+            _PLAN_CACHE.clear()
+        _PLAN_CACHE[key] = plan
+    ws = _workspace(plan.ws_bytes, dev)
+    out = torch.empty((batch, n, H * d), dtype=bf, device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    if mode == "auto":
+        plan.select(qd, kd, ws)
+    ev[1].record()
+    plan.run(qd, kd, vd, out, ws)
+    ev[2].record()
+    try:
+        plans = plan.plans(ws, flag=flag)  # raises before any output is returned
+    except NonFiniteError:
+        names = [nm for nm, x in (("q", qf), ("k", kf), ("v", vf)) if not bool(torch.isfinite(x).all())]
+        raise NonFiniteError(f"{names[0] if names else 'input'} contains NaN or Inf") from None
+    out32 = qf.view(-1)[: out.numel()].view(out.shape)  # q's fp32 staging is free again
+    _lib.call("sa_bf16_to_f32", out.data_ptr(), out32.data_ptr(), out.numel(), st)
+    outputs = np.empty((batch, n, H * d), dtype=np.float32)
+    D.d2h_f32(out32, outputs)
+    cache.length = n
+    cache._np = True
+    torch.cuda.synchronize()
+    return PrefillResult(outputs=outputs, cache=cache, plans=plans, elapsed_s=time.perf_counter() - t0,
+                         select_s=ev[0].elapsed_time(ev[1]) / 1e3, kernel_s=ev[1].elapsed_time(ev[2]) / 1e3)
 
 
 # tools/e2e_timeline.py sets this to a list to collect per-group stream event times (ms)
