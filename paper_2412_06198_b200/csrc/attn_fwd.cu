@@ -70,7 +70,8 @@ struct AttnArgs {
   __nv_bfloat16* peer_out[kMaxPeers];  // other ranks' outputs mapped over NVLink (fused all-gather)
 };
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 192;     // softmax WG + producer + MMA warp
+constexpr int kThreadsEwg = 384;  // + an epilogue WG (and two idle warps: warpgroup-aligned setmaxnreg)
 constexpr int kDefaultPoly = 4;
 #ifndef SA_PRODUCER_SLEEP_NS
 #define SA_PRODUCER_SLEEP_NS 64
@@ -80,6 +81,9 @@ constexpr int kDefaultPoly = 4;
 #endif
 // polling back-off of the producer / MMA warps (they share sub-partitions with softmax warps)
 constexpr int kProducerSleepNs = SA_PRODUCER_SLEEP_NS;
+#ifndef SA_EWG_SLEEP_NS
+#define SA_EWG_SLEEP_NS 256
+#endif
 constexpr int kMmaSleepNs = SA_MMA_SLEEP_NS;
 #ifdef SA_ATTN_PROF
 constexpr bool kProf = true;
@@ -100,7 +104,9 @@ constexpr int kSlotBytes = 16384;
 constexpr int kSmemQ = 0;
 constexpr int kSmemRing = 32768;
 constexpr int kSmemBar = kSmemRing + kRing * kSlotBytes;           // 114688
+constexpr int kSmemL = kSmemBar + 256;     // EWG: the row sums l of the item handed to the epilogue WG
 constexpr int kSmemBytes = kSmemBar + 256;  // + barriers; base is 1024-aligned (two CTAs per SM must fit)
+constexpr int kSmemBytesEwg = kSmemL + 512;
 
 enum Bar {
   B_Q = 0,                     // Q tile landed
@@ -114,7 +120,9 @@ enum Bar {
   B_OE = B_OF + 1,             // epilogue has read O
   B_IF0 = B_OE + 1,            // 2: work-item slot published
   B_IE0 = B_IF0 + 2,           // 2: work-item slot consumed
-  B_NUM = B_IE0 + 2
+  B_LF = B_IE0 + 2,            // EWG: row sums of the finished item in smem
+  B_LE = B_LF + 1,             // EWG: the epilogue WG has read them
+  B_NUM = B_LE + 1
 };
 
 // Work item idx -> (hh * nqt + qt): the caller's order (LPT), else kv-group-major
@@ -137,8 +145,15 @@ __device__ __forceinline__ int item_at(const AttnArgs& a, int idx) {
 //
 // POLY > 0: every POLY-th exp pair of a row chunk runs on the FMA pipe
 // (exp2_poly2) instead of MUFU, balancing the two pipes.
-template <int POLY>
-__global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnArgs a) {
+//
+// EWG: a fourth role, an epilogue warpgroup (warps 4-7), takes the finished
+// item's O out of TMEM, normalises, packs and stores it (and the peer copies)
+// while the softmax warps already run the next item; registers are
+// rebalanced with setmaxnreg (softmax 144, epilogue 56, producer / MMA 40).
+template <int POLY, bool EWG>
+__global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnArgs a) {
+  constexpr int kProdWarp = EWG ? 8 : 4;
+  constexpr int kMmaWarp = EWG ? 9 : 5;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem) & 1023u) != 0u) __trap();  // SWIZZLE_128B tiles need 1024-byte alignment
@@ -164,14 +179,16 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       mbar_init(&bars[B_SF0 + i], 1);
       mbar_init(&bars[B_PF0 + i], 128);
       mbar_init(&bars[B_IF0 + i], 1);
-      mbar_init(&bars[B_IE0 + i], 1 + 128);
+      mbar_init(&bars[B_IE0 + i], EWG ? 1 + 256 : 1 + 128);
     }
     mbar_init(&bars[B_OD], 1);
     mbar_init(&bars[B_OF], 1);
     mbar_init(&bars[B_OE], 128);
+    mbar_init(&bars[B_LF], 128);
+    mbar_init(&bars[B_LE], 128);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc(tmem_holder, kTmemCols);
+  if (warp == kMmaWarp) tmem_alloc(tmem_holder, kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -181,8 +198,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int n_items = a.n_work ? *a.n_work : a.hh_total * a.nqt;
 
-  if (warp == 4) {
+  if (warp == kProdWarp) {
     // ------------------------------------------------------------ producer
+    if constexpr (EWG) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     const int lane = lane_id();
     if (lane == 0) {
       tma_prefetch(&a.tmap_q);
@@ -271,8 +289,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       rb += 2 * nsub;
     }
     PT_FLUSH(32);
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
+    if constexpr (EWG) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     const bool leader = elect_one();
     constexpr uint32_t idesc_qk = idesc_bf16_f32(128, kSub, 0, 0);
     constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
@@ -349,8 +368,64 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     }
     (void)pb;
     PT_FLUSH(16);
-  } else {
+  } else if (EWG && warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ epilogue WG
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    const int r = threadIdx.x - 128;  // row of the tile = TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const volatile float* sL = reinterpret_cast<const volatile float*>(smem + kSmemL);
+    for (int J = 0;; ++J) {
+      mbar_wait_backoff<SA_EWG_SLEEP_NS>(&bars[B_IF0 + (J & 1)], (J >> 1) & 1);
+      const int item = sItem[J & 1];
+      mbar_arrive(&bars[B_IE0 + (J & 1)]);
+      if (item < 0) break;
+      const int hh = item / a.nqt, qt = item % a.nqt;
+      const int bidx = hh / a.heads, h = hh % a.heads;
+      const int i = qt * kTile + r;
+      const bool valid = i < a.n && a.tile_cnt[item] > 0;  // cnt == 0: query tile not requested
+      const long long ooff = (long long)bidx * a.out_batch_stride + (long long)i * a.out_row_stride +
+                             (long long)h * kHeadDim;
+      mbar_wait_backoff<SA_EWG_SLEEP_NS>(&bars[B_LF], J & 1);
+      const float inv = 1.0f / sL[r];
+      mbar_arrive(&bars[B_LE]);
+      mbar_wait_backoff<SA_EWG_SLEEP_NS>(&bars[B_OF], J & 1);
+      tc_fence_after();
+      __nv_bfloat16* orow = a.out + ooff;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tbase + lane_off + kColO + 32 * c, o);
+        tmem_ld_wait();
+        if (c == 3) {
+          tc_fence_before();
+          mbar_arrive(&bars[B_OE]);  // O may now be overwritten by the next item's PV(0)
+        }
+        if (valid) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            pk[t] = pack_bf16(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
+          auto store = [&](__nv_bfloat16* row) {
+            if (a.st256) {
+#pragma unroll
+              for (int t = 0; t < 2; ++t) st_global_v8(row + 32 * c + 16 * t, pk + 8 * t);
+            } else {
+              uint4* dst = reinterpret_cast<uint4*>(row + 32 * c);
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+            }
+          };
+          store(orow);
+#pragma unroll 1
+          for (int pr = 0; pr < a.n_peers; ++pr) store(a.peer_out[pr] + ooff);
+        }
+      }
+    }
+    if (a.n_peers > 0) __threadfence_system();  // peer stores drained before the CTA retires
+  } else if (warp < 4) {
     // ------------------------------------------------------------ softmax warps
+    if constexpr (EWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n" ::: "memory");
     const int r = threadIdx.x;  // 0..127
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     const float sl2 = a.scale_log2;
@@ -519,6 +594,18 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       }
       // ---------------------------------------------------------- epilogue
       fetch_item(J + 1);  // next item's loads in flight during this epilogue
+      if constexpr (EWG) {
+        // hand the row sum to the epilogue WG (its previous one has been read)
+        if (J >= 1) mbar_wait(&bars[B_LE], (J - 1) & 1);
+        reinterpret_cast<volatile float*>(smem + kSmemL)[r] = l;
+        mbar_arrive(&bars[B_LF]);
+        if (a.lse != nullptr && i < a.n && cur_cnt > 0)
+          a.lse[(size_t)hh * a.n + i] = (m_used + log2f(l)) * 0.69314718055994531f;
+        PT(9);
+        sb += nsub / 2;
+        pb += nsub;
+        continue;
+      }
       mbar_wait(&bars[B_OF], J & 1);
       PT(8);
       tc_fence_after();
@@ -569,11 +656,13 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     }
     if (kProf) pc[11] += clock64() - t_entry;
     PT_FLUSH(0);
-    if (a.n_peers > 0) __threadfence_system();  // peer stores drained before the CTA retires
+    if (!EWG && a.n_peers > 0) __threadfence_system();  // peer stores drained before the CTA retires
+  } else if (EWG) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");  // warps 10-11: idle
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc(tbase, kTmemCols);
+  if (warp == kMmaWarp) tmem_dealloc(tbase, kTmemCols);
 }
 
 }  // namespace sa
@@ -660,13 +749,21 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
     const int v = e ? atoi(e) : kDefaultPoly;
     return (v == 0 || v == 2 || v == 3 || v == 4 || v == 8) ? v : kDefaultPoly;
   }();
+  // SA_ATTN_EWG=1: an epilogue warpgroup takes the output stores off the
+  // softmax warps (384-thread CTAs).  Opt-in: measured slower (32K auto
+  // attention 0.869 vs 0.828 ms, Block(8,1) 0.217 vs 0.209, VS 8.0 vs 7.7;
+  // DESIGN.md), though removing the epilogue outright would save 4.6%.
+  static const bool ewg = [] {
+    const char* e = getenv("SA_ATTN_EWG");
+    return e && e[0] == '1';
+  }();
   static std::atomic<uint64_t> attr_done{0};
   once_per_device(attr_done, [] {
-    cudaFuncSetAttribute(attn_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    cudaFuncSetAttribute(attn_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    cudaFuncSetAttribute(attn_fwd_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    cudaFuncSetAttribute(attn_fwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    cudaFuncSetAttribute(attn_fwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+#define SA_ATTR(P)                                                                                           \
+  cudaFuncSetAttribute(attn_fwd_kernel<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes); \
+  cudaFuncSetAttribute(attn_fwd_kernel<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesEwg);
+    SA_ATTR(0) SA_ATTR(2) SA_ATTR(3) SA_ATTR(4) SA_ATTR(8)
+#undef SA_ATTR
   });
   // persistent: two CTAs per SM (113 KB shared memory and 256 TMEM columns each)
   const int num_sms = device_sm_count();
@@ -679,11 +776,11 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   // the need_weights path derives weights from lse: keep exact MUFU exps there
   void (*kern)(AttnArgs);
   switch (lse != nullptr ? 0 : poly) {
-    case 2: kern = attn_fwd_kernel<2>; break;
-    case 3: kern = attn_fwd_kernel<3>; break;
-    case 4: kern = attn_fwd_kernel<4>; break;
-    case 8: kern = attn_fwd_kernel<8>; break;
-    default: kern = attn_fwd_kernel<0>; break;
+    case 2: kern = ewg ? attn_fwd_kernel<2, true> : attn_fwd_kernel<2, false>; break;
+    case 3: kern = ewg ? attn_fwd_kernel<3, true> : attn_fwd_kernel<3, false>; break;
+    case 4: kern = ewg ? attn_fwd_kernel<4, true> : attn_fwd_kernel<4, false>; break;
+    case 8: kern = ewg ? attn_fwd_kernel<8, true> : attn_fwd_kernel<8, false>; break;
+    default: kern = ewg ? attn_fwd_kernel<0, true> : attn_fwd_kernel<0, false>; break;
   }
   // programmatic dependent launch: the CTAs become resident and run their
   // prologue (barriers, TMEM, tensor-map prefetch) while the previous kernel
@@ -695,8 +792,8 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   }();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.blockDim = dim3(ewg ? kThreadsEwg : kThreads);
+  cfg.dynamicSmemBytes = ewg ? kSmemBytesEwg : kSmemBytes;
   cfg.stream = cs;
   // highest scheduling priority: when a short-CTA kernel (the finiteness scan /
   // cache fill) runs beside it, freed SM slots go to attention CTAs first
