@@ -32,3 +32,13 @@ clean:
 	rm -rf build $(LIB)
 
 .PHONY: all clean prof
+
+# A/B variant: attention epilogue through a TMA-store stage (SA_ATTN_TMA_STORE=1)
+TMA_LIB := paper_2412_06198_b200/_sa_b200_tma.so
+build/tma/attn_fwd.o: paper_2412_06198_b200/csrc/attn_fwd.cu $(HDR)
+	@mkdir -p build/tma
+	$(NVCC) $(NVFLAGS) -DSA_ATTN_TMA_STORE=1 -c $< -o $@ 2> build/tma/attn_fwd.ptxas.txt || (cat build/tma/attn_fwd.ptxas.txt; false)
+$(TMA_LIB): build/tma/attn_fwd.o $(filter-out build/attn_fwd.o,$(OBJ))
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart_static
+tma: $(TMA_LIB)
+.PHONY: tma

@@ -70,6 +70,22 @@ int make_tmap_3d_bf16(CUtensorMap* map, const void* base, int d0, int d1, int d2
   return SA_OK;
 }
 
+// The attention output [B][n][row_stride] bf16 as a 3-D map {cols, n, B} with
+// box {64 cols, 128 rows, 1}: TMA stores clip rows past n inside each batch.
+int make_tmap_out_bf16(CUtensorMap* map, void* base, long long cols, int n, int batch, long long row_stride) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return fail(SA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)n, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)row_stride * 2, (cuuint64_t)row_stride * 2 * (cuuint64_t)n};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SA_ERR_CUDA, "cuTensorMapEncodeTiled (out) failed (%d)", (int)r);
+  return SA_OK;
+}
+
 // K/V viewed as [groups][n rows][2 d-halves][64] with the halves as the box's
 // outer dim: one box {64, 8, 2} = 8 rows x both halves = 2 KB, laid out in
 // shared memory as [half][8 rows][128 B] (two SWIZZLE_128B atoms).

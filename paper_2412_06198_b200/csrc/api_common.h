@@ -18,6 +18,7 @@ int fail(int status, const char* fmt, ...);
 // box {64, box_rows, 1}, 128-byte swizzle.
 int make_tmap_3d_bf16(CUtensorMap* map, const void* base, int d0, int d1, int d2, int box_rows);
 int make_tmap_kv_gather(CUtensorMap* map, const void* base, int n, int groups);
+int make_tmap_out_bf16(CUtensorMap* map, void* base, long long cols, int n, int batch, long long row_stride);
 
 inline int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();

@@ -66,6 +66,8 @@ struct AttnArgs {
   int st256;                 // output rows 32-byte aligned: 256-bit stores
   int skip_dead;             // warps whose 32 rows are all masked out of a sub-tile write P = 0 only
   int epi_mode;              // experiment (SA_ATTN_EPI): 1 = full epilogue, 0 = no global stores, 2 = no O read
+  CUtensorMap tmap_out;      // SA_ATTN_TMA_STORE: the output as {cols, n, B}, box {64, 128, 1}
+  int tma_out;               // use it (no peer copies, TMA-compatible layout)
   int n_peers;               // > 0: every output row is also stored into these buffers (same layout),
   __nv_bfloat16* peer_out[kMaxPeers];  // other ranks' outputs mapped over NVLink (fused all-gather)
 };
@@ -99,11 +101,18 @@ constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kColS = 0;    // S buffers at 0 and 64 (P aliased at their first 32 columns)
 constexpr uint32_t kColO = 128;
 constexpr int kSub = 64;         // keys per sub-tile
-constexpr int kRing = 5;         // K/V ring slots of 16 KB
+#ifndef SA_ATTN_TMA_STORE
+#define SA_ATTN_TMA_STORE 0
+#endif
+// SA_ATTN_TMA_STORE: the epilogue writes each 64-column half of the output tile
+// into a 16 KB shared-memory stage (taken from the K/V ring) and one thread
+// TMA-stores it, instead of 8 x 32-byte global stores per thread
+constexpr int kRing = SA_ATTN_TMA_STORE ? 4 : 5;  // K/V ring slots of 16 KB
 constexpr int kSlotBytes = 16384;
 constexpr int kSmemQ = 0;
 constexpr int kSmemRing = 32768;
-constexpr int kSmemBar = kSmemRing + kRing * kSlotBytes;           // 114688
+constexpr int kSmemStage = kSmemRing + kRing * kSlotBytes;          // TMA-store stage (1024-aligned)
+constexpr int kSmemBar = kSmemStage + (SA_ATTN_TMA_STORE ? 16384 : 0);  // 114688
 constexpr int kSmemL = kSmemBar + 256;     // EWG: the row sums l of the item handed to the epilogue WG
 constexpr int kSmemBytes = kSmemBar + 256;  // + barriers; base is 1024-aligned (two CTAs per SM must fit)
 constexpr int kSmemBytesEwg = kSmemL + 512;
@@ -611,6 +620,45 @@ __global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kern
       tc_fence_after();
       const float inv = 1.0f / l;
       const bool valid = i < a.n && cur_cnt > 0;  // cnt == 0: query tile not requested
+      if (SA_ATTN_TMA_STORE && a.tma_out) {
+        // two 64-column halves through the swizzled stage; rows past n are
+        // clipped by the TMA box bounds
+        uint8_t* stage = smem + kSmemStage;
+        const uint32_t st_addr = smem_u32(stage) + (uint32_t)r * 128u;
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+          if (r == 0) bulk_wait_read0();  // the previous store has read the stage
+          named_bar_sync(1, 128);
+          uint32_t o[2][32];
+          tmem_ld32(tbase + lane_off + kColO + 64 * hf, o[0]);
+          tmem_ld32(tbase + lane_off + kColO + 64 * hf + 32, o[1]);
+          tmem_ld_wait();
+          if (hf == 1) {
+            tc_fence_before();
+            mbar_arrive(&bars[B_OE]);  // O may now be overwritten by the next item's PV(0)
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t w[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              w[t] = pack_bf16(__uint_as_float(o[j >> 2][(j & 3) * 8 + 2 * t]) * inv,
+                               __uint_as_float(o[j >> 2][(j & 3) * 8 + 2 * t + 1]) * inv);
+            st_shared_v4(st_addr + ((uint32_t)(j ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
+          }
+          fence_proxy_async();
+          named_bar_sync(1, 128);
+          if (r == 0 && cur_cnt > 0) {
+            tma_store_3d(&a.tmap_out, stage, h * kHeadDim + 64 * hf, qt * kTile, bidx);
+            bulk_commit();
+          }
+        }
+        if (valid && a.lse != nullptr) a.lse[(size_t)hh * a.n + i] = (m_used + log2f(l)) * 0.69314718055994531f;
+        PT(9);
+        sb += nsub / 2;
+        pb += nsub;
+        continue;
+      }
       const long long ooff = (long long)bidx * a.out_batch_stride + (long long)i * a.out_row_stride +
                              (long long)h * kHeadDim;
       __nv_bfloat16* orow = a.out + ooff;
@@ -654,6 +702,7 @@ __global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kern
       sb += nsub / 2;
       pb += nsub;
     }
+    if (SA_ATTN_TMA_STORE && a.tma_out && r == 0) bulk_wait0();  // every output store complete
     if (kProf) pc[11] += clock64() - t_entry;
     PT_FLUSH(0);
     if (!EWG && a.n_peers > 0) __threadfence_system();  // peer stores drained before the CTA retires
@@ -729,6 +778,10 @@ int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const vo
   a.heads = heads;
   a.kv_heads = kv_heads;
   a.nqt = (n + kTile - 1) / kTile;
+  if (SA_ATTN_TMA_STORE && n_peers == 0) {
+    if ((st = make_tmap_out_bf16(&a.tmap_out, out, a.out_row_stride, n, batch, a.out_row_stride))) return st;
+    a.tma_out = 1;
+  }
   a.hh_total = batch * heads;
   a.scale_log2 = scale * 1.4426950408889634f;
   a.tile_off = tile_off;
