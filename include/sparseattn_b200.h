@@ -84,8 +84,10 @@ typedef struct {
   int32_t ncand;         /* SA_MODE_AUTO: 1..SA_MAX_CAND                     */
   sa_pattern cand[SA_MAX_CAND];
   sa_pattern full[SA_MAX_CAND];
-  int32_t preselected;   /* SA_MODE_AUTO: 1 = the caller already wrote the
-                            per-head choice into view.choice (skip the selector) */
+  int32_t preselected;   /* SA_MODE_AUTO: 0 = run the selector inside
+                            sa_prefill; 1 = the caller already wrote the per-head
+                            choice into view.choice; 2 = sa_prefill_select already
+                            selected and applied it (same workspace) */
   void* stage_events[6]; /* optional cudaEvent_t, recorded on `stream` after:
                             [0] selection, [1] VS estimator + top-k, [2] block
                             estimator, [3] tile lists, [4] attention, [5] unused */
@@ -130,6 +132,12 @@ int sa_version(void);
 /* ---- the whole path: runtime.prefill (runtime.py:134-206) --------------- */
 size_t sa_prefill_workspace_size(const sa_prefill_desc* desc);
 int sa_prefill_views(const sa_prefill_desc* desc, void* ws, sa_prefill_view* view);
+/* The per-head selection of an SA_MODE_AUTO layer alone (search.py:276-319):
+ * the windowed selector writes view.choice / view.errors and the chosen
+ * patterns' per-head parameters; a following sa_prefill with preselected = 2
+ * on the same workspace skips its own selection. */
+int sa_prefill_select(const sa_prefill_desc* desc, const void* q, const void* k, void* ws, size_t ws_bytes,
+                      void* stream);
 int sa_prefill(const sa_prefill_desc* desc, const void* q, const void* k, const void* v,
                void* out, void* ws, size_t ws_bytes, void* stream);
 

@@ -106,6 +106,7 @@ _SIGNATURES = {
     "sa_prefill_workspace_size": (_SZ, [_DESC]),
     "sa_prefill_views": (ctypes.c_int, [_DESC, _P, ctypes.POINTER(sa_prefill_view)]),
     "sa_prefill": (ctypes.c_int, [_DESC, _P, _P, _P, _P, _P, _SZ, _P]),
+    "sa_prefill_select": (ctypes.c_int, [_DESC, _P, _P, _P, _SZ, _P]),
     "sa_select_windowed": (ctypes.c_int, [_I, _I, _I, _I, _I, _F, _P, _P, _I, _P, _P, _P, _P, _P,
                                           _P, _P]),
     "sa_score_tail_workspace": (_SZ, [_I, _I, _I, _I]),

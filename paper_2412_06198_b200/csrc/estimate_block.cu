@@ -103,7 +103,8 @@ struct BlockScoreArgs {
   int b;                 // block side (stored in the index)
   // FUSED output: fixed-stride rows of (k_b + 1) slots, INT32_MAX padded
   int32_t* blk_idx;      // per head at hh * head_stride: [nb, k_b + 1]
-  int32_t* blk_row_off;  // per head at hh * row_stride: [nb + 1] (absolute offsets into blk_idx)
+  int32_t* blk_row_off;  // per head at hh * row_stride: [nb + 1] (absolute offsets into blk_idx); FUSED
+                         // rows write their own (no separate row-offset kernel)
   long long head_stride;
   int row_stride;
   // MATERIALIZE output
@@ -333,6 +334,9 @@ __global__ void __launch_bounds__(kBsThreads, 2) block_score_kernel(const __grid
       const int stride = a.k_b + 1;
       int32_t* dst = a.blk_idx + (size_t)hh * a.head_stride + (size_t)gq * stride;
       for (int q = 0; q < stride; ++q) dst[q] = q < m ? ids[q] : INT_MAX;
+      int32_t* ro = a.blk_row_off + (size_t)hh * a.row_stride;
+      ro[gq] = (int32_t)(hh * a.head_stride + (long long)gq * stride);
+      if (gq == a.nb - 1) ro[a.nb] = (int32_t)(hh * a.head_stride + (long long)a.nb * stride);
     }
   }
   tc_fence_before();
@@ -465,12 +469,9 @@ int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_
   a.row_stride = row_stride;
   a.gate = gate;
   a.gate_val = gate_val;
-  {
-    const long long tot = (long long)hh_total * (nb + 1);
-    fixed_row_off_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        blk_row_off, hh_total, nb, k_b + 1, row_stride, head_stride, gate, gate_val);
-    if ((rc = check_launch("fixed_row_off_kernel"))) return rc;
-  }
+  if (k_b > 8 && (rc = launch_fixed_row_off(blk_row_off, hh_total, nb, k_b + 1, row_stride, head_stride, gate,
+                                              gate_val, st)))
+    return rc;  // (the fused k_b <= 8 kernel writes its rows' offsets itself)
   static std::atomic<uint64_t> attr_done{0};
   once_per_device(attr_done, [] {
     cudaFuncSetAttribute(block_score_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBsSmemBytes);

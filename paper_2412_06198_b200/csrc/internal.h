@@ -103,10 +103,21 @@ int launch_block_select(int batch, int heads, int kv_heads, int n, int b, int k_
                         const void* qp, const void* kp, int32_t* blk_idx, long long head_stride,
                         int32_t* blk_row_off, int row_stride, const int32_t* gate, int gate_val,
                         void* ws, size_t ws_bytes, cudaStream_t st);
+// sa_prefill's use of the selector: the last CTA of each head takes the
+// argmin and writes the chosen full-length pattern's per-head parameters (no
+// separate argmin / apply kernels); counter: [HH] ints, zeroed by launch_select
+struct SelectApply {
+  sa_pattern full[SA_MAX_CAND];
+  int32_t* family;
+  int32_t* tri_w;
+  int32_t* tri_s;
+  int32_t* blk_b;
+  int* counter;
+};
 int launch_select(int batch, int heads, int kv_heads, int n, int cal, float scale, const void* q,
                   const void* k, int ncand, const int32_t* cand_fam, const int32_t* cand_p1,
                   const int32_t* cand_p2, int32_t* choice_out, int32_t* family_out,
-                  double* err_out, cudaStream_t stream);
+                  double* err_out, cudaStream_t stream, const SelectApply* apply = nullptr);
 
 int launch_attn(int batch, int heads, int kv_heads, int n, float scale, const void* q, const void* k,
                 const void* v, void* out, const sa_head_index* index, const int32_t* tile_off,

@@ -63,7 +63,7 @@ struct Layout {
 enum WsSlot {
   W_CHOICE = 0, W_FAMILY, W_ERR, W_TRIW, W_TRIS, W_COLBITS, W_DIAGREV, W_COLSC, W_DIAGSC,
   W_COLIDX, W_DIAGIDX, W_TAIL, W_BLKB, W_ROWOFF, W_BLKIDX, W_QP, W_KP, W_BLKWS,
-  W_TOFF, W_TCNT, W_TILES, W_WORK, W_NUM
+  W_TOFF, W_TCNT, W_TILES, W_WORK, W_SELCNT, W_NUM
 };
 
 struct Plan {
@@ -212,6 +212,7 @@ static int make_plan(const sa_prefill_desc* d, Plan* p, Layout* L) {
   sz[W_TCNT] = hh * p->nqt * 4;
   sz[W_TILES] = hh * (size_t)p->nqt * (p->nqt + 1) / 2 * 4;
   sz[W_WORK] = (64 + hh * p->nqt) * 4;  // [counter, item count], then the work order
+  sz[W_SELCNT] = hh * 4;                // selector: candidate CTAs finished per head
   size_t o = 0;
   for (int i = 0; i < W_NUM; ++i) {
     L->off[i] = o;
@@ -288,6 +289,42 @@ extern "C" int sa_prefill_views(const sa_prefill_desc* desc, void* ws, sa_prefil
   return SA_OK;
 }
 
+// The windowed selector (search.py:276-319) over the refined candidates, its
+// last CTA per head taking the argmin and writing the chosen full-length
+// pattern's per-head parameters into the workspace views.
+static int select_apply(const sa_prefill_desc* desc, const Plan& p, const Layout& L, const sa_prefill_view& V,
+                        char* b, const void* q, const void* k, cudaStream_t st) {
+  int32_t fam[SA_MAX_CAND], p1[SA_MAX_CAND], p2[SA_MAX_CAND];
+  for (int c = 0; c < p.ncand; ++c) {
+    fam[c] = desc->cand[c].family;
+    p1[c] = desc->cand[c].p1;
+    p2[c] = desc->cand[c].p2;
+  }
+  SelectApply ap{};
+  for (int c = 0; c < p.ncand; ++c) ap.full[c] = p.cand[c];
+  ap.family = V.family;
+  ap.tri_w = const_cast<int32_t*>(V.index.tri_window);
+  ap.tri_s = const_cast<int32_t*>(V.index.tri_sinks);
+  ap.blk_b = const_cast<int32_t*>(V.index.blk_b);
+  ap.counter = reinterpret_cast<int*>(b + L.off[W_SELCNT]);
+  return launch_select(desc->batch, desc->heads, desc->kv_heads, p.n, std::min(desc->cal, p.n), desc->scale, q, k,
+                       p.ncand, fam, p1, p2, V.choice, nullptr, V.errors, st, &ap);
+}
+
+extern "C" int sa_prefill_select(const sa_prefill_desc* desc, const void* q, const void* k, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  Plan p;
+  Layout L;
+  int rc;
+  if ((rc = make_plan(desc, &p, &L))) return rc;
+  if (desc->mode != SA_MODE_AUTO) return fail(SA_ERR_SEARCH, "sa_prefill_select needs SA_MODE_AUTO");
+  if (!q || !k || !ws) return fail(SA_ERR_DIMENSION, "null pointer argument");
+  if (ws_bytes < L.total) return fail(SA_ERR_DIMENSION, "workspace too small (%zu < %zu)", ws_bytes, L.total);
+  sa_prefill_view V;
+  sa_prefill_views(desc, ws, &V);
+  return select_apply(desc, p, L, V, reinterpret_cast<char*>(ws), q, k, reinterpret_cast<cudaStream_t>(stream));
+}
+
 extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void* k, const void* v,
                           void* out, void* ws, size_t ws_bytes, void* stream) {
   Plan p;
@@ -361,24 +398,15 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
     if (rc) return rc;
     cudaEventRecord(side->kdone, side->s);
   }
-  // 1. per-head choice
+  // 1. per-head choice: preselected 0 = the selector runs here (its last CTA
+  // per head applies the choice), 2 = sa_prefill_select already did that,
+  // 1 = the caller wrote view.choice (composed wide-window selection): apply it
   int32_t* choice = nullptr;
-  if (desc->mode == SA_MODE_AUTO && desc->preselected) {
+  if (desc->mode == SA_MODE_AUTO) {
     choice = V.choice;
-  } else if (desc->mode == SA_MODE_AUTO) {
-    choice = V.choice;
-    int32_t fam[SA_MAX_CAND], p1[SA_MAX_CAND], p2[SA_MAX_CAND];
-    for (int c = 0; c < p.ncand; ++c) {
-      fam[c] = desc->cand[c].family;
-      p1[c] = desc->cand[c].p1;
-      p2[c] = desc->cand[c].p2;
-    }
-    const int cal = std::min(desc->cal, n);
-    if ((rc = launch_select(B, H, HK, n, cal, desc->scale, q, k, p.ncand, fam, p1, p2, choice,
-                            nullptr, V.errors, st)))
-      return rc;
+    if (desc->preselected == 0 && (rc = select_apply(desc, p, L, V, b, q, k, st))) return rc;
   }
-  {
+  if (desc->mode != SA_MODE_AUTO || desc->preselected == 1) {
     ApplyArgs a{};
     a.hh = p.hh;
     a.ncand = p.ncand;

@@ -43,6 +43,8 @@ struct SelectArgs {
   int32_t* choice_out;  // [HH] index of the chosen candidate
   int32_t* family_out;  // [HH] family of the chosen candidate (optional)
   double* err_out;      // [HH, SA_MAX_CAND] Frobenius errors (optional)
+  int apply;            // SelectApply below is set
+  SelectApply ap;
 };
 
 struct SelectSmem {
@@ -295,6 +297,32 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     double tot = 0.0;
     for (int w = 0; w < kWarps; ++w) tot += S.red[w];
     a.err_out[(size_t)hh * SA_MAX_CAND + ci] = sqrt(tot);
+    if (a.apply) {
+      // the head's last candidate CTA: strict-< argmin in candidate order
+      // (search.py:245-250; NaN never wins, all-NaN -> candidate 0) and the
+      // chosen pattern's per-head parameters (what apply_choice_kernel writes)
+      __threadfence();
+      if (atomicAdd(&a.ap.counter[hh], 1) == a.ncand - 1) {
+        a.ap.counter[hh] = 0;
+        __threadfence();
+        double best = INFINITY;
+        int bc = 0;
+        for (int c = 0; c < a.ncand; ++c) {
+          const double e = __ldcg(&a.err_out[(size_t)hh * SA_MAX_CAND + c]);
+          if (e < best) {
+            best = e;
+            bc = c;
+          }
+        }
+        a.choice_out[hh] = bc;
+        if (a.family_out) a.family_out[hh] = a.cand_fam[bc];
+        const sa_pattern pf = a.ap.full[bc];
+        a.ap.family[hh] = pf.family;
+        a.ap.tri_w[hh] = pf.family == SA_TRIANGULAR ? pf.p1 : 1;
+        a.ap.tri_s[hh] = pf.family == SA_TRIANGULAR ? pf.p2 : 0;
+        a.ap.blk_b[hh] = pf.family == SA_BLOCK_SPARSE ? pf.p1 : 1;
+      }
+    }
   }
 }
 
@@ -325,7 +353,7 @@ namespace sa {
 int launch_select(int batch, int heads, int kv_heads, int n, int cal, float scale, const void* q,
                   const void* k, int ncand, const int32_t* cand_fam, const int32_t* cand_p1,
                   const int32_t* cand_p2, int32_t* choice_out, int32_t* family_out,
-                  double* err_out, cudaStream_t stream) {
+                  double* err_out, cudaStream_t stream, const SelectApply* apply) {
   if (batch < 1 || heads < 1 || kv_heads < 1 || heads % kv_heads)
     return fail(SA_ERR_DIMENSION, "bad head layout");
   if (cal < 1 || cal > n) return fail(SA_ERR_SEARCH, "cal_window must be in [1, %d], got %d", n, cal);
@@ -371,9 +399,15 @@ int launch_select(int batch, int heads, int kv_heads, int n, int cal, float scal
     }
     a.err_out = s.p;
   }
+  if (apply) {
+    if (!choice_out || !apply->counter) return fail(SA_ERR_DIMENSION, "selector apply needs choice and counter");
+    a.apply = 1;
+    a.ap = *apply;
+    cudaMemsetAsync(apply->counter, 0, (size_t)a.hh_total * sizeof(int), stream);
+  }
   select_kernel<<<dim3(a.hh_total, ncand), kSelThreads, sizeof(SelectSmem), stream>>>(a);
   int rc = check_launch("select_kernel");
-  if (rc) return rc;
+  if (rc || apply) return rc;
   CandFamilies fams{};
   for (int c = 0; c < ncand; ++c) fams.f[c] = a.cand_fam[c];
   select_argmin_kernel<<<(a.hh_total + 127) / 128, 128, 0, stream>>>(a.err_out, a.hh_total, ncand, choice_out,

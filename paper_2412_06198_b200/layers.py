@@ -90,7 +90,9 @@ class LayerStack:
         if p.mode == "auto":
             hh = p.hh
             self.choice[l].copy_(self._ws_view(self.view.choice, hh, torch.int32))
-            self.errors[l].copy_(self._ws_view(self.view.errors, hh * _lib.MAX_CAND, torch.float64))
+            nc = len(p.refined)  # only the written columns of the error table
+            self.errors[l].view(hh, _lib.MAX_CAND)[:, :nc].copy_(
+                self._ws_view(self.view.errors, hh * _lib.MAX_CAND, torch.float64).view(hh, _lib.MAX_CAND)[:, :nc])
 
     def _ws_view(self, ptr: int, count: int, dtype) -> torch.Tensor:
         off = ptr - self.ws.data_ptr()

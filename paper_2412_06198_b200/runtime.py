@@ -248,17 +248,15 @@ class PrefillPlan:
 
     def select(self, q: torch.Tensor, k: torch.Tensor, ws: torch.Tensor) -> None:
         """Per-head selection into the workspace's choice slot (auto mode)."""
-        v = self.views(ws)
         if self.cal <= SELECTOR_CAL_MAX:
-            fam = (_ct_i32 * _lib.MAX_CAND)()
-            p1 = (_ct_i32 * _lib.MAX_CAND)()
-            p2 = (_ct_i32 * _lib.MAX_CAND)()
-            for c, rc in enumerate(self.refined):
-                fam[c], p1[c], p2[c] = pattern_params(rc.pattern)
-            _lib.call("sa_select_windowed", self.batch, self.heads, self.kv_heads, self.length, self.cal,
-                      self.scale, q.data_ptr(), k.data_ptr(), len(self.refined), fam, p1, p2, v.choice,
-                      None, v.errors, D.stream())
+            # the device selector; its last CTA per head applies the choice, so
+            # sa_prefill (preselected = 2) starts straight at the estimators
+            self.desc.preselected = 2
+            _lib.call("sa_prefill_select", self.desc, q.data_ptr(), k.data_ptr(), ws.data_ptr(), ws.numel(),
+                      D.stream())
             return
+        self.desc.preselected = 1
+        v = self.views(ws)
         # wide calibration windows: composed device selection per head, the
         # weights in fp32 like the reference's (search.py:242-250); every
         # candidate's error lands in the error rows like the selector kernel's
@@ -317,8 +315,10 @@ class PrefillPlan:
         v = self.views(ws)
         hh = self.hh
         parts = [] if flag is None else [flag.double()]
-        if self.mode == "auto":
-            parts += [_wrap(v.choice, hh, torch.int32).double(), _wrap(v.errors, hh * _lib.MAX_CAND, torch.float64)]
+        nc = len(self.refined) if self.mode == "auto" else 0
+        if self.mode == "auto":  # only the written error columns (the rest of the table is scratch)
+            errs_dev = _wrap(v.errors, hh * _lib.MAX_CAND, torch.float64).view(hh, _lib.MAX_CAND)[:, :nc]
+            parts += [_wrap(v.choice, hh, torch.int32).double(), errs_dev.reshape(-1)]
         small = torch.cat(parts).cpu().numpy() if parts else None
         if flag is not None:
             if int(small[0]):
@@ -327,7 +327,7 @@ class PrefillPlan:
         if self.mode != "auto":
             return self.plans_from(None, None, self.batch, self.heads, with_search)
         choice = small[:hh].astype(np.int64)
-        errs = small[hh:].reshape(hh, _lib.MAX_CAND)
+        errs = small[hh:].reshape(hh, nc)
         return self.plans_from(choice, errs, self.batch, self.heads, with_search)
 
     def plans_from(self, choice, errs, batch: int, heads: int, with_search: bool = True):
@@ -605,7 +605,8 @@ def _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window
     view = plan.views(ws)
     auto = mode == "auto"
     choice_all = torch.zeros(batch * H, dtype=torch.int32, device=dev)
-    err_all = torch.zeros((batch * H, _lib.MAX_CAND), dtype=torch.float64, device=dev)
+    nc = len(plan.refined) if auto else 0
+    err_all = torch.zeros((batch * H, max(nc, 1)), dtype=torch.float64, device=dev)
     cache = KvCache(batch, H, d, cfg.max_context, dtype=k.dtype, kv_heads=HK)
     comp = torch.cuda.current_stream()
     h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
@@ -640,7 +641,7 @@ def _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window
         plan.run(qg, kg, vg, og, ws)
         if auto:
             choice_all[h0:h0 + g].copy_(_wrap(view.choice, g, torch.int32))
-            err_all[h0:h0 + g].copy_(_wrap(view.errors, g * _lib.MAX_CAND, torch.float64).view(g, _lib.MAX_CAND))
+            err_all[h0:h0 + g].copy_(_wrap(view.errors, g * _lib.MAX_CAND, torch.float64).view(g, _lib.MAX_CAND)[:, :nc])
         cache._k[b, kh, :n].copy_(kd[grp])
         cache._v[b, kh, :n].copy_(vd[grp])
         done = torch.cuda.Event(enable_timing=tl is not None)
@@ -669,7 +670,7 @@ def _prefill_host_streamed(q, k, v, cfg, search, mode, fixed_pattern, cal_window
         cache._v[:, :, :n].copy_(v)
     if auto:
         nh = batch * H
-        plans = plan.plans_from(small[1:1 + nh].astype(np.int64), small[1 + nh:].reshape(nh, _lib.MAX_CAND), batch, H)
+        plans = plan.plans_from(small[1:1 + nh].astype(np.int64), small[1 + nh:].reshape(nh, nc), batch, H)
     else:
         plans = plan.plans_from(None, None, batch, H)
     select_s = sum(a.elapsed_time(z) for a, z in sel) / 1e3
