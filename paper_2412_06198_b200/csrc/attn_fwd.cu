@@ -124,8 +124,7 @@ enum Bar {
   B_EMPTY0 = B_FULL0 + kRing,  // kRing
   B_SF0 = B_EMPTY0 + kRing,    // 2
   B_PF0 = B_SF0 + 2,           // 2
-  B_OD = B_PF0 + 2,            // O updated by PV(u)
-  B_OF = B_OD + 1,             // final O of the item
+  B_OF = B_PF0 + 2,            // final O of the item
   B_OE = B_OF + 1,             // epilogue has read O
   B_IF0 = B_OE + 1,            // 2: work-item slot published
   B_IE0 = B_IF0 + 2,           // 2: work-item slot consumed
@@ -190,7 +189,6 @@ __global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kern
       mbar_init(&bars[B_IF0 + i], 1);
       mbar_init(&bars[B_IE0 + i], EWG ? 1 + 256 : 1 + 128);
     }
-    mbar_init(&bars[B_OD], 1);
     mbar_init(&bars[B_OF], 1);
     mbar_init(&bars[B_OE], 128);
     mbar_init(&bars[B_LF], 128);
@@ -310,9 +308,14 @@ __global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kern
     int rb = 0, sb = 0, pb = 0;  // ring items, S-buffer uses (per buffer), PV commits so far
     for (int J = 0;; ++J) {
       mbar_wait_backoff<kMmaSleepNs>(&bars[B_IF0 + (J & 1)], (J >> 1) & 1);
-      const int item = sItem[J & 1];
-      __syncwarp();
-      if (leader) mbar_arrive(&bars[B_IE0 + (J & 1)]);
+      // the elected lane reads the slot and releases it; the warp gets the item
+      // by shuffle (every read of the slot precedes its own release)
+      int item = 0;
+      if (leader) {
+        item = sItem[J & 1];
+        mbar_arrive(&bars[B_IE0 + (J & 1)]);
+      }
+      item = __shfl_sync(0xffffffffu, item, __ffs(__ballot_sync(0xffffffffu, leader)) - 1);
       if (item < 0) break;
       const int nsub = 2 * a.tile_cnt[item];
       if (leader) {
@@ -362,8 +365,7 @@ __global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kern
             mma_ts(tbase + kColO, p_addr + kk * 8, sdesc_sw128(v_addr + kk * v_step, v_lbo, v_sbo),
                    idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&bars[B_EMPTY0 + slot]);
-          mma_commit(&bars[B_OD]);
+          mma_commit(&bars[B_EMPTY0 + slot]);  // also "PV(u) has updated O" for a rescaling softmax
           PT(6);
           if (kProf) pc[15] += 1;
           if (u + 2 < nsub) issue_qk(u + 2);
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kern
     const float sl2 = a.scale_log2;
     PT_INIT
     if (kProf) { pc[10] += pt_last - t_entry; pc[12] += 1; }
-    int sb = 0, pb = 0;
+    int sb = 0, pb = 0, rb = 0;  // S-buffer uses, PV count, ring positions (as the MMA warp counts them)
     // The next item's descriptor, row constants and first tile entries are
     // loaded before the current item's epilogue, hiding their latency.
     int item, cnt;
@@ -545,8 +547,12 @@ __global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kern
           const float alpha = need ? fast_exp2(m_used - mt) : 1.0f;  // 0 when m_used == -inf
           l *= alpha;
           if (u > 0) {
-            // PV(u-1) may still be accumulating into O (PV(u-2) completed before S_u)
-            mbar_wait(&bars[B_OD], (pb + u - 1) & 1);
+            // PV(u-1) may still be accumulating into O (PV(u-2) completed before
+            // S_u): wait for the commit that releases V(u-1)'s ring slot.  That
+            // slot cannot complete another phase before P(u) exists (its next
+            // reader, QK(u+2), is issued after PV(u)), so the parity is exact.
+            const int gv = rb + 2 * (u - 1) + 1;
+            mbar_wait(&bars[B_EMPTY0 + gv % kRing], (gv / kRing) & 1);
             tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < 4; ++c) {
@@ -613,6 +619,7 @@ __global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kern
         PT(9);
         sb += nsub / 2;
         pb += nsub;
+        rb += 2 * nsub;
         continue;
       }
       mbar_wait(&bars[B_OF], J & 1);
@@ -657,6 +664,7 @@ __global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kern
         PT(9);
         sb += nsub / 2;
         pb += nsub;
+        rb += 2 * nsub;
         continue;
       }
       const long long ooff = (long long)bidx * a.out_batch_stride + (long long)i * a.out_row_stride +
@@ -701,6 +709,7 @@ __global__ void __launch_bounds__(EWG ? kThreadsEwg : kThreads, 2) attn_fwd_kern
       PT(9);
       sb += nsub / 2;
       pb += nsub;
+      rb += 2 * nsub;
     }
     if (SA_ATTN_TMA_STORE && a.tma_out && r == 0) bulk_wait0();  // every output store complete
     if (kProf) pc[11] += clock64() - t_entry;
