@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-128k", action="store_true", help="skip the 131072-token sub-record")
     ap.add_argument("--no-est", action="store_true", help="skip the all-VS estimator roofline block")
     ap.add_argument("--no-ttft", action="store_true", help="skip the 32-layer 64K TTFT sub-record")
+    ap.add_argument("--no-c5", action="store_true", help="skip the 16K-128K context sweep against dense SDPA")
     ap.add_argument("--ttft-layers", type=int, default=32)
     ap.add_argument("--ttft-ctx", type=int, default=65536)
     return ap.parse_args()
@@ -765,6 +766,12 @@ def run_ours(args):
     ttft = None
     if not args.no_ttft:
         ttft = run_ttft(args, world, rank, dev)
+    c5 = None
+    if world == 1 and not args.no_c5 and args.mode == "auto" and args.pattern is None:
+        known = {n: round(ms, 4)}
+        if sub128 is not None:
+            known[131072] = sub128["value"]
+        c5 = c5_sweep(args, R, make_fixed, dev, known)
 
     if rank == 0:
         fam_counts = {f: fams.count(f) for f in sorted(set(fams))}
@@ -801,6 +808,7 @@ def run_ours(args):
             "ctx_131072": sub128,
             "estimator_roofline": est,
             "ttft_c4": ttft,
+            "c5_sweep": c5,
         }
         print(json.dumps(line), flush=True)
     if peer is not None:
@@ -922,6 +930,73 @@ def run_sub_layer(args, R, make_fixed, n, dev):
             "stage_ms": {k2: round(float(x), 4) for k2, x in zip(
                 ["select", "vs_estimator", "block_estimator", "tile_lists", "attention"], stage_ms[:5])},
             "e2e": e2e, "clocks": sampler.summary() if sampler else None, "l2": l2_note(n)}
+
+
+def sdpa_dense_ms(n, dev, reps=3):
+    """Dense causal attention of the same shape by torch SDPA (cuDNN on B200, the
+    best installed dense kernel here: profiles/r02/dense_baseline_32k.txt),
+    library code timed for comparison only."""
+    import torch
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    q = torch.rand((1, H, n, D), generator=g, device=dev).bfloat16()
+    k = torch.rand((1, HK, n, D), generator=g, device=dev).bfloat16()
+    v = torch.rand((1, HK, n, D), generator=g, device=dev).bfloat16()
+    f = lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)  # noqa: E731
+    f()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    del q, k, v
+    torch.cuda.empty_cache()
+    return e0.elapsed_time(e1) / reps
+
+
+def c5_sweep(args, R, make_fixed, dev, known):
+    """BASELINE configs[4] on one GPU: the auto layer at 16K-128K (graph replay,
+    the same synthetic draw as the headline; 32K / 128K reuse the lines above)
+    against dense causal SDPA, and the TTFT growth gradient (least-squares ms
+    per 1K tokens over the sweep, reference bench.py:336-378)."""
+    import torch
+
+    rows = []
+    for n in (16384, 32768, 65536, 131072):
+        ms = known.get(n)
+        if ms is None:
+            mode, fixed = make_fixed(n)
+            q, k, v = synth_inputs(args.seed, n)
+            qd, kd, vd = (torch.from_numpy(x).bfloat16().to(dev) for x in (q, k, v))
+            del q, k, v
+            plan = R.PrefillPlan(1, H, HK, n, D, mode, fixed_pattern=fixed)
+            ws = R._workspace(plan.ws_bytes, dev)
+            out = torch.empty((1, n, H * D), dtype=torch.bfloat16, device=dev)
+            flag = torch.zeros(1, dtype=torch.int32, device=dev)
+            cache_k = torch.empty((HK, n, D), dtype=torch.bfloat16, device=dev)
+            cache_v = torch.empty((HK, n, D), dtype=torch.bfloat16, device=dev)
+            for _ in range(2):
+                if plan.mode == "auto":
+                    plan.select(qd, kd, ws)
+                plan.run(qd, kd, vd, out, ws)
+            graph = layer_graph(plan, qd, kd, vd, out, ws, flag, cache_k, cache_v)
+            ms, _ = time_graph(graph, 5, torch.cuda.current_device(), clocks=False)
+            plan.desc.check_flag = None
+            plan.desc.cache_k = plan.desc.cache_v = None
+            plan.desc.cache_capacity = 0
+            del graph, qd, kd, vd, out, cache_k, cache_v
+            torch.cuda.empty_cache()
+            ms = round(ms, 4)
+        dn = sdpa_dense_ms(n, dev)
+        rows.append({"ctx": n, "auto_ms": ms, "dense_sdpa_ms": round(dn, 4), "speedup_vs_dense": round(dn / ms, 2)})
+    xs = np.array([r["ctx"] / 1024 for r in rows])
+    grad = lambda key: float(np.polyfit(xs, np.array([r[key] for r in rows]), 1)[0])  # noqa: E731
+    return {"rows": rows, "gradient_auto_ms_per_1k_tokens": round(grad("auto_ms"), 4),
+            "gradient_dense_ms_per_1k_tokens": round(grad("dense_sdpa_ms"), 4),
+            "dense": "torch SDPA (cuDNN) causal, enable_gqa, same shape, bf16"}
 
 
 def main():
