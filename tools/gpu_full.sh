@@ -14,7 +14,7 @@ timeout 1200 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; ech
 tail -3 $OUT/pytest_gpu.log
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc=$?"
-CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-128k --no-est --no-ttft"
+CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-128k --no-est --no-ttft --no-c5"
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 2 -c 1 \
