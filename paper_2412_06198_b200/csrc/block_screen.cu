@@ -1,9 +1,12 @@
 // block_screen.cu — the Block-Cluster index for small k_b (<= 8, the auto
-// search's Block(8, 1)) by an fp16 screen and an exact refine.  Opt-in inside
-// sa_prefill (SA_BLOCK_SCREEN=1) and the sa_block_index_bf16 entry point: at
-// 32K it measured slower than the split-bf16 GEMM it would replace (the screen
-// epilogue's top-T tracking is issue/latency-bound where the GEMM is
-// tensor-bound, and the exact re-scoring is latency-bound).
+// search's Block(8, 1)) by fp16 tensor passes and an exact refine.  Opt-in
+// inside sa_prefill (SA_BLOCK_SCREEN=1) and the sa_block_index_bf16 entry
+// point: at 32K both variants measured slower than the split-bf16 GEMM they
+// would replace: for 2 <= k_b <= 8 the one-pass screen's top-T
+// tracking epilogue is issue/latency-bound; for k_b = 1 the two-pass top-1
+// (block_top1_kernel) runs its GEMM ~13% faster than the split GEMM, but the
+// second read of every logit from TMEM, the exact refine and the fp16 pooling
+// give the gain back.
 //
 // Reference: patterns.py:279-287 (block_mean) and patterns.py:290-321
 // (build_block_index): per query block, the top-min(k_b, gq+1) causal key
@@ -60,8 +63,8 @@ namespace sa {
 // pooled block layout of one side (Q or K) in the workspace:
 //   f16  [G, nb, 128] half   normalised copy (TMA operand)
 //   mean [G, nb, 128] float  exact fp32 means (refine)
-//   aux  [G, nb]      float2 (|mean|_2, 2^e: the block's own scale for q, the head's for k)
-//   head [G]          int2   k only: (max biased exponent, max |mean|_2 as float bits)
+//   aux  [G, nb]      float2 (|x~|_2 of the normalised copy, 2^e: the block's own scale for q, the head's for k)
+//   head [G]          int2   k only: (max biased exponent, max |y~|_2 as float bits)
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 size_t pool16_bytes(int groups, int nb) {
   const size_t gb = (size_t)groups * nb;
@@ -80,6 +83,24 @@ static Pool16View pool16_view(void* base, int groups, int nb) {
                     reinterpret_cast<float2*>(p + gb * 768), reinterpret_cast<int2*>(p + gb * 768 + al256(gb * 8))};
 }
 constexpr int kExpBias = 256;
+
+// max of non-negative ints into base[2 g + comp] for the CTA's half-warps:
+// the CTA's first two groups reduce in shared memory first (one global atomic
+// each instead of one per block: thousands of same-address atomics per head
+// serialise in L2).  Every thread of the CTA must call it.
+__device__ __forceinline__ void cta_group_max(int* base, int comp, int g, int g0, bool on, int v) {
+  __shared__ int sm[2];
+  if (threadIdx.x < 2) sm[threadIdx.x] = 0;
+  __syncthreads();
+  if (on) {
+    if (g - g0 < 2)
+      atomicMax(&sm[g - g0], v);
+    else
+      atomicMax(base + 2 * g + comp, v);
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 && sm[threadIdx.x] > 0) atomicMax(base + 2 * (g0 + threadIdx.x) + comp, sm[threadIdx.x]);
+}
 
 // One half-warp per (group, block); lane l pools dims 8 (l % 16) .. + 7 over
 // the block's rows in order (fp32), like block_pool_kernel.  Query side
@@ -118,68 +139,87 @@ __global__ void block_pool16_kernel(const __nv_bfloat16* __restrict__ x, int G, 
     for (; r < r1; ++r) add(__ldg(src + (size_t)(r - r0) * (kHeadDim / 8)));
   }
   const float cntf = on ? (float)(r1 - r0) : 1.f;
-  float mean[8], amax = 0.f, ss = 0.f;
+  float mean[8], amax = 0.f;
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     mean[u] = __fdiv_rn(acc[u], cntf);
     amax = fmaxf(amax, fabsf(mean[u]));
-    ss = fmaf(mean[u], mean[u], ss);
   }
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) {  // the half-warp's 16 lanes (xor < 16 stays inside)
+  for (int o = 8; o > 0; o >>= 1)  // the half-warp's 16 lanes (xor < 16 stays inside)
     amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  }
-  if (!on) return;
   // 2^-e * max in [2^13, 2^14); e clamped so 2^e stays a normal float
   int E = -1000;
   if (amax > 0.f) frexpf(amax, &E);  // amax in [2^(E-1), 2^E)
+  const int ex = amax > 0.f ? max(E - 14, -120) : 0;
+  // the norm of the normalised copy (its squares cannot underflow the way the
+  // raw means' squares can: the bound E of the screens is taken from it)
+  float ss = 0.f;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const float y = ldexpf(mean[u], -ex);
+    ss = fmaf(y, y, ss);
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   const long long row = (long long)g * nb + blk;
-  float* mo = mean_out + row * kHeadDim + 8 * hl;
-  *reinterpret_cast<float4*>(mo) = make_float4(mean[0], mean[1], mean[2], mean[3]);
-  *reinterpret_cast<float4*>(mo + 4) = make_float4(mean[4], mean[5], mean[6], mean[7]);
-  const float nrm = sqrtf(ss);
-  if (head != nullptr) {
-    if (hl == 0) {
-      aux[row] = make_float2(nrm, 0.f);
-      if (amax > 0.f) atomicMax(&head[g].x, E + kExpBias);
-      atomicMax(&head[g].y, __float_as_int(nrm));  // non-negative floats order as ints
-    }
+  if (on) {
+    float* mo = mean_out + row * kHeadDim + 8 * hl;
+    *reinterpret_cast<float4*>(mo) = make_float4(mean[0], mean[1], mean[2], mean[3]);
+    *reinterpret_cast<float4*>(mo + 4) = make_float4(mean[4], mean[5], mean[6], mean[7]);
+  }
+  if (head != nullptr) {  // key side: the head's exponent now, the fp16 copy and |y~| in key_f16_kernel
+    const int g0 = (int)(((long long)blockIdx.x * blockDim.x >> 4) / nb);
+    cta_group_max(reinterpret_cast<int*>(head), 0, g, g0, on && hl == 0 && amax > 0.f, E + kExpBias);
     return;
   }
-  const int ex = amax > 0.f ? max(E - 14, -120) : 0;
+  if (!on) return;
   __align__(16) __half h[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) h[u] = __float2half_rn(ldexpf(mean[u], -ex));
   *reinterpret_cast<uint4*>(f16 + row * kHeadDim + 8 * hl) = *reinterpret_cast<uint4*>(h);
-  if (hl == 0) aux[row] = make_float2(nrm, ldexpf(1.f, ex));
+  if (hl == 0) aux[row] = make_float2(sqrtf(ss), ldexpf(1.f, ex));  // (|x~|, 2^e)
 }
 
-// Key side, second pass: fp16 copy of every block at its kv head's common scale.
+// Key side, second pass: fp16 copy of every block at its kv head's common
+// scale; head[g].y = max |y~| over the head (as float bits, zeroed by the caller).
 __global__ void key_f16_kernel(int G, int nb, const float* __restrict__ mean, __half* f16, float2* aux,
-                               const int2* head) {
+                               int2* head) {
   const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
   const int hl = threadIdx.x & 15;
-  if (gid >= (long long)G * nb) return;
-  const int g = (int)(gid / nb);
-  const int hx = head[g].x;
-  const int ex = hx > 0 ? max(hx - kExpBias - 14, -120) : 0;
-  const float4* mi = reinterpret_cast<const float4*>(mean + gid * kHeadDim + 8 * hl);
-  const float4 m0 = __ldg(mi), m1 = __ldg(mi + 1);
-  const float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-  __align__(16) __half h[8];
+  const bool live = gid < (long long)G * nb;
+  const int g = live ? (int)(gid / nb) : 0;
+  float ss = 0.f;
+  if (live) {
+    const int hx = head[g].x;
+    const int ex = hx > 0 ? max(hx - kExpBias - 14, -120) : 0;
+    const float4* mi = reinterpret_cast<const float4*>(mean + gid * kHeadDim + 8 * hl);
+    const float4 m0 = __ldg(mi), m1 = __ldg(mi + 1);
+    const float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+    __align__(16) __half h[8];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) h[u] = __float2half_rn(ldexpf(m[u], -ex));
-  *reinterpret_cast<uint4*>(f16 + gid * kHeadDim + 8 * hl) = *reinterpret_cast<uint4*>(h);
-  if (hl == 0) aux[gid].y = ldexpf(1.f, ex);
+    for (int u = 0; u < 8; ++u) {
+      const float y = ldexpf(m[u], -ex);
+      h[u] = __float2half_rn(y);
+      ss = fmaf(y, y, ss);
+    }
+    *reinterpret_cast<uint4*>(f16 + gid * kHeadDim + 8 * hl) = *reinterpret_cast<uint4*>(h);
+    if (hl == 0) aux[gid].y = ldexpf(1.f, ex);
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);  // xor < 16: inside the half-warp
+  const float yn = sqrtf(ss);
+  if (live && hl == 0) aux[gid].x = yn;  // |y~|
+  const int g0 = (int)(((long long)blockIdx.x * blockDim.x >> 4) / nb);
+  cta_group_max(reinterpret_cast<int*>(head), 1, g, g0, live && hl == 0, __float_as_int(yn));  // floats >= 0 order as ints
 }
 
 struct ScreenArgs {
   CUtensorMap tmap_q;  // q16 [HH, nb, 128] (2-byte elements), box {64, 128}
   CUtensorMap tmap_k;  // k16 [HK, nb, 128]
-  const float2* qaux;  // [HH, nb] (|x|, 2^e_q)
-  const float2* kaux;  // [HK, nb] (|y|, 2^e_head)
-  const int2* khead;   // [HK] (max biased exponent, max |y| bits)
+  const float2* qaux;  // [HH, nb] (|x~|, 2^e_q): the normalised copy's norm
+  const float2* kaux;  // [HK, nb] (|y~|, 2^e_head)
+  const int2* khead;   // [HK] (max biased exponent, max |y~| bits)
   int nb, heads, kv_heads, nqt, k_b;
   float* tv;           // [HH, nb, T] tracked chunk maxima (raw units), -inf padded
   float* t2;           // [HH, nb, T] each tracked chunk's second largest value
@@ -367,9 +407,8 @@ __global__ void __launch_bounds__(kScThreads, 2) block_screen_kernel(const __gri
     if (valid) {
       const float2 qa = a.qaux[(size_t)hh * a.nb + gq];
       const int2 kh = a.khead[hkv];
-      const int ek = kh.x > 0 ? max(kh.x - kExpBias - 14, -120) : 0;
-      const float xn = qa.x / qa.y;                             // |x~|
-      const float yn = ldexpf(__int_as_float(kh.y), -ek);       // |y~|max
+      const float xn = qa.x;                 // |x~|
+      const float yn = __int_as_float(kh.y);  // |y~|max
       const float E = (ldexpf(1.f, -9) + ldexpf(1.f, -15)) * xn * yn + ldexpf(xn + yn, -21) + ldexpf(1.f, -40);
       const size_t r = (size_t)hh * a.nb + gq;
 #pragma unroll
@@ -385,6 +424,257 @@ __global__ void __launch_bounds__(kScThreads, 2) block_screen_kernel(const __gri
   tc_fence_before();
   __syncthreads();
   if (warp == 5) tmem_dealloc(tbase, 256);
+}
+
+// ---------------------------------------------------------------- k_b = 1
+// The auto search's Block(8, 1) needs only each row's argmax, so k_b = 1 runs
+// the fp16 GEMM TWICE per CTA instead of tracking candidates in one pass:
+//   pass A: every key tile's logits reduce to the row max M~ (a max tree: ~0.5
+//           instructions per logit, far below the tensor time of the tile);
+//   pass B: the same MMAs again (bit-identical values); every logit with
+//           s~ >= M~ - 2E is a candidate (the exact argmax is one of them:
+//           s >= M >= M~ - E and s~ >= s - E), appended per row (few: the
+//           argmax and whatever lies within the fp16 error of it).
+// A row with one candidate is decided at once; rows with 2..kTop1Cand go to
+// block_top1_refine_kernel (exact fp64 dots of the fp32 means), rows with
+// more to the CTA-per-row rescan (massive exact ties only).  A zero query block (or an all-zero key head) has all logits
+// exactly 0 and takes block 0.  Two fp16 passes are 16 MMAs per 128 x 128
+// tile against the split-bf16 GEMM's 24.
+constexpr int kTop1Cand = 16;  // candidates kept per row (global slots; more go to the rescan)
+__device__ __forceinline__ void write_block_row(int32_t* dst, int gq, const int (&sel)[8], int K, int stride);
+
+struct Top1Args {
+  CUtensorMap tmap_q;
+  CUtensorMap tmap_k;
+  const float2* qaux;
+  const int2* khead;
+  int nb, heads, kv_heads, nqt;
+  int32_t* blk_idx;  // per head at hh * head_stride: [nb, 2]
+  long long head_stride;
+  int32_t* blk_row_off;  // per head at hh * row_stride: [nb + 1]
+  int row_stride;
+  int32_t* cand;    // [HH * nb, kTop1Cand] candidate slots
+  int32_t* ccount;  // [HH * nb] candidates of the rows sent to the refine
+  int* refine;      // [count, rows...]: 2..kTop1Cand candidates
+  int* rescan;      // [count, rows...]: more than kTop1Cand
+  const int32_t* gate;
+  int gate_val;
+};
+
+__device__ __forceinline__ float max32(const float (&x)[32]) {
+  float m[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) m[i] = fmax3(x[3 * i], x[3 * i + 1], x[3 * i + 2]);
+  m[10] = fmaxf(x[30], x[31]);
+  const float a = fmax3(m[0], m[1], m[2]), b = fmax3(m[3], m[4], m[5]), c = fmax3(m[6], m[7], m[8]);
+  return fmax3(fmax3(a, b, c), m[9], m[10]);
+}
+
+__device__ __forceinline__ void utccp_128x256b(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
+}
+
+// The MMAs read the query operand from TMEM (copied once per CTA with
+// tcgen05.cp) and only the key chunk from shared memory: an SS MMA reads both
+// operands (8 KB per M=128 N=128 K=16 MMA = the 128 B/clk shared-memory port
+// by itself), which with the TMA fills left the tensor pipe ~60% busy.  TMEM
+// (256 columns per CTA, two CTAs per SM): q [0, 64), three 64-column S
+// buffers (one per 64-key chunk, N = 64 runs at the full rate from TMEM).
+constexpr int kT1ColS = 64;
+constexpr int kT1Threads = 320;  // 8 epilogue warps (two per TMEM lane quarter), producer, MMA issuer
+enum T1Bar { T1_A = 0, T1_KF0, T1_KE0 = T1_KF0 + kScRing, T1_SF0 = T1_KE0 + kScRing, T1_SE0 = T1_SF0 + 3, T1_NUM = T1_SE0 + 3 };
+
+// The two epilogue warps of a lane quarter take alternate 64-key chunks (warp
+// set p = warp / 4 takes chunks u = p, p + 2, ...), so each has two MMA chunk
+// times to finish one; they meet twice, through shared memory: the row max
+// after pass A, and the candidate counts at the end (set p appends into slots
+// [8 p, 8 p + 8) of the row's kTop1Cand).
+__global__ void __launch_bounds__(kT1Threads, 2) block_top1_kernel(const __grid_constant__ Top1Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem) & 1023u) != 0u) __trap();
+  const int hh = blockIdx.x;
+  if (a.gate && a.gate[hh] != a.gate_val) return;
+  const int qt = a.nqt - 1 - blockIdx.y;  // heaviest query tiles first
+  const int cnt = qt + 1;                 // causal key tiles per pass
+  uint8_t* sA = smem + kScSmemA;
+  uint8_t* sB = smem + kScSmemB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kScSmemBar);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + T1_NUM);
+  __shared__ float sM[128];
+  __shared__ int sN[128];
+  const int warp = warp_id();
+  const int bidx = hh / a.heads;
+  const int hkv = bidx * a.kv_heads + (hh % a.heads) / (a.heads / a.kv_heads);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[T1_A], 1);
+    for (int s = 0; s < kScRing; ++s) {
+      mbar_init(&bars[T1_KF0 + s], 1);
+      mbar_init(&bars[T1_KE0 + s], 1);
+    }
+    for (int s = 0; s < 3; ++s) {
+      mbar_init(&bars[T1_SF0 + s], 1);
+      mbar_init(&bars[T1_SE0 + s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_holder, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+
+  if (warp == 8) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(&bars[T1_A], 32768);
+      for (int c = 0; c < 2; ++c) tma_load_3d(sA + c * 16384, &a.tmap_q, &bars[T1_A], 64 * c, qt * kTile, hh);
+      // the key tiles' d-halves, once per pass (pass B's are L2 hits: nb x 256 B per kv head)
+      for (int j = 0; j < 2 * cnt; ++j) {
+        const int jt = j < cnt ? j : j - cnt;
+        for (int c = 0; c < 2; ++c) {
+          const int g = 2 * j + c, slot = g % kScRing;
+          if (g >= kScRing) mbar_wait_backoff<256>(&bars[T1_KE0 + slot], ((g / kScRing) - 1) & 1);
+          mbar_arrive_expect_tx(&bars[T1_KF0 + slot], 16384);
+          tma_load_3d(sB + slot * 16384, &a.tmap_k, &bars[T1_KF0 + slot], 64 * c, jt * kTile, hkv);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_f16_f32(128, 64);
+      const uint32_t a_addr = smem_u32(sA);
+      const uint32_t b_addr = smem_u32(sB);
+      mbar_wait(&bars[T1_A], 0);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        utccp_128x256b(tbase + kk * 8, sdesc_sw128(a_addr + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024));
+      for (int j = 0; j < 2 * cnt; ++j) {
+        const int s0 = (2 * j) % kScRing, s1 = (2 * j + 1) % kScRing;
+        mbar_wait(&bars[T1_KF0 + s0], ((2 * j) / kScRing) & 1);
+        mbar_wait(&bars[T1_KF0 + s1], ((2 * j + 1) / kScRing) & 1);
+        for (int h = 0; h < 2; ++h) {  // 64-key chunk h of the tile (keys 64 h .. 64 h + 63: +8 KB in SW128)
+          const int u = 2 * j + h, buf = u % 3;
+          if (u >= 3) mbar_wait(&bars[T1_SE0 + buf], ((u / 3) - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const int slot = (kk >> 2) ? s1 : s0;
+            mma_ts(tbase + kT1ColS + 64 * buf, tbase + kk * 8,
+                   sdesc_sw128(b_addr + slot * 16384 + h * 8192 + (kk & 3) * 32, 16, 1024), idesc, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&bars[T1_SF0 + buf]);
+        }
+        mma_commit(&bars[T1_KE0 + s0]);
+        mma_commit(&bars[T1_KE0 + s1]);
+      }
+    }
+  } else {
+    const int t = threadIdx.x & 127;  // query block row of the tile (TMEM lane)
+    const int p = warp >> 2;          // warp set: chunks u = p, p + 2, ...
+    const int gq = qt * kTile + t;
+    const bool valid = gq < a.nb;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const size_t r = (size_t)hh * a.nb + (valid ? gq : 0);
+    float M = -INFINITY;     // pass A: max over this set's chunks of the row (raw units)
+    float theta = INFINITY;  // pass B: candidate threshold M~ - 2E
+    int nc = 0;
+    int32_t* cand = a.cand + r * kTop1Cand + 8 * p;  // this set's 8 slots (written only for candidates)
+    for (int u = p; u < 4 * cnt; u += 2) {  // 64-key chunks: pass A, then pass B
+      const int j = u >> 1;
+      const bool pb = j >= cnt;
+      const int jt = pb ? j - cnt : j;
+      const int buf = u % 3;
+      const int g0 = jt * kTile + (u & 1) * 64;
+      const int lim = gq - g0;          // block-causal: key block g0 + c <= gq
+      const bool diag = jt == cnt - 1;  // the only tile with block-causal cuts
+      if (u == 2 * cnt + p) {  // first pass-B chunk: the row max over both sets
+        if (p == 1) sM[t] = M;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (p == 0) sM[t] = fmaxf(M, sM[t]);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        M = sM[t];
+        if (valid) {
+          // E bounds |s~ - s| in raw units (block_screen_kernel's bound)
+          const float xn = a.qaux[r].x, yn = __int_as_float(a.khead[hkv].y);  // |x~|, |y~|max
+          const float E = (ldexpf(1.f, -9) + ldexpf(1.f, -15)) * xn * yn + ldexpf(xn + yn, -21) + ldexpf(1.f, -40);
+          theta = M - 2.0002f * E;
+        }
+      }
+      mbar_wait(&bars[T1_SF0 + buf], (u / 3) & 1);
+      tc_fence_after();
+      // both halves in flight, then the buffer goes straight back to the MMA warp
+      uint32_t s0[32], s1[32];
+      const uint32_t col = tbase + lane_off + kT1ColS + 64 * buf;
+      tmem_ld32(col, s0);
+      tmem_ld32(col + 32, s1);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&bars[T1_SE0 + buf]);
+      auto process = [&](const uint32_t (&s)[32], int c) {
+        float x[32];
+#pragma unroll
+        for (int v = 0; v < 32; ++v) x[v] = __uint_as_float(s[v]);
+        if (diag || !valid) {
+#pragma unroll
+          for (int v = 0; v < 32; ++v) x[v] = (valid && 32 * c + v <= lim) ? x[v] : -INFINITY;
+        }
+        // maxima of the four 8-column groups, then of the 32
+        float gm[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          gm[q] = fmax3(fmax3(x[8 * q], x[8 * q + 1], x[8 * q + 2]), fmax3(x[8 * q + 3], x[8 * q + 4], x[8 * q + 5]),
+                        fmaxf(x[8 * q + 6], x[8 * q + 7]));
+        const float m = fmaxf(fmax3(gm[0], gm[1], gm[2]), gm[3]);
+        if (!pb) {
+          M = fmaxf(M, m);
+        } else if (__any_sync(0xffffffffu, m >= theta)) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (gm[q] >= theta) {  // rare per lane: scan the group
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                if (x[8 * q + v] >= theta) {
+                  if (nc < 8) cand[nc] = g0 + 32 * c + 8 * q + v;
+                  ++nc;
+                }
+              }
+            }
+          }
+        }
+      };
+      process(s0, 0);
+      process(s1, 1);
+    }
+    // both sets' counts meet; set 0 finishes the row
+    if (p == 1) sN[t] = nc;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (p == 0 && valid) {
+      const int n1 = sN[t];
+      int32_t* c0 = a.cand + r * kTop1Cand;
+      int32_t* ro = a.blk_row_off + (size_t)hh * a.row_stride;
+      ro[gq] = (int32_t)(hh * a.head_stride + (long long)gq * 2);
+      if (gq == a.nb - 1) ro[a.nb] = (int32_t)(hh * a.head_stride + (long long)a.nb * 2);
+      // a zero query block (or an all-zero key head) makes every logit exactly
+      // 0: the lowest id wins, like the reference's stable top-k
+      const bool zero = a.qaux[r].x == 0.f || a.khead[hkv].y == 0;
+      const int tot = nc + n1;
+      if (zero || tot == 1) {
+        int sel[8] = {zero ? 0 : (nc == 1 ? c0[0] : c0[8]), -1, -1, -1, -1, -1, -1, -1};
+        write_block_row(a.blk_idx + (size_t)hh * a.head_stride + (size_t)gq * 2, gq, sel, 1, 2);
+      } else if (nc <= 8 && n1 <= 8) {
+        for (int c = 0; c < n1; ++c) c0[nc + c] = c0[8 + c];  // pack set 1's slots after set 0's
+        a.ccount[r] = tot;
+        a.refine[1 + atomicAdd(a.refine, 1)] = (int)r;
+      } else {
+        a.rescan[1 + atomicAdd(a.rescan, 1)] = (int)r;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc(tbase, 256);
 }
 
 __device__ __forceinline__ double warp_sum_d(double x) {
@@ -607,9 +897,9 @@ __global__ void __launch_bounds__(256) block_refine_kernel(
 // blocks' loads in flight per thread; per-thread top-k lists merge through
 // warp shuffles and then across the eight warps.
 constexpr int kRescanThreads = 256;
-__global__ void __launch_bounds__(kRescanThreads) block_rescan_kernel(
-    const int* __restrict__ list, const float* __restrict__ qmean, const float* __restrict__ kmean, int heads,
-    int kv_heads, int nb, int k_b, int32_t* blk_idx, long long head_stride) {
+__device__ __forceinline__ void rescan_rows(const int* __restrict__ list, const float* __restrict__ qmean,
+                                            const float* __restrict__ kmean, int heads, int kv_heads, int nb,
+                                            int k_b, int32_t* blk_idx, long long head_stride) {
   __shared__ float4 sq[32];
   __shared__ double sv[8][8];
   __shared__ int si[8][8];
@@ -650,6 +940,55 @@ __global__ void __launch_bounds__(kRescanThreads) block_rescan_kernel(
     __syncthreads();
   }
 }
+__global__ void __launch_bounds__(kRescanThreads) block_rescan_kernel(
+    const int* __restrict__ list, const float* __restrict__ qmean, const float* __restrict__ kmean, int heads,
+    int kv_heads, int nb, int k_b, int32_t* blk_idx, long long head_stride) {
+  rescan_rows(list, qmean, kmean, heads, kv_heads, nb, k_b, blk_idx, head_stride);
+}
+
+// k_b = 1 rows with 2..kTop1Cand candidates: a warp per row, lane l holds
+// dims 4l..4l+3 of the query mean and of each candidate's key mean; fp64
+// products summed across the warp and taken from lane 0, so every lane
+// compares the same values; the largest exact logit wins, ties to the lower
+// id.  Then the CTAs re-score the rescan rows (rescan_rows, k_b = 1).
+__global__ void __launch_bounds__(kRescanThreads) block_top1_refine_kernel(
+    const int* __restrict__ refine, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
+    const int* __restrict__ rescan, const float* __restrict__ qmean, const float* __restrict__ kmean, int heads,
+    int kv_heads, int nb, int32_t* blk_idx, long long head_stride) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (kRescanThreads / 32);
+  const int cnt = refine[0];
+  for (int it = (int)((blockIdx.x * kRescanThreads + threadIdx.x) >> 5); it < cnt; it += nwarps) {
+    const int r = refine[1 + it];
+    const int hh = r / nb, gq = r % nb;
+    const int hkv = (hh / heads) * kv_heads + (hh % heads) / (heads / kv_heads);
+    const float4 qx = __ldg(reinterpret_cast<const float4*>(qmean + (size_t)r * kHeadDim) + lane);
+    const int nc = ccount[r];
+    double best = -INFINITY;
+    int bi = INT_MAX;
+    for (int c = 0; c < nc; ++c) {
+      const int g = cand[(size_t)r * kTop1Cand + c];
+      const float4 kx = __ldg(reinterpret_cast<const float4*>(kmean + ((size_t)hkv * nb + g) * kHeadDim) + lane);
+      double d = (double)qx.x * (double)kx.x;
+      d = fma((double)qx.y, (double)kx.y, d);
+      d = fma((double)qx.z, (double)kx.z, d);
+      d = fma((double)qx.w, (double)kx.w, d);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      d = __shfl_sync(0xffffffffu, d, 0);
+      if (d > best || (d == best && g < bi)) {
+        best = d;
+        bi = g;
+      }
+    }
+    if (lane == 0) {
+      int sel[8] = {bi, -1, -1, -1, -1, -1, -1, -1};
+      write_block_row(blk_idx + (size_t)hh * head_stride + (size_t)gq * 2, gq, sel, 1, 2);
+    }
+  }
+  rescan_rows(rescan, qmean, kmean, heads, kv_heads, nb, 1, blk_idx, head_stride);
+}
+
 
 int launch_block_pool16(int groups, int n, int b, const void* x, void* pooled, bool key_side, const int32_t* gate,
                         int gate_val, cudaStream_t st) {
@@ -670,7 +1009,8 @@ int launch_block_pool16(int groups, int n, int b, const void* x, void* pooled, b
 }
 
 // tracked candidates per row: k_b + 3, rounded to the kernel instantiations
-static int screen_T(int k_b) { return k_b <= 1 ? 4 : k_b == 2 ? 5 : k_b <= 4 ? 7 : 11; }
+// (k_b = 1: the top-1 path's candidate slots, kTop1Cand per row, in the tv region)
+static int screen_T(int k_b) { return k_b <= 1 ? kTop1Cand : k_b == 2 ? 5 : k_b <= 4 ? 7 : 11; }
 
 size_t block_screen_ws(int nb, int k_b, int hh_total) {
   const size_t rows = (size_t)hh_total * nb;
@@ -750,13 +1090,45 @@ int launch_block_screen(int batch, int heads, int kv_heads, int n, int b, int k_
   int* rescan = reinterpret_cast<int*>(p);  // [count, rows...]
   a.gate = gate;
   a.gate_val = gate_val;
-  if ((rc = launch_fixed_row_off(blk_row_off, hh_total, nb, k_b + 1, row_stride, head_stride, gate, gate_val, st)))
+  if (k_b > 1 &&
+      (rc = launch_fixed_row_off(blk_row_off, hh_total, nb, k_b + 1, row_stride, head_stride, gate, gate_val, st)))
     return rc;
   cudaMemsetAsync(rescan, 0, sizeof(int), st);
   switch (k_b) {
-    case 1:
-      if ((rc = run_screen<4>(a, hh_total, a.nqt, st))) return rc;
-      return run_refine<4>(a, qv.mean, kv.mean, hh_total, blk_idx, head_stride, rescan, st);
+    case 1: {
+      // two fp16 passes (block_top1_kernel); the tracked-maxima workspace holds
+      // the candidate slots (tv), the refine list (ti) and counts (terr)
+      Top1Args t;
+      memset(&t, 0, sizeof(t));
+      t.tmap_q = a.tmap_q;
+      t.tmap_k = a.tmap_k;
+      t.qaux = a.qaux;
+      t.khead = a.khead;
+      t.nb = nb;
+      t.heads = heads;
+      t.kv_heads = kv_heads;
+      t.nqt = a.nqt;
+      t.blk_idx = blk_idx;
+      t.head_stride = head_stride;
+      t.blk_row_off = blk_row_off;
+      t.row_stride = row_stride;
+      t.cand = reinterpret_cast<int32_t*>(a.tv);
+      t.ccount = reinterpret_cast<int32_t*>(a.terr);
+      t.refine = reinterpret_cast<int*>(a.ti);
+      t.rescan = rescan;
+      t.gate = gate;
+      t.gate_val = gate_val;
+      cudaMemsetAsync(t.refine, 0, sizeof(int), st);
+      static std::atomic<uint64_t> attr_done{0};
+      once_per_device(attr_done, [] {
+        cudaFuncSetAttribute(block_top1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kScSmemBytes);
+      });
+      block_top1_kernel<<<dim3(hh_total, a.nqt), kT1Threads, kScSmemBytes, st>>>(t);
+      if ((rc = check_launch("block_top1_kernel"))) return rc;
+      block_top1_refine_kernel<<<16 * device_sm_count(), kRescanThreads, 0, st>>>(
+          t.refine, t.cand, t.ccount, rescan, qv.mean, kv.mean, heads, kv_heads, nb, blk_idx, head_stride);
+      return check_launch("block_top1_refine_kernel");
+    }
     case 2:
       if ((rc = run_screen<5>(a, hh_total, a.nqt, st))) return rc;
       return run_refine<5>(a, qv.mean, kv.mean, hh_total, blk_idx, head_stride, rescan, st);

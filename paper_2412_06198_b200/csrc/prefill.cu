@@ -105,9 +105,11 @@ static int clamp_pattern(const sa_pattern& in, int n, sa_pattern* out) {
 }
 
 // SA_BLOCK_SCREEN=1: Block-Cluster candidates with k_b <= 8 take the fp16
-// screen + exact refine of block_screen.cu instead of the split-bf16 GEMM of
-// estimate_block.cu.  Opt-in: measured slower at 32K ("Block
-// estimator: fp16 screen"), kept for A/B and as the sa_block_index_bf16 path.
+// paths of block_screen.cu (k_b = 1, the auto search's Block(8, 1): two fp16
+// passes + exact refine; 2..8: one fp16 pass tracking chunk maxima + exact
+// refine) instead of the split-bf16 GEMM of estimate_block.cu.  Opt-in: both
+// measured slower than the split GEMM at 32K ("Block estimator:
+// fp16 screen"); kept for A/B and as the sa_block_index_bf16 path.
 static bool use_block_screen(int k_b) {
   static const bool on = [] {
     const char* e = getenv("SA_BLOCK_SCREEN");

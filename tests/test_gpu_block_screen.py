@@ -70,7 +70,7 @@ def check_rows(got, q, k, b, k_b, tol=2e-6):
 
 @pytest.mark.parametrize("n,b,k_b", [(13, 4, 2), (1000, 8, 1), (4096, 8, 1), (4096, 64, 6), (3000, 7, 3),
                                      (2000, 128, 2), (600, 200, 1), (1001, 8, 8), (20000, 8, 1),
-                                     (16390, 16, 4)])
+                                     (16390, 16, 4), (32768, 8, 1), (8200, 16, 1), (129, 1, 1)])
 def test_block_screen_vs_oracle(lib, n, b, k_b):
     q, k = rand_heads(11, 1, n), rand_heads(12, 1, n)
     got = screen_rows(q, k, b, k_b)[0]
@@ -86,7 +86,7 @@ def test_block_screen_gqa_heads(lib):
         check_rows(got[h], q[h], k[h // 2], b, k_b)
 
 
-@pytest.mark.parametrize("case", ["zeros", "repeated_keys", "two_level", "wide_range", "tiny"])
+@pytest.mark.parametrize("case", ["zeros", "repeated_keys", "two_level", "pairs", "zero_keys", "wide_range", "tiny"])
 @pytest.mark.parametrize("k_b", [1, 3])
 def test_block_screen_ties_and_ranges(lib, case, k_b):
     """Exact ties everywhere (every row re-scored in full), repeated blocks,
@@ -99,6 +99,10 @@ def test_block_screen_ties_and_ranges(lib, case, k_b):
         k = np.tile(k[:b], (n // b, 1))
     elif case == "two_level":
         k = np.tile(np.concatenate([k[:b], k[b:2 * b]]), (n // (2 * b), 1))
+    elif case == "pairs":  # every key block twice in a row: each row's best block ties with its twin
+        k = np.repeat(k.reshape(n // b, b, -1)[::2], 2, axis=0).reshape(n, -1)
+    elif case == "zero_keys":
+        k = np.zeros_like(k)
     elif case == "wide_range":  # 30x queries, key blocks spanning 1e-6 .. 1e1 (logits stay where the
         # reference's softmax keeps every weight nonzero: it selects on weights, ties at 0 to low ids)
         q = O.bf16_round(q * 30)
@@ -107,7 +111,7 @@ def test_block_screen_ties_and_ranges(lib, case, k_b):
     else:  # pooled values below fp16's normal range (logits still resolvable after the softmax)
         q, k = O.bf16_round(q * 1e-4), O.bf16_round(k * 3e-5)
     got = screen_rows(q[None], k[None], b, k_b)[0]
-    if case in ("zeros", "repeated_keys", "two_level"):
+    if case in ("zeros", "repeated_keys", "two_level", "pairs", "zero_keys"):
         want = O.block_index(q.astype(np.float64), k.astype(np.float64), b, k_b).block_rows
         for g, (r_got, r_want) in enumerate(zip(got, want)):
             assert r_got == r_want.tolist(), (g, r_got, r_want.tolist())
@@ -118,9 +122,10 @@ def test_block_screen_ties_and_ranges(lib, case, k_b):
 
 
 def test_block_screen_matches_split_path_in_prefill(lib):
-    """sa_prefill with a fixed Block(8, 1) layer: the screen path
-    (SA_BLOCK_SCREEN=1) and the default split-bf16 GEMM (separate processes)
-    give the same block rows except at split-bf16 near-ties."""
+    """sa_prefill with a fixed Block(8, 1) layer: the two-pass fp16 top-1
+    (SA_BLOCK_SCREEN=1) and the default split-bf16 GEMM (unset / =0;
+    separate processes) give the same block rows except at split-bf16
+    near-ties."""
     import json
     import os
     import subprocess
@@ -142,11 +147,15 @@ def test_block_screen_matches_split_path_in_prefill(lib):
         "print(json.dumps(rows.tolist()))"
     )
     outs = []
-    for env in ("1", "0"):
-        r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300,
-                           env=dict(os.environ, SA_BLOCK_SCREEN=env))
+    for env in (None, "1", "0"):
+        e = dict(os.environ)
+        e.pop("SA_BLOCK_SCREEN", None)
+        if env is not None:
+            e["SA_BLOCK_SCREEN"] = env
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300, env=e)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
-    a, b = np.array(outs[0]).reshape(4, 512, 2), np.array(outs[1]).reshape(4, 512, 2)
-    diff = int((a != b).any(axis=2).sum())
+    dflt, scr, split = (np.array(o).reshape(4, 512, 2) for o in outs)
+    np.testing.assert_array_equal(dflt, split)  # the split GEMM is the default
+    diff = int((scr != split).any(axis=2).sum())
     assert diff <= 4, diff
