@@ -48,8 +48,8 @@ struct SelectArgs {
 };
 
 struct SelectSmem {
-  float q[kCalMax][129];
-  float k[kCalMax][129];
+  float q[kCalMax][132];  // 16-byte rows: the logit loop reads float4 along d
+  float k[kCalMax][132];
   float L[kCalMax][kCalMax + 1];   // scaled causal logits
   float Wd[kCalMax][kCalMax + 1];  // dense weights
   unsigned char M[kCalMax][kCalMax];  // candidate mask
@@ -129,17 +129,24 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     const int tr = tid / 16, tc = tid % 16;  // rows tr + kRowStep i, columns tc + 16 j
     float acc[kLogitRows][4] = {};
     if (tr < cal) {
-#pragma unroll 4
-      for (int d = 0; d < kHeadDim; ++d) {
-        float qv[kLogitRows], kv[4];
+      // float4 loads along d (the fmaf chain per (row, column) keeps d order)
+#pragma unroll 2
+      for (int d = 0; d < kHeadDim; d += 4) {
+        float4 qv[kLogitRows], kv[4];
 #pragma unroll
-        for (int i = 0; i < kLogitRows; ++i) qv[i] = S.q[min(tr + kRowStep * i, kCalMax - 1)][d];
+        for (int i = 0; i < kLogitRows; ++i)
+          qv[i] = *reinterpret_cast<const float4*>(&S.q[min(tr + kRowStep * i, kCalMax - 1)][d]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) kv[j] = S.k[min(tc + 16 * j, kCalMax - 1)][d];
+        for (int j = 0; j < 4; ++j) kv[j] = *reinterpret_cast<const float4*>(&S.k[min(tc + 16 * j, kCalMax - 1)][d]);
 #pragma unroll
         for (int i = 0; i < kLogitRows; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(qv[i], kv[j], acc[i][j]);
+          for (int j = 0; j < 4; ++j) {
+            acc[i][j] = fmaf(qv[i].x, kv[j].x, acc[i][j]);
+            acc[i][j] = fmaf(qv[i].y, kv[j].y, acc[i][j]);
+            acc[i][j] = fmaf(qv[i].z, kv[j].z, acc[i][j]);
+            acc[i][j] = fmaf(qv[i].w, kv[j].w, acc[i][j]);
+          }
       }
     }
 #pragma unroll
