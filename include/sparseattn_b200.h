@@ -207,11 +207,14 @@ int sa_block_select(int batch, int heads, int kv_heads, int n, int b, int k_b, f
                     void* ws, size_t ws_bytes, void* stream);
 
 /* Block-Cluster index for k_b <= 8 straight from bf16 q [B*H, n, 128] and k
- * [B*HK, n, 128] (the path sa_prefill takes; replaces block_mean +
- * build_block_index, patterns.py:279-321): fp32 pooling, one fp16 tcgen05
- * screen pass with a rigorous error bound, exact fp64 re-scoring of every
- * near-cut candidate.  Same row layout as sa_block_select (scale-free: the
- * positive 1/sqrt(d) does not change a row's order). */
+ * [B*HK, n, 128] (replaces block_mean + build_block_index,
+ * patterns.py:279-321; sa_prefill takes it under SA_BLOCK_SCREEN=1, its
+ * default is the split-bf16 GEMM of sa_block_select): fp32 pooling, fp16
+ * tcgen05 passes with a rigorous error bound (k_b = 1: a row-max pass, then a
+ * pass collecting every logit within the bound of it; 2..8: one pass tracking
+ * chunk maxima), exact fp64 re-scoring of every near-cut candidate.  Same row
+ * layout as sa_block_select (scale-free: the positive 1/sqrt(d) does not
+ * change a row's order). */
 size_t sa_block_index_workspace(int batch, int heads, int kv_heads, int n, int b, int k_b);
 int sa_block_index_bf16(int batch, int heads, int kv_heads, int n, int b, int k_b, const void* q, const void* k,
                         int32_t* blk_idx, int32_t* blk_row_off, void* ws, size_t ws_bytes, void* stream);

@@ -1144,8 +1144,9 @@ int launch_block_screen(int batch, int heads, int kv_heads, int n, int b, int k_
 
 }  // namespace sa
 
-// Block-Cluster index straight from bf16 q / k (pool16 + screen + refine): the
-// path sa_prefill takes for k_b <= 8.  Workspace: sa_block_index_workspace.
+// Block-Cluster index straight from bf16 q / k (pool16 + fp16 passes + refine):
+// sa_prefill's path for k_b <= 8 under SA_BLOCK_SCREEN=1.  Workspace:
+// sa_block_index_workspace.
 extern "C" size_t sa_block_index_workspace(int batch, int heads, int kv_heads, int n, int b, int k_b) {
   if (batch < 1 || heads < 1 || kv_heads < 1 || n < 1 || b < 1 || b > n || k_b < 1) return 0;
   const int nb = (n + b - 1) / b;
