@@ -470,9 +470,6 @@ __device__ __forceinline__ float max32(const float (&x)[32]) {
   return fmax3(fmax3(a, b, c), m[9], m[10]);
 }
 
-__device__ __forceinline__ void utccp_128x256b(uint32_t taddr, uint64_t desc) {
-  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
-}
 
 // The MMAs read the query operand from TMEM (copied once per CTA with
 // tcgen05.cp) and only the key chunk from shared memory: an SS MMA reads both

@@ -179,6 +179,13 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t smem_addr, uint32_t lbo
   return d;
 }
 
+// smem -> TMEM copy of a 128-row x 32-byte operand slice (the SS descriptor's
+// K=16 slice; an A operand for TS MMAs), issued by the MMA thread: ordered with
+// its later tcgen05.mma in the tensor pipe.
+__device__ __forceinline__ void utccp_128x256b(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
+}
+
 // 32 lanes x 32 columns of 32-bit, one row (lane) per thread.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
