@@ -44,3 +44,17 @@ print("d2h_f32 (warm out)  %.1f ms" % t(lambda: D.d2h_f32(qf, out)))
 print("d2h_f32 (fresh out) %.1f ms" % t(lambda: D.d2h_f32(qf, np.empty((1, n, H * d), dtype=np.float32))))
 print("np.empty + fill     %.1f ms" % t(lambda: np.empty((1, n, H * d), dtype=np.float32).fill(0)))
 print("torch threads", torch.get_num_threads())
+# one kv group's output columns (n x 512 floats, 2 KB rows, row stride 16 KB)
+pin = D.pinned_out(0, n * 512)
+ot = torch.from_numpy(out)
+print("strided group copy pinned->numpy (warm) %.2f ms" % t(lambda: ot[0, :, 0:512].copy_(pin.view(n, 512))))
+fresh = lambda: torch.from_numpy(np.empty((1, n, H * d), dtype=np.float32))[0, :, 0:512].copy_(pin.view(n, 512))
+print("strided group copy pinned->numpy (fresh) %.2f ms" % t(fresh))
+print("contiguous 67 MB copy pinned->numpy (warm) %.2f ms" % t(lambda: ot.view(-1)[: n * 512].copy_(pin)))
+import time as _t
+def phases():
+    R._PHASE = []
+    R.prefill(q, k, v, cfg, mode="auto")
+for _ in range(2):
+    torch.cuda.synchronize(); t0 = _t.perf_counter(); R.prefill(q, k, v, cfg, mode="auto"); torch.cuda.synchronize()
+    print("prefill again %.1f ms" % (1e3 * (_t.perf_counter() - t0)))
