@@ -52,9 +52,6 @@ fresh = lambda: torch.from_numpy(np.empty((1, n, H * d), dtype=np.float32))[0, :
 print("strided group copy pinned->numpy (fresh) %.2f ms" % t(fresh))
 print("contiguous 67 MB copy pinned->numpy (warm) %.2f ms" % t(lambda: ot.view(-1)[: n * 512].copy_(pin)))
 import time as _t
-def phases():
-    R._PHASE = []
-    R.prefill(q, k, v, cfg, mode="auto")
 for _ in range(2):
     torch.cuda.synchronize(); t0 = _t.perf_counter(); R.prefill(q, k, v, cfg, mode="auto"); torch.cuda.synchronize()
     print("prefill again %.1f ms" % (1e3 * (_t.perf_counter() - t0)))
