@@ -43,7 +43,17 @@ static SideStream* side_stream() {
   cudaGetDevice(&dev);
   SideStream& x = tab[dev & 15];
   if (!x.s) {
-    cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+    // the estimator side stream runs at the device's top priority, so the VS
+    // chain's CTAs claim SMs ahead of the block chain's and its latency-bound
+    // kernels finish early (32K auto layer: VS chain done 101 vs 202 us after
+    // selection, layer 1.115 vs 1.119 ms; SA_SIDE_PRIO=0: default priority)
+    static const bool hi = [] {
+      const char* e = getenv("SA_SIDE_PRIO");
+      return !(e && e[0] == '0');
+    }();
+    int lo_p = 0, hi_p = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p);
+    cudaStreamCreateWithPriority(&x.s, cudaStreamNonBlocking, hi ? hi_p : 0);
     cudaStreamCreateWithFlags(&x.s2, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&x.fork2, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&x.join2, cudaEventDisableTiming);
