@@ -69,14 +69,22 @@ __global__ void build_tiles_kernel(TileBuildArgs a) {
     __syncwarp();
     const int32_t* ro = a.idx.blk_row_off + (size_t)hh * a.idx.blk_row_stride;
     const int g0 = i0 / b, g1 = i1v / b;
-    for (int gq = g0; gq <= g1; ++gq) {
-      for (int k = ro[gq] + lane; k < ro[gq + 1]; k += 32) {
-        const int gk = a.idx.blk_idx[k];
-        if (gk >= (a.n + b - 1) / b) continue;  // sentinel padding
-        const int t0 = (gk * b) / kTile;
-        const int t1 = min((gk + 1) * b - 1, a.n - 1) / kTile;
-        for (int t = t0; t <= t1 && t <= qt; ++t) atomicOr(&blk_mark[t >> 5], 1u << (t & 31));
-      }
+    const int nbk = (a.n + b - 1) / b;
+    auto mark = [&](int k) {
+      const int gk = a.idx.blk_idx[k];
+      if (gk >= nbk) return;  // sentinel padding
+      const int t0 = (gk * b) / kTile;
+      const int t1 = min((gk + 1) * b - 1, a.n - 1) / kTile;
+      for (int t = t0; t <= t1 && t <= qt; ++t) atomicOr(&blk_mark[t >> 5], 1u << (t & 31));
+    };
+    if (g1 - g0 >= 7) {
+      // many short rows (b <= 16): a lane per query block, all rows' loads in flight at once
+      for (int gq = g0 + lane; gq <= g1; gq += 32)
+        for (int k = ro[gq], k1 = ro[gq + 1]; k < k1; ++k) mark(k);
+    } else {
+      // few long rows (b >= 32): the lanes split each row
+      for (int gq = g0; gq <= g1; ++gq)
+        for (int k = ro[gq] + lane; k < ro[gq + 1]; k += 32) mark(k);
     }
     __syncwarp();
   }
