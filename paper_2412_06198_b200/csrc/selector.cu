@@ -28,7 +28,6 @@ namespace sa {
 
 constexpr int kCalMax = 64;
 constexpr int kSelThreads = 512;
-constexpr int kLogitRows = kCalMax / (kSelThreads / 16);  // register tile rows per thread
 
 struct SelectArgs {
   const __nv_bfloat16* q;  // [HH, n, 128]
@@ -52,7 +51,6 @@ struct SelectSmem {
   float k[kCalMax][132];
   float L[kCalMax][kCalMax + 1];   // scaled causal logits
   float Wd[kCalMax][kCalMax + 1];  // dense weights
-  unsigned char M[kCalMax][kCalMax];  // candidate mask
   double colscore[kCalMax];
   double diagscore[kCalMax];
   float pq[kCalMax][129];  // pooled q (block candidate)
@@ -62,6 +60,10 @@ struct SelectSmem {
   unsigned char diagsel[kCalMax];
   unsigned char blksel[kCalMax][kCalMax];
   double red[kSelThreads / 32];
+  // bf16 copies of the windows for the tensor-core logits (rows padded to 272 B:
+  // conflict-free ldmatrix)
+  __align__(16) __nv_bfloat16 q16[kCalMax][136];
+  __align__(16) __nv_bfloat16 k16[kCalMax][136];
 };
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -105,7 +107,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     }
 #pragma unroll
     for (int u = 0; u < kVec; ++u) {
-      const int e = tid + u * kSelThreads;
+      const int e = tid + u * kSelThreads;  // every row of the bf16 copies (zeros past cal)
+      *reinterpret_cast<uint4*>(&S.q16[e / (kHeadDim / 8)][8 * (e % (kHeadDim / 8))]) = qv[u];
+      *reinterpret_cast<uint4*>(&S.k16[e / (kHeadDim / 8)][8 * (e % (kHeadDim / 8))]) = kv[u];
       if (e < cal * (kHeadDim / 8)) {
         const int r = e / (kHeadDim / 8), d = 8 * (e % (kHeadDim / 8));
         const uint32_t qw[4] = {qv[u].x, qv[u].y, qv[u].z, qv[u].w};
@@ -123,52 +127,88 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     }
   }
   __syncthreads();
-  // dense causal logits: each thread a kLogitRows x 4 register tile of (row, column)
+  // dense causal logits on the tensor cores (mma.sync m16n8k16, bf16 in, fp32
+  // accumulate: the products of bf16 values are exact, only the summation
+  // order differs from a sequential fp32 dot): warp w owns rows 16 (w / 4) ..
+  // + 15 and columns 16 (w % 4) .. + 15
   {
-    constexpr int kRowStep = kSelThreads / 16;
-    const int tr = tid / 16, tc = tid % 16;  // rows tr + kRowStep i, columns tc + 16 j
-    float acc[kLogitRows][4] = {};
-    if (tr < cal) {
-      // float4 loads along d (the fmaf chain per (row, column) keeps d order)
-#pragma unroll 2
-      for (int d = 0; d < kHeadDim; d += 4) {
-        float4 qv[kLogitRows], kv[4];
+    static_assert(kCalMax == 64 && kWarps == 16, "one 16 x 16 logit block per warp");
+    const int mb = wid >> 2, nb = wid & 3;
+    const int g = lane >> 2, t = lane & 3;
+    float c[2][4] = {};
 #pragma unroll
-        for (int i = 0; i < kLogitRows; ++i)
-          qv[i] = *reinterpret_cast<const float4*>(&S.q[min(tr + kRowStep * i, kCalMax - 1)][d]);
+    for (int ks = 0; ks < kHeadDim / 16; ++ks) {
+      uint32_t af[4], bq[4];
+      const uint32_t aaddr =
+          static_cast<uint32_t>(__cvta_generic_to_shared(&S.q16[16 * mb + (lane & 15)][16 * ks + (lane >> 4) * 8]));
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
+                   : "r"(aaddr));
+      const uint32_t baddr = static_cast<uint32_t>(__cvta_generic_to_shared(
+          &S.k16[16 * nb + ((lane >> 4) << 3) + (lane & 7)][16 * ks + ((lane >> 3) & 1) * 8]));
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(bq[0]), "=r"(bq[1]), "=r"(bq[2]), "=r"(bq[3])
+                   : "r"(baddr));
 #pragma unroll
-        for (int j = 0; j < 4; ++j) kv[j] = *reinterpret_cast<const float4*>(&S.k[min(tc + 16 * j, kCalMax - 1)][d]);
-#pragma unroll
-        for (int i = 0; i < kLogitRows; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            acc[i][j] = fmaf(qv[i].x, kv[j].x, acc[i][j]);
-            acc[i][j] = fmaf(qv[i].y, kv[j].y, acc[i][j]);
-            acc[i][j] = fmaf(qv[i].z, kv[j].z, acc[i][j]);
-            acc[i][j] = fmaf(qv[i].w, kv[j].w, acc[i][j]);
-          }
-      }
+      for (int nt = 0; nt < 2; ++nt)
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(c[nt][0]), "+f"(c[nt][1]), "+f"(c[nt][2]), "+f"(c[nt][3])
+            : "r"(af[0]), "r"(af[1]), "r"(af[2]), "r"(af[3]), "r"(bq[2 * nt]), "r"(bq[2 * nt + 1]));
     }
 #pragma unroll
-    for (int i = 0; i < kLogitRows; ++i)
+    for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = tr + kRowStep * i, c = tc + 16 * j;
-        if (r < cal && c < cal) S.L[r][c] = (c <= r) ? acc[i][j] * a.scale : 0.f;
-      }
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          const int r = 16 * mb + g + 8 * h, cc = 16 * nb + 8 * nt + 2 * t + x;
+          if (r < cal && cc < cal) S.L[r][cc] = (cc <= r) ? c[nt][2 * h + x] * a.scale : 0.f;
+        }
   }
   __syncthreads();
-  // dense weights (core.py:138-154): one warp per row
-  for (int r = wid; r < cal; r += kWarps) {
-    const int c0 = lane, c1 = lane + 32;
-    const float l0 = (c0 <= r) ? S.L[r][c0] : -INFINITY;
-    const float l1 = (c1 <= r && c1 < cal) ? S.L[r][c1] : -INFINITY;
-    const float mx = warp_max(fmaxf(l0, l1));
-    const float e0 = (c0 <= r) ? expf(l0 - mx) : 0.f;
-    const float e1 = (c1 <= r && c1 < cal) ? expf(l1 - mx) : 0.f;
-    const float sum = warp_sum(e0 + e1);
-    if (c0 < cal) S.Wd[r][c0] = e0 / sum;
-    if (c1 < cal) S.Wd[r][c1] = e1 / sum;
+  // dense weights (core.py:138-154): one warp per row, the warp's rows
+  // (wid, wid + 16, ...) side by side so their shuffle / exp latencies overlap
+  {
+    constexpr int kR = kCalMax / kWarps;
+    float l[kR][2], mx[kR], e[kR][2], sm[kR];
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      const int r = wid + kWarps * i;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int c = lane + 32 * t;
+        l[i][t] = (r < cal && c <= r && c < cal) ? S.L[r][c] : -INFINITY;
+      }
+      mx[i] = fmaxf(l[i][0], l[i][1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < kR; ++i) mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      const int r = wid + kWarps * i;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int c = lane + 32 * t;
+        e[i][t] = (r < cal && c <= r && c < cal) ? expf(l[i][t] - mx[i]) : 0.f;
+      }
+      sm[i] = e[i][0] + e[i][1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < kR; ++i) sm[i] += __shfl_xor_sync(0xffffffffu, sm[i], o);
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      const int r = wid + kWarps * i;
+      if (r < cal) {
+        if (lane < cal) S.Wd[r][lane] = e[i][0] / sm[i];
+        if (lane + 32 < cal) S.Wd[r][lane + 32] = e[i][1] / sm[i];
+      }
+    }
   }
   __syncthreads();
 
@@ -254,46 +294,59 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     }
     __syncthreads();
   }
-  // candidate mask
-  for (int e = tid; e < cal * cal; e += kSelThreads) {
-    const int r = e / cal, c = e % cal;
-    bool m = false;
-    if (c <= r) {
-      if (fam == FAM_TRI) {
-        m = (r - c < p1) || (c < p2) || (r == c);
-      } else if (fam == FAM_VS) {
-        m = S.colsel[c] || S.diagsel[r - c] || (r == c);
-      } else {
-        const int b = min(p1, cal);
-        m = S.blksel[r / b][c / b];
-      }
-    }
-    S.M[r][c] = m;
-  }
-  __syncthreads();
-  // sparse weights per row vs dense, squared error in float64 (core.py:179-186)
+  // sparse weights per row vs dense, squared error in float64 (core.py:179-186);
+  // the candidate's mask is evaluated in place; the warp's rows side by side,
+  // each thread's float64 partial summed in row order as before
   double part = 0.0;
-  for (int r = wid; r < cal; r += kWarps) {
-    float lv[2];
-    bool mv[2];
+  {
+    constexpr int kR = kCalMax / kWarps;
+    auto in_mask = [&](int r, int c) -> bool {
+      if (c > r) return false;
+      if (fam == FAM_TRI) return (r - c < p1) || (c < p2) || (r == c);
+      if (fam == FAM_VS) return S.colsel[c] || S.diagsel[r - c] || (r == c);
+      const int b = min(p1, cal);
+      return S.blksel[r / b][c / b];
+    };
+    float lv[kR][2], mx[kR], ev[kR][2], sm[kR];
+    bool mv[kR][2];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int c = lane + 32 * t;
-      mv[t] = c < cal && c <= r && S.M[r][c];
-      lv[t] = mv[t] ? S.L[r][c] : -INFINITY;
+    for (int i = 0; i < kR; ++i) {
+      const int r = wid + kWarps * i;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int c = lane + 32 * t;
+        mv[i][t] = r < cal && c < cal && in_mask(r, c);
+        lv[i][t] = mv[i][t] ? S.L[r][c] : -INFINITY;
+      }
+      mx[i] = fmaxf(lv[i][0], lv[i][1]);
     }
-    const float mx = warp_max(fmaxf(lv[0], lv[1]));
-    float ev[2];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) ev[t] = mv[t] ? expf(lv[t] - mx) : 0.f;
-    const float sum = warp_sum(ev[0] + ev[1]);
+    for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int c = lane + 32 * t;
-      if (c < cal) {
-        const float w = mv[t] ? ev[t] / sum : 0.f;
-        const double dlt = (double)w - (double)S.Wd[r][c];
-        part += dlt * dlt;
+      for (int i = 0; i < kR; ++i) mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) ev[i][t] = mv[i][t] ? expf(lv[i][t] - mx[i]) : 0.f;
+      sm[i] = ev[i][0] + ev[i][1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < kR; ++i) sm[i] += __shfl_xor_sync(0xffffffffu, sm[i], o);
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      const int r = wid + kWarps * i;
+      if (r < cal) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int c = lane + 32 * t;
+          if (c < cal) {
+            const float w = mv[i][t] ? ev[i][t] / sm[i] : 0.f;
+            const double dlt = (double)w - (double)S.Wd[r][c];
+            part += dlt * dlt;
+          }
+        }
       }
     }
   }
