@@ -618,3 +618,27 @@ def test_sparse_rejects_non_causal(sa):
     m = sa.AttnMatrices(m.q, m.k, m.v, causal=False)
     with pytest.raises(sa.PatternParamError):
         sa.vertical_slash_attention(m, sa.SparseIndex(n=4))
+
+
+@pytest.mark.parametrize("target", ["q_block_head", "q_other_head", "k", "v"])
+@pytest.mark.parametrize("value", [float("nan"), float("inf")])
+def test_device_nonfinite_every_writer(sa, target, value):
+    """Device inputs: a Block-Cluster head's q rows are checked by its query
+    pooling, every other q row and k / v by the scan beside the attention
+    (prefill.cu); a NaN or Inf anywhere must raise (core.py:72-74)."""
+    H, HK, n = 32, 8, 4096
+    q, k, v = (torch.from_numpy(O.bf16_round(x)).bfloat16().cuda() for x in O.synth_qkv_gqa(0, n, H, HK, 128))
+    cfg = sa.ModelConfig(n_heads=H, d_model=H * 128, d_head=128, max_context=n)
+    fams = [type(hp.pattern).__name__ for hp in sa.prefill(q, k, v, cfg, mode="auto").plans[0]]
+    assert "BlockSparse" in fams and any(f != "BlockSparse" for f in fams), fams
+    if target == "q_block_head":
+        x, idx = q, (0, fams.index("BlockSparse"), 1234, 5)
+    elif target == "q_other_head":
+        x, idx = q, (0, next(i for i, f in enumerate(fams) if f != "BlockSparse"), n - 1, 127)
+    else:
+        x, idx = (k if target == "k" else v), (0, 3, 17, 64)
+    x[idx] = value
+    with pytest.raises(sa.NonFiniteError):
+        sa.prefill(q, k, v, cfg, mode="auto")
+    x[idx] = 0.0
+    sa.prefill(q, k, v, cfg, mode="auto")  # clean again: no stale flag
