@@ -535,9 +535,16 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   // 4. executed tiles + attention
   if ((rc = sa_build_tiles(&V.index, p.hh, n, V.tile_off, V.tile_cnt, V.tiles, stream))) return rc;
   mark(3);
-  // SA_SCAN_AT=2: the scan is queued here, ahead of the work-order kernel
-  // (queueing it after the attention launch measured 20 us slower)
-  if (chk && scan_at == 2 && (rc = fork_scan(true))) return rc;
+  // SA_SCAN_AT=2: the scan is forked after the work-order kernel, just ahead of
+  // the attention launch, so its short CTAs start once the attention's
+  // persistent CTAs (launched early through PDL) hold their SM slots (32K:
+  // 1.0952 vs 1.0934 ms forked before the work order, SA_SCAN_LATE=0; queueing
+  // it after the attention launch measured 20 us slower)
+  static const bool scan_late = [] {
+    const char* e = getenv("SA_SCAN_LATE");
+    return !(e && e[0] == '0');
+  }();
+  if (chk && scan_at == 2 && !(scan_late && !desc->stop_after_tiles) && (rc = fork_scan(true))) return rc;
   if (chk && (scan_at == 0 || desc->stop_after_tiles)) cudaStreamWaitEvent(st, chk->join2, 0);
   if (desc->stop_after_tiles) return SA_OK;
   // CTA order: auto layers mix heavy (VS, dense-like) and light (Block) heads,
@@ -563,6 +570,7 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   if (lpt && (rc = launch_order_work(V.tile_cnt, p.hh * p.nqt, p.nqt, work, n_work, st, p.nqt,
                                      sib ? H / HK : 1, counter)))
     return rc;
+  if (chk && scan_at == 2 && scan_late && (rc = fork_scan(true))) return rc;
   rc = launch_attn(B, H, HK, n, desc->scale, q, k, v, out, &V.index, V.tile_off, V.tile_cnt, V.tiles,
                    lpt ? work : nullptr, nullptr, st, desc->out_ld, counter, lpt ? n_work : nullptr, nullptr, 0,
                    lpt);
