@@ -699,9 +699,14 @@ static int launch_tail64(int batch, int heads, int kv_heads, int n, float scale,
   a.qrow0 = r_hi - 64;
   a.nkt = (r_hi + kTile - 1) / kTile;
   a.wave_units = tail_wave_units(n);
+  // fewest key tiles per CTA: a unit of a small launch (the auto layer's few
+  // VS heads) takes ceil(key tiles / 8) CTAs instead of one per key tile, so
+  // its CTAs leave SMs to the block GEMM beside it (32K auto layer 1.100 ->
+  // 1.090 ms with the side stream at top priority; all-VS layers, whose units
+  // fill the waves, unchanged).  SA_VS_MIN_TILES overrides, for A/B.
   static const int min_tiles = [] {
-    const char* e = getenv("SA_VS_MIN_TILES");  // A/B
-    const int v = e ? atoi(e) : 1;
+    const char* e = getenv("SA_VS_MIN_TILES");
+    const int v = e ? atoi(e) : 8;
     return v >= 1 ? v : 1;
   }();
   a.min_tiles = min_tiles;
