@@ -232,7 +232,8 @@ def refined_candidates(s: SearchSpace, n: int, d_h: int, cost_q_est: int):
 
 def _device_select(q, k, heads, kv_heads, n, scale, refined, batch=1):
     """Selector kernel on staged (B*H, n, 128) bf16 q / (B*HK, n, 128) k with
-    cal = n: returns (choice[HH] int32 cuda, errors[HH, MAX_CAND] float64 cuda)."""
+    cal = n: returns (choice[HH] int32 cuda, errors[HH, len(refined)] float64 cuda:
+    the written columns of the kernel's [HH, MAX_CAND] table)."""
     hh = batch * heads
     fam = (ctypes_int * _lib.MAX_CAND)()
     p1 = (ctypes_int * _lib.MAX_CAND)()
@@ -243,7 +244,7 @@ def _device_select(q, k, heads, kv_heads, n, scale, refined, batch=1):
     errs = torch.empty((hh, _lib.MAX_CAND), dtype=torch.float64, device=q.device)
     _lib.call("sa_select_windowed", batch, heads, kv_heads, n, n, scale, q.data_ptr(), k.data_ptr(),
               len(refined), fam, p1, p2, choice.data_ptr(), None, errs.data_ptr(), D.stream())
-    return choice, errs
+    return choice, errs[:, :len(refined)]
 
 
 import ctypes as _ct  # noqa: E402
