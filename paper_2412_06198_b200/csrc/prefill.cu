@@ -399,7 +399,15 @@ extern "C" int sa_prefill(const sa_prefill_desc* desc, const void* q, const void
   for (int c = 0; c < p.ncand; ++c)
     if (p.cand[c].family == SA_BLOCK_SPARSE) ++nblk, blk_c = c;
   SideStream* side = (overlap && p.any_block && (p.any_vs || nblk == 1)) ? side_stream() : nullptr;
-  const bool kpool_early = side && nblk == 1;
+  // Session 4: with the VS chain on a top-priority side stream and a 16 us
+  // selector, the key pooling goes after the selection on the caller's stream
+  // (32K layer 1.0835-1.0846 -> 1.0787-1.0821 ms); SA_KPOOL_EARLY=1 runs it on
+  // the side stream from the start, beside the selector, as before.
+  static const bool kpool_env = [] {
+    const char* e = getenv("SA_KPOOL_EARLY");
+    return e && e[0] == '1';
+  }();
+  const bool kpool_early = side && nblk == 1 && kpool_env;
   if (kpool_early) {
     cudaEventRecord(side->fork0, st);
     cudaStreamWaitEvent(side->s, side->fork0, 0);
